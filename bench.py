@@ -1,0 +1,357 @@
+#!/usr/bin/env python
+"""Benchmark: wire-scan depth reconstruction on B200 (BASELINE.json metric).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+One "step" = one daxm_reconstruct of the whole synthetic stack of the config
+(SURVEY.md §8(a) rows 3-6 in one kernel launch; the geometry pre-pass, row 2,
+is per plan and timed separately as `prepass_ms`).  For N > 1 (torchrun, one
+process per GPU, NCCL) every rank reconstructs its own detector row band --
+no data-path collective; the timed region is bracketed by a
+barrier + synchronize and the per-step time is the max over ranks.
+
+Inputs (13.4 GB per step at C4: 6.7 GB stack read + 6.7 GB output written)
+are far larger than the 126 MB L2, so no flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+UNIT = "pixel·wire-steps/s"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        v = float(json.load(open(p))["hbm_gbs"])
+        return v, "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def workload_config(cfg, noise, world, parallelism_rows):
+    return {
+        "workload": f"{cfg.name}: {cfg.description}",
+        "detector": f"{cfg.n}x{cfg.n}", "n_steps": cfg.n_steps, "n_bins": cfg.n_bins,
+        "depth_res_um": cfg.depth_res, "input_dtype": cfg.dtype, "edge": "leading", "pixel_model": "finite",
+        "stack_noise": noise, "geometry": "34-ID-E-like synthetic (SURVEY.md §8(d))",
+        "parallelism": f"row-sharded x{world} (no collective)", "rows_per_gpu": parallelism_rows,
+        "l2": "inputs larger than L2 (stack + output per step >> 126 MB); no flush",
+    }
+
+
+def cpu_oracle_rate(cfg, maps, g, noise, budget_s, max_pixels=1 << 20):
+    """Time the fp64 oracle (as it stands) on a random pixel sample of the workload."""
+    import numpy as np
+
+    import oracle
+    import synth
+    rng = np.random.default_rng(12345)
+    threads = oracle.max_threads()
+
+    def run(n):
+        js = rng.integers(0, cfg.n, n)
+        is_ = rng.integers(0, cfg.n, n)
+        ser = synth.pixel_series(maps, js, is_, cfg.dtype, noise=noise)
+        t0 = time.perf_counter()
+        oracle.reconstruct_pixels(g, js, is_, ser, n_threads=threads)
+        return time.perf_counter() - t0
+
+    n = 256
+    t = run(n)
+    while t < 0.5 and n < max_pixels:
+        n *= 4
+        t = run(n)
+    n = int(min(max_pixels, max(n, n * budget_s / max(t, 1e-6))))
+    t = run(n)
+    return n * cfg.n_steps / t, n, t, threads
+
+
+def run_reference(args):
+    """--impl reference: the fp64 CPU oracle (as it stands) on the box's host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    import synth
+    oracle.build()
+    cfg = synth.get_config(args.config)
+    noise = not cfg.sparse if args.noise is None else args.noise
+    g = synth.geometry(cfg)
+    maps = synth.make_maps(cfg)
+    rng = np.random.default_rng(99)
+    threads = oracle.max_threads()
+    # size each step to ~args.ref_step_s of CPU work
+    n = 512
+    while True:
+        js, is_ = rng.integers(0, cfg.n, n), rng.integers(0, cfg.n, n)
+        ser = synth.pixel_series(maps, js, is_, cfg.dtype, noise=noise)
+        t0 = time.perf_counter()
+        oracle.reconstruct_pixels(g, js, is_, ser, n_threads=threads)
+        t = time.perf_counter() - t0
+        if t > 0.3 or n >= 1 << 20:
+            break
+        n *= 4
+    n = int(max(256, min(1 << 20, n * args.ref_step_s / max(t, 1e-6))))
+    times = []
+    for s in range(args.warmup + args.steps):
+        js, is_ = rng.integers(0, cfg.n, n), rng.integers(0, cfg.n, n)
+        ser = synth.pixel_series(maps, js, is_, cfg.dtype, noise=noise)
+        t0 = time.perf_counter()
+        oracle.reconstruct_pixels(g, js, is_, ser, n_threads=threads)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    step_s = sum(times) / len(times)
+    value = n * cfg.n_steps / step_s
+    sample = f"{n} random pixels x {cfg.n_steps} steps of {cfg.name} per step (fp64 oracle, all host threads)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(cfg, noise, 1, cfg.n),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--noise", type=int, default=None, help="stack noise (default: on, except the sparse C5)")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=12.0)
+    ap.add_argument("--ref-step-s", type=float, default=3.0)
+    ap.add_argument("--all-gather", action="store_true", help="also time an NCCL all-gather of the output planes")
+    args = ap.parse_args()
+    if args.noise is not None:
+        args.noise = bool(args.noise)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2201_13309_b200 as daxm
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = synth.get_config(args.config)
+    noise = (not cfg.sparse) if args.noise is None else args.noise
+    g = synth.geometry(cfg)
+    R = cfg.n
+    r0, r1 = rank * R // world, (rank + 1) * R // world
+    maps = synth.make_maps(cfg)
+    stack = synth.stack_torch(maps, cfg.dtype, dev, noise=noise, rows=(r0, r1))
+    plan = daxm.create(g, device=local, rows=(r0, r1))
+    st = plan.stats()
+    out = torch.empty(plan.output_shape(), dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    b_in = 2 if cfg.dtype == "u16" else 4
+
+    # warm-up
+    for _ in range(args.warmup):
+        plan.reconstruct(stack, out, stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        t_start.record(stream)
+        for s in range(K):
+            ev[s][0].record(stream)
+            plan.reconstruct(stack, out, stream)
+            ev[s][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    kern_ms = [a.elapsed_time(b) for a, b in ev]
+    kern_avg = sum(kern_ms) / len(kern_ms)
+    alg_bytes = (st["contrib_pairs"] + st["contrib_pixels"]) * b_in + st["rows"] * st["cols"] * st["n_bins"] * 4
+    achieved = alg_bytes / (kern_avg * 1e-3) / 1e9
+    ms_step = total_ms / K
+    stats = torch.tensor([ms_step, kern_avg, -achieved], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+    ms_step_max, kern_max, achieved_min = stats[0].item(), stats[1].item(), -stats[2].item()
+    units = R * cfg.n * cfg.n_steps
+    value = units / (ms_step_max * 1e-3)
+
+    # optional all-gather of the output planes (timed separately, not in value)
+    allgather_ms = None
+    if args.all_gather and world > 1 and R % world == 0:
+        gathered = torch.empty((world,) + tuple(out.shape), dtype=out.dtype, device=dev)
+        dist.all_gather_into_tensor(gathered, out)
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        a.record(stream)
+        dist.all_gather_into_tensor(gathered, out)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        allgather_ms = a.elapsed_time(b)
+        del gathered
+
+    # end to end through the C ABI from pinned host buffers (copies inside the timed region)
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, K // 4)
+    h_stack = stack.cpu().pin_memory()
+    h_out = torch.empty(plan.output_shape(), dtype=torch.float32).pin_memory()
+    del stack
+    torch.cuda.empty_cache()
+    plan.reconstruct_host(h_stack, h_out, stream)  # warm (allocates the plan's device buffers)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_a.record(stream)
+    for _ in range(e2e_steps):
+        plan.reconstruct_host(h_stack, h_out, stream)
+    e_b.record(stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = torch.tensor([e_a.elapsed_time(e_b) / e2e_steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = units / (e2e_ms.item() * 1e-3)
+    h2d = h_stack.numel() * h_stack.element_size() * world
+    d2h = h_out.numel() * h_out.element_size() * world
+
+    if rank == 0:
+        peak, peak_src = peak_hbm()
+        traffic = None
+        prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(prof):
+            try:
+                tj = json.load(open(prof))
+                key = f"{cfg.name}:{world}"
+                if key in tj:
+                    traffic = tj[key]["dram_bytes_per_launch"]
+            except Exception:
+                traffic = None
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                rate, n_pix, t_s, cores = cpu_oracle_rate(cfg, maps, g, noise, args.cpu_budget_s)
+                cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
+                       "sample": f"{n_pix} random pixels x {cfg.n_steps} steps of {cfg.name} ({t_s:.1f} s, fp64 "
+                                 f"C oracle, OpenMP over pixels)"}
+            except Exception as e:  # reported, not fatal
+                cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
+            "ms_per_step": ms_step_max, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": workload_config(cfg, noise, world, r1 - r0),
+            "roofline": {"bound": "hbm", "achieved": achieved_min, "peak": peak, "unit": "GB/s",
+                         "frac": achieved_min / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "deposit (daxm_reconstruct)", "kernel_ms": kern_max,
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "bytes_rule": "sum_p (S_c(p)+1)*b_in + rows*C*M*4 (SURVEY.md §8(d))"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": e2e_ms.item(), "path": "daxm_reconstruct_host, pinned host buffers"},
+            "cpu_baseline": cpu,
+            "gpu_launches": K * world,
+            "clocks": clocks.summary(),
+            "prepass_ms": st["prepass_ms"],
+            "plan": {"contrib_pairs": st["contrib_pairs"], "window_pairs": st["window_pairs"],
+                     "staged_steps": st["staged_steps"], "fit_max_err_bins": st["fit_max_err_bins"],
+                     "fit_model_err_bins": st["fit_model_err_bins"]},
+        }
+        if allgather_ms is not None:
+            line["all_gather_ms"] = allgather_ms
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

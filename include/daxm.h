@@ -1,0 +1,150 @@
+/*
+ * daxm.h -- C ABI of the B200 (sm_100a) wire-scan depth reconstruction library
+ * (differential-aperture X-ray microscopy, "DAXM"; arXiv:2201.13309).
+ *
+ * The method (Fig. 6 P:L304-349 and Fig. 7): for every
+ * detector pixel and every pair of consecutive wire steps k, k+1, take the
+ * intensity difference dI = I_k - I_{k+1}; ray-trace
+ * from the pixel's two edges, tangent to the wire edge, to the incident beam
+ * ("depth is measured along the incident beam from the origin"),
+ * which gives four corner depths of a trapezoidal depth response
+ * (device_get_trapezoid_height); distribute dI over the fixed
+ * depth bins (device_index_to_beam_depth P:L330/P:L344-345) in proportion to the
+ * trapezoid area inside each bin (device_depth_resolve_pixel).
+ * The result is one image per depth bin (image_set.depth_resolved).
+ * Conventions the paper leaves open are fixed in DESIGN.md "Readings" (R1-R13)
+ * and are identical to the CPU oracle's.
+ *
+ * Calls (all return daxm_status; no exceptions cross the ABI):
+ *   daxm_create        geometry -> plan (validates, runs the fp64 geometry
+ *                      pre-pass on the GPU, caches per-pixel windows and
+ *                      per-edge-point depth polynomials in device memory)
+ *   daxm_reconstruct   device stack [S][rows][C] -> device output [M][rows][C]
+ *                      (stream-ordered, asynchronous, allocates nothing,
+ *                      CUDA-graph capturable)
+ *   daxm_reconstruct_host  the same from/to HOST buffers (copies included)
+ *   daxm_plan_info / daxm_plan_stats / daxm_last_error / daxm_status_string
+ *   daxm_destroy
+ */
+#ifndef DAXM_H_
+#define DAXM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DAXM_ABI_VERSION 1
+
+typedef struct daxm_plan daxm_plan; /* opaque; owned by the library */
+
+typedef enum {
+    DAXM_OK = 0,
+    DAXM_ERR_INVALID_ARGUMENT = 1, /* bad sizes/enums/NaN/null pointers (see daxm_create)          */
+    DAXM_ERR_NONMONOTONE_SCAN = 2, /* wire travel or a pixel's depth-vs-step not monotone           */
+    DAXM_ERR_GEOMETRY = 3,         /* non-collinear wire path, NaN depth inside a window, depth
+                                      model (cubic) error above tolerance, or no valid pixel          */
+    DAXM_ERR_OUT_OF_MEMORY = 4,
+    DAXM_ERR_CUDA = 5              /* any CUDA runtime error; detail in daxm_last_error()            */
+} daxm_status;
+
+typedef enum { DAXM_EDGE_LEADING = 0, DAXM_EDGE_TRAILING = 1 } daxm_edge;
+typedef enum {
+    DAXM_PIXEL_FINITE = 0, /* pixel of finite width along the column axis: trapezoid (the paper)   */
+    DAXM_PIXEL_POINT = 1   /* pixel centre only: box response                                       */
+} daxm_pixel_model;
+typedef enum { DAXM_U16 = 0, DAXM_F32 = 1 } daxm_dtype;
+
+/* Geometry (all lengths in um, lab frame).  Passed by pointer; copied. */
+typedef struct {
+    int32_t n_rows, n_cols;         /* full detector R x C; image layout [row][col], col fastest        */
+    int32_t row_begin, row_end;     /* this plan's row band [begin, end) (0, R = whole detector)        */
+    double pitch_col, pitch_row;    /* um per pixel along x' (col) and y' (row)                          */
+    double det_rot[3];              /* Rodrigues vector (rad): |R| = angle, R/|R| = axis                 */
+    double det_trans[3];            /* lab = rho * ((x', y', 0) + det_trans);                            */
+                                    /* pixel centre (i, j): x' = (i-(C-1)/2) pitch_col, y' likewise      */
+    double beam_dir[3];             /* incident beam direction k-hat (normalised by the library)         */
+    double beam_origin[3];          /* depth origin O: depth D is the point O + D k-hat                  */
+    double wire_axis[3];            /* wire axis a-hat (normalised by the library)                       */
+    double wire_radius;             /* r > 0                                                             */
+    int32_t n_steps;                /* S >= 2 wire steps                                                 */
+    const double *wire_xyz;         /* host pointer, S x 3 wire-centre positions (copied at create);    */
+                                    /* must be collinear (perpendicular to a-hat) and monotone           */
+    double depth_start, depth_end;  /* centres of the first / last depth bin                             */
+    double depth_res;               /* bin width dz > 0; M = round((end-start)/dz) + 1 bins,            */
+                                    /* bin m covers [start + (m-1/2) dz, start + (m+1/2) dz)             */
+    int32_t edge;                   /* daxm_edge: which wire edge the tangent touches                    */
+    int32_t pixel_model;            /* daxm_pixel_model                                                  */
+} daxm_geometry;
+
+/* Per-plan statistics (for roofline accounting and tests). */
+typedef struct {
+    int64_t n_bins, rows, cols, n_steps; /* M, rows in band, C, S                                       */
+    int64_t contrib_pairs;     /* sum over band pixels of step pairs whose trapezoid overlaps the bins   */
+                               /* (S_c, exact fp64; the algorithmic read count per pixel is S_c + 1)      */
+    int64_t contrib_pixels;    /* band pixels with S_c > 0                                               */
+    int64_t window_pairs;      /* pairs the deposit kernel visits (S_c plus one guard pair each side)     */
+    int64_t staged_steps;      /* sum over band tiles of steps the deposit kernel streams for the tile    */
+    int64_t n_tiles;           /* deposit tiles covering the band                                         */
+    int32_t tile_rows, tile_cols;
+    double fit_max_err_bins;   /* max |fp32-stored cubic (fp32 tau) - exact fp64 depth| over every edge  */
+                               /* point and every step the kernel can read, in bins (<= 1e-3 enforced)    */
+    double fit_model_err_bins; /* the same for the fp64 cubic: approximation error (<= 1e-6 enforced)     */
+    double prepass_ms;         /* GPU time of the geometry pre-pass                                       */
+    int64_t device_bytes;      /* device memory owned by the plan                                         */
+} daxm_plan_stats;
+
+/* daxm_create -- validate `g`, run the fp64 geometry pre-pass on `cuda_device`,
+ * return a plan in *out (NULL on error).
+ *   INVALID_ARGUMENT: g/out NULL; S < 2; R, C < 1 or band outside [0, R) or empty;
+ *     pitch, r or dz <= 0 or non-finite; depth_end < depth_start; (end-start)/dz
+ *     not an integer within 1e-6; zero-length or non-finite beam/axis vectors;
+ *     any non-finite input; beam parallel to the axis; unknown enum value;
+ *     wire_xyz NULL.
+ *   NONMONOTONE_SCAN: projected wire travel decreases anywhere, all positions
+ *     equal, or a pixel edge's depth is not monotone in the step index.
+ *   GEOMETRY: wire centres off a straight line by > 1e-6 um (+1e-9 relative);
+ *     NaN tangent depth inside a pixel's contributing window; cubic depth
+ *     model error > 1e-6 bins (fp64) or > 1e-3 bins (as stored in fp32).
+ *   OUT_OF_MEMORY / CUDA: allocation or runtime failure.
+ * The calling thread's current device is restored before returning. */
+daxm_status daxm_create(const daxm_geometry *g, int cuda_device, daxm_plan **out);
+
+/* M, rows in the plan's band, C.  Any output pointer may be NULL. */
+daxm_status daxm_plan_info(const daxm_plan *p, int64_t *n_bins, int64_t *rows, int64_t *cols);
+daxm_status daxm_plan_stats_get(const daxm_plan *p, daxm_plan_stats *st);
+
+/* daxm_reconstruct -- d_stack: device pointer, [S][rows][C] of `dt`, rows = the
+ * plan's band (row_end - row_begin), C contiguous, 16-byte aligned.
+ * d_out: device pointer, [M][rows][C] float32, fully overwritten (zeros
+ * included), 16-byte aligned.  cuda_stream: cudaStream_t (NULL = legacy
+ * default stream).  Asynchronous; no allocation; graph-capturable.  Caller
+ * owns both buffers; they must stay valid until the stream reaches the work.
+ * Errors: INVALID_ARGUMENT (NULL pointers, misalignment, unknown dtype), CUDA
+ * (launch failure; detail in daxm_last_error). */
+daxm_status daxm_reconstruct(daxm_plan *p, const void *d_stack, daxm_dtype dt, float *d_out, void *cuda_stream);
+
+/* daxm_reconstruct_host -- end-to-end path from HOST memory: copies h_stack
+ * ([S][rows][C] of dt) to device buffers owned by the plan (allocated on first
+ * use), reconstructs, copies the result to h_out ([M][rows][C] float32) and
+ * synchronises `cuda_stream`.  Pinned host buffers give full PCIe/C2C speed;
+ * pageable buffers work too. */
+daxm_status daxm_reconstruct_host(daxm_plan *p, const void *h_stack, daxm_dtype dt, float *h_out,
+                                  void *cuda_stream);
+
+/* Detail text for the last failing call on this plan ("" if none).  Valid until
+ * the next call on the plan. */
+const char *daxm_last_error(const daxm_plan *p);
+/* Detail text of the last daxm_create failure on the calling thread. */
+const char *daxm_create_error(void);
+const char *daxm_status_string(daxm_status s);
+/* Frees all plan-owned device memory (synchronises the device first).  NULL is a no-op. */
+void daxm_destroy(daxm_plan *p);
+int daxm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DAXM_H_ */

@@ -1,0 +1,197 @@
+"""ctypes binding of libdaxm.so (include/daxm.h) -- argument marshalling only.
+
+Names follow the C ABI: ``create`` -> daxm_create, ``Plan.reconstruct`` ->
+daxm_reconstruct (device tensors, torch's current stream),
+``Plan.reconstruct_host`` -> daxm_reconstruct_host (host arrays).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libdaxm.so")
+
+EDGE = {"leading": 0, "trailing": 1}
+PIXEL_MODEL = {"finite": 0, "point": 1}
+DTYPE = {"u16": 0, "f32": 1}
+
+STATUS = {0: "ok", 1: "invalid argument", 2: "non-monotone scan", 3: "geometry error", 4: "out of memory",
+          5: "CUDA error"}
+
+
+class DaxmError(RuntimeError):
+    def __init__(self, status: int, detail: str):
+        super().__init__(f"{STATUS.get(status, status)}: {detail}")
+        self.status = status
+        self.detail = detail
+
+
+class Geometry(C.Structure):
+    _fields_ = [
+        ("n_rows", C.c_int32), ("n_cols", C.c_int32), ("row_begin", C.c_int32), ("row_end", C.c_int32),
+        ("pitch_col", C.c_double), ("pitch_row", C.c_double),
+        ("det_rot", C.c_double * 3), ("det_trans", C.c_double * 3),
+        ("beam_dir", C.c_double * 3), ("beam_origin", C.c_double * 3),
+        ("wire_axis", C.c_double * 3), ("wire_radius", C.c_double),
+        ("n_steps", C.c_int32), ("wire_xyz", C.POINTER(C.c_double)),
+        ("depth_start", C.c_double), ("depth_end", C.c_double), ("depth_res", C.c_double),
+        ("edge", C.c_int32), ("pixel_model", C.c_int32),
+    ]
+
+
+class PlanStats(C.Structure):
+    _fields_ = [
+        ("n_bins", C.c_int64), ("rows", C.c_int64), ("cols", C.c_int64), ("n_steps", C.c_int64),
+        ("contrib_pairs", C.c_int64), ("contrib_pixels", C.c_int64), ("window_pairs", C.c_int64), ("staged_steps", C.c_int64), ("n_tiles", C.c_int64),
+        ("tile_rows", C.c_int32), ("tile_cols", C.c_int32),
+        ("fit_max_err_bins", C.c_double), ("fit_model_err_bins", C.c_double), ("prepass_ms", C.c_double), ("device_bytes", C.c_int64),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdaxm.so (fails loudly if it was not built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(_LIB_PATH)
+        P = C.c_void_p
+        L.daxm_create.argtypes = [C.POINTER(Geometry), C.c_int, C.POINTER(P)]
+        L.daxm_create.restype = C.c_int
+        L.daxm_plan_info.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.daxm_plan_info.restype = C.c_int
+        L.daxm_plan_stats_get.argtypes = [P, C.POINTER(PlanStats)]
+        L.daxm_plan_stats_get.restype = C.c_int
+        L.daxm_reconstruct.argtypes = [P, P, C.c_int, P, P]
+        L.daxm_reconstruct.restype = C.c_int
+        L.daxm_reconstruct_host.argtypes = [P, P, C.c_int, P, P]
+        L.daxm_reconstruct_host.restype = C.c_int
+        L.daxm_last_error.argtypes = [P]
+        L.daxm_last_error.restype = C.c_char_p
+        L.daxm_create_error.restype = C.c_char_p
+        L.daxm_status_string.argtypes = [C.c_int]
+        L.daxm_status_string.restype = C.c_char_p
+        L.daxm_destroy.argtypes = [P]
+        L.daxm_destroy.restype = None
+        L.daxm_abi_version.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def abi_version() -> int:
+    return lib().daxm_abi_version()
+
+
+def _v3(x):
+    return (C.c_double * 3)(*[float(v) for v in x])
+
+
+def make_geometry(g: dict, rows: tuple | None = None):
+    """dict (synth.geometry format) -> (Geometry struct, keep-alive array)."""
+    wire = np.ascontiguousarray(np.asarray(g["wire_xyz"], dtype=np.float64).reshape(-1, 3))
+    r0, r1 = rows if rows is not None else (0, int(g["n_rows"]))
+    s = Geometry(int(g["n_rows"]), int(g["n_cols"]), int(r0), int(r1), float(g["pitch_col"]), float(g["pitch_row"]),
+                 _v3(g["det_rot"]), _v3(g["det_trans"]), _v3(g["beam_dir"]), _v3(g["beam_origin"]),
+                 _v3(g["wire_axis"]), float(g["wire_radius"]), int(wire.shape[0]),
+                 wire.ctypes.data_as(C.POINTER(C.c_double)), float(g["depth_start"]), float(g["depth_end"]),
+                 float(g["depth_res"]), EDGE.get(g.get("edge", "leading"), g.get("edge")),
+                 PIXEL_MODEL.get(g.get("pixel_model", "finite"), g.get("pixel_model")))
+    return s, wire
+
+
+class Plan:
+    """Owns a daxm_plan*.  Use ``create(geometry_dict, device, rows)``."""
+
+    def __init__(self, handle: int, device: int):
+        self._h = C.c_void_p(handle)
+        self.device = device
+        M, R, Cc = C.c_int64(), C.c_int64(), C.c_int64()
+        lib().daxm_plan_info(self._h, C.byref(M), C.byref(R), C.byref(Cc))
+        self.n_bins, self.rows, self.cols = M.value, R.value, Cc.value
+
+    def _check(self, st: int):
+        if st != 0:
+            raise DaxmError(st, lib().daxm_last_error(self._h).decode())
+
+    def stats(self) -> dict:
+        s = PlanStats()
+        self._check(lib().daxm_plan_stats_get(self._h, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in PlanStats._fields_}
+
+    def output_shape(self):
+        return (self.n_bins, self.rows, self.cols)
+
+    def reconstruct(self, stack, out=None, stream=None):
+        """stack: CUDA tensor [S][rows][C] uint16 or float32 -> out [M][rows][C] float32 (CUDA)."""
+        import torch
+        if not (stack.is_cuda and stack.is_contiguous()):
+            raise ValueError("stack must be a contiguous CUDA tensor")
+        dt = {torch.uint16: 0, torch.float32: 1}.get(stack.dtype)
+        if dt is None:
+            raise ValueError(f"unsupported stack dtype {stack.dtype}")
+        if out is None:
+            out = torch.empty(self.output_shape(), dtype=torch.float32, device=stack.device)
+        if not (out.is_cuda and out.is_contiguous() and out.dtype == torch.float32 and
+                tuple(out.shape) == self.output_shape()):
+            raise ValueError("out must be a contiguous float32 CUDA tensor of shape [M][rows][C]")
+        if stream is None:
+            stream = torch.cuda.current_stream(stack.device)
+        self._check(lib().daxm_reconstruct(self._h, C.c_void_p(stack.data_ptr()), dt, C.c_void_p(out.data_ptr()),
+                                           C.c_void_p(stream.cuda_stream)))
+        return out
+
+    def reconstruct_host(self, stack, out=None, stream=None):
+        """Host (numpy or pinned CPU torch) stack -> host output, copies included (daxm_reconstruct_host)."""
+        import torch
+        if isinstance(stack, np.ndarray):
+            stack = torch.from_numpy(np.ascontiguousarray(stack))
+        dt = {torch.uint16: 0, torch.float32: 1}.get(stack.dtype)
+        if dt is None or stack.is_cuda or not stack.is_contiguous():
+            raise ValueError("stack must be a contiguous host uint16/float32 tensor or array")
+        if out is None:
+            out = torch.empty(self.output_shape(), dtype=torch.float32, pin_memory=stack.is_pinned())
+        st = 0 if stream is None else stream.cuda_stream
+        self._check(lib().daxm_reconstruct_host(self._h, C.c_void_p(stack.data_ptr()), dt,
+                                                C.c_void_p(out.data_ptr()), C.c_void_p(st)))
+        return out
+
+    def close(self):
+        if self._h is not None and self._h.value:
+            lib().daxm_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+def create(g: dict, device: int = 0, rows: tuple | None = None) -> Plan:
+    s, keep = make_geometry(g, rows)
+    h = C.c_void_p()
+    st = lib().daxm_create(C.byref(s), int(device), C.byref(h))
+    del keep
+    if st != 0:
+        raise DaxmError(st, lib().daxm_create_error().decode())
+    return Plan(h.value, device)
+
+
+def reconstruct(plan: Plan, stack, out=None, stream=None):
+    return plan.reconstruct(stack, out, stream)
+
+
+def reconstruct_host(plan: Plan, stack, out=None, stream=None):
+    return plan.reconstruct_host(stack, out, stream)

@@ -1,0 +1,733 @@
+// plan.cu -- C ABI entry points, validation and the fp64 geometry pre-pass.
+//
+// Pre-pass (paper: device_pixel_xyz_to_depth,
+// P:L306-319, called four times per thread in setTwo):
+//   pixel_window_kernel  per pixel: exact fp64 tangent depths of both pixel
+//                        edges at every wire step -> the window of step pairs
+//                        whose trapezoid overlaps the bin range, the depth
+//                        direction, monotonicity and NaN checks;
+//   tile_kernel          per 32x32 tile: union step range and t_ref;
+//   fit_kernel           per tile edge point: cubic in wire travel about t_ref
+//                        (Chebyshev interpolation, fp64), stored fp32 in bin
+//                        units, verified against the exact depth at every step
+//                        the deposit kernel can read.
+// The deposit kernel then evaluates corner depths with 3 FMAs instead of the
+// paper's per-thread trig.
+#include <cuda_runtime.h>
+#include <limits.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <new>
+#include <string>
+#include <vector>
+
+#include "daxm.h"
+#include "daxm_internal.cuh"
+
+using namespace daxm;
+
+struct daxm_plan {
+    int device = 0;
+    daxm_geometry g{};
+    std::vector<double> wire;
+    std::vector<double> t;        // wire travel t_k
+    GeomConst gc{};
+    int M = 0, rows = 0, C = 0, S = 0;
+    int pre_row0 = 0, pre_rows = 0;   // global rows covered by the plan's tiles
+    int tr0 = 0, n_tr = 0, n_tc = 0;
+    double* d_t = nullptr;
+    double* d_wire = nullptr;
+    TileInfo* d_tiles = nullptr;
+    int2* d_win = nullptr;
+    float* d_coef = nullptr;
+    signed char* d_pdir = nullptr;
+    // end-to-end (host buffer) path scratch, allocated on first use
+    void* d_stack_buf = nullptr;
+    size_t stack_buf_bytes = 0;
+    float* d_out_buf = nullptr;
+    size_t out_buf_bytes = 0;
+    daxm_plan_stats stats{};
+    std::string err;
+};
+
+static thread_local std::string g_create_err;
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// ------------------------------------------------------------ fp64 geometry
+__device__ __forceinline__ double dot3(const double* a, const double* b) {
+    return a[0] * b[0] + a[1] * b[1] + a[2] * b[2];
+}
+
+// Lab position of detector point (column coordinate x, row j).
+__device__ void detector_point(const GeomConst& g, double x, int j, double Q[3]) {
+    double p0 = (x - 0.5 * (g.C - 1)) * g.pitch_col + g.trans[0];
+    double p1 = ((double)j - 0.5 * (g.R - 1)) * g.pitch_row + g.trans[1];
+    double p2 = g.trans[2];
+    for (int r = 0; r < 3; ++r) Q[r] = g.rho[3 * r] * p0 + g.rho[3 * r + 1] * p1 + g.rho[3 * r + 2] * p2;
+}
+
+// Edge side: +1 when (a x (Q - W0)).d >= 0 for the leading edge (reading R3).
+__device__ double edge_sigma(const GeomConst& g, const double Q[3]) {
+    double q[3] = {Q[0] - g.w0[0], Q[1] - g.w0[1], Q[2] - g.w0[2]};
+    double c[3] = {g.axis[1] * q[2] - g.axis[2] * q[1], g.axis[2] * q[0] - g.axis[0] * q[2],
+                   g.axis[0] * q[1] - g.axis[1] * q[0]};
+    double lead = dot3(c, g.d) >= 0.0 ? 1.0 : -1.0;
+    return g.edge ? -lead : lead;
+}
+
+// Tangent depth in bin units relative to m_ref: u = (D - lo0)/dz - m_ref.
+// D from the plane through Q tangent to the wire cylinder (contact normal n,
+// n.(Q-W) = r) intersected with the beam: D = (n.(W-O) + r)/(n.k).  NaN if the
+// pixel is inside the cylinder or the plane is parallel to the beam.
+__device__ double tangent_u(const GeomConst& g, const double Q[3], double sigma, const double W[3]) {
+    double qw[3] = {Q[0] - W[0], Q[1] - W[1], Q[2] - W[2]};
+    double pa = dot3(qw, g.axis);
+    double e[3] = {qw[0] - pa * g.axis[0], qw[1] - pa * g.axis[1], qw[2] - pa * g.axis[2]};
+    double L2 = dot3(e, e);
+    double r2 = g.r * g.r;
+    if (!(L2 > r2)) return nan("");
+    double s = sqrt(L2 - r2);
+    double ae[3] = {g.axis[1] * e[2] - g.axis[2] * e[1], g.axis[2] * e[0] - g.axis[0] * e[2],
+                    g.axis[0] * e[1] - g.axis[1] * e[0]};
+    double n[3];
+    for (int c = 0; c < 3; ++c) n[c] = (g.r * e[c] + sigma * s * ae[c]) / L2;
+    double nk = dot3(n, g.beam);
+    if (fabs(nk) < 1e-12) return nan("");
+    double wo[3] = {W[0] - g.origin[0], W[1] - g.origin[1], W[2] - g.origin[2]};
+    double D = (dot3(n, wo) + g.r) / nk;
+    return (D - g.lo0) / g.dz - (double)g.m_ref;
+}
+
+__device__ __forceinline__ void edge_point(const GeomConst& g, int j, int edge_col, double Q[3]) {
+    double x = g.point_mode ? (double)edge_col : (double)edge_col - 0.5;
+    detector_point(g, x, j, Q);
+}
+
+__device__ __forceinline__ void atomic_max_pos_double(double* addr, double v) {
+    // non-negative doubles order like their bit patterns
+    atomicMax(reinterpret_cast<unsigned long long*>(addr), (unsigned long long)__double_as_longlong(v));
+}
+
+// ------------------------------------------------------------ pixel windows
+__global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire, int pre_row0, int pre_rows,
+                                    int band_r0, int band_r1, int2* __restrict__ win,
+                                    signed char* __restrict__ pdir, unsigned* __restrict__ flags,
+                                    unsigned long long* __restrict__ counters) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int jl = blockIdx.y * blockDim.y + threadIdx.y;
+    if (i >= g.C || jl >= pre_rows) return;
+    const int j = pre_row0 + jl;
+    double Qb[3], Qf[3];
+    edge_point(g, j, i, Qb);
+    edge_point(g, j, g.point_mode ? i : i + 1, Qf);
+    const double sb = edge_sigma(g, Qb), sf = edge_sigma(g, Qf);
+    const double upper = (double)(g.M - g.m_ref), lower = (double)(-g.m_ref);
+
+    // pass 1: relevant pairs (trapezoid overlaps (0, M) bins), NaN bookkeeping
+    double ub0 = tangent_u(g, Qb, sb, wire), uf0 = tangent_u(g, Qf, sf, wire);
+    int first = -1, last = -1;
+    bool prev_nan = false, first_prev_nan = false, pending_nan = false, next_nan = false, nan_inside = false;
+    for (int k = 0; k + 1 < g.S; ++k) {
+        double ub1 = tangent_u(g, Qb, sb, wire + 3 * (k + 1)), uf1 = tangent_u(g, Qf, sf, wire + 3 * (k + 1));
+        bool isn = isnan(ub0) || isnan(uf0) || isnan(ub1) || isnan(uf1);
+        if (last >= 0 && k == last + 1) next_nan = isn;
+        if (!isn) {
+            double lo = fmin(fmin(ub0, uf0), fmin(ub1, uf1)), hi = fmax(fmax(ub0, uf0), fmax(ub1, uf1));
+            if (hi > lower && lo < upper) {
+                if (first < 0) {
+                    first = k;
+                    first_prev_nan = prev_nan;
+                }
+                if (pending_nan) nan_inside = true;
+                last = k;
+            }
+        } else if (first >= 0) {
+            pending_nan = true;
+        }
+        prev_nan = isn;
+        ub0 = ub1;
+        uf0 = uf1;
+    }
+    int2 w = make_int2(0, 0);
+    signed char dir = 0;
+    if (first >= 0) {
+        if (nan_inside) atomicOr(flags, FLAG_NAN_IN_WINDOW);
+        if (j >= band_r0 && j < band_r1) {
+            atomicAdd(&counters[2], (unsigned long long)(last - first + 1));
+            atomicAdd(&counters[3], 1ull);
+        }
+        int kb = first, ke = last + 1;  // pairs [kb, ke)
+        if (kb > 0 && !first_prev_nan) --kb;             // one guard pair each side (fp32 rounding)
+        if (ke <= g.S - 2 && !next_nan) ++ke;
+        // pass 2: monotonicity and direction over the window's points kb..ke
+        bool pos = false, neg = false;
+        double pb = tangent_u(g, Qb, sb, wire + 3 * kb), pf = tangent_u(g, Qf, sf, wire + 3 * kb);
+        for (int k = kb + 1; k <= ke; ++k) {
+            double cb = tangent_u(g, Qb, sb, wire + 3 * k), cf = tangent_u(g, Qf, sf, wire + 3 * k);
+            double db = cb - pb, df = cf - pf;
+            pos |= (db > 0.0) || (df > 0.0);
+            neg |= (db < 0.0) || (df < 0.0);
+            pb = cb;
+            pf = cf;
+        }
+        if (pos && neg) atomicOr(flags, FLAG_NONMONOTONE);
+        dir = neg ? -1 : 1;
+        w = make_int2(kb, ke);
+    }
+    win[(size_t)jl * g.C + i] = w;
+    pdir[(size_t)jl * g.C + i] = dir;
+}
+
+// ------------------------------------------------------------ tiles
+__global__ void tile_kernel(GeomConst g, const double* __restrict__ t, int pre_row0, int pre_rows, int tr0,
+                            int n_tc, int band_r0, int band_r1, const int2* __restrict__ win,
+                            const signed char* __restrict__ pdir, TileInfo* __restrict__ tiles,
+                            unsigned* __restrict__ flags, unsigned long long* __restrict__ counters) {
+    const int tile = blockIdx.x;
+    const int tr = tile / n_tc, tc = tile % n_tc;
+    const int r = threadIdx.y, c = threadIdx.x;  // 32 x 32
+    const int j = (tr0 + tr) * TILE_R + r, i = tc * TILE_C + c;
+    int kb = INT_MAX, ke = INT_MIN, dpos = 0, dneg = 0;
+    long long pairs = 0;
+    if (j < g.R && i < g.C && j >= pre_row0 && j < pre_row0 + pre_rows) {
+        int2 w = win[(size_t)(j - pre_row0) * g.C + i];
+        if (w.y > w.x) {
+            kb = w.x;
+            ke = w.y;  // last point read = ke
+            signed char d = pdir[(size_t)(j - pre_row0) * g.C + i];
+            dpos = d > 0;
+            dneg = d < 0;
+            if (j >= band_r0 && j < band_r1) pairs = w.y - w.x;
+        }
+    }
+    __shared__ int s_kb, s_ke, s_pos, s_neg;
+    __shared__ unsigned long long s_pairs;
+    if (r == 0 && c == 0) {
+        s_kb = INT_MAX;
+        s_ke = INT_MIN;
+        s_pos = 0;
+        s_neg = 0;
+        s_pairs = 0;
+    }
+    __syncthreads();
+    if (kb != INT_MAX) {
+        atomicMin(&s_kb, kb);
+        atomicMax(&s_ke, ke);
+        if (dpos) atomicOr(&s_pos, 1);
+        if (dneg) atomicOr(&s_neg, 1);
+        atomicAdd(&s_pairs, (unsigned long long)pairs);
+    }
+    __syncthreads();
+    if (r == 0 && c == 0) {
+        TileInfo ti;
+        ti.pad = 0;
+        if (s_kb == INT_MAX) {
+            ti.t_ref = 0.0;
+            ti.k_lo = 0;
+            ti.k_hi = -1;
+            ti.dir = 1;
+        } else {
+            ti.k_lo = s_kb;
+            ti.k_hi = s_ke;
+            ti.t_ref = 0.5 * (t[s_kb] + t[s_ke]);
+            ti.dir = s_neg ? -1 : 1;
+            if (s_pos && s_neg) atomicOr(flags, FLAG_MIXED_DIR);
+            // staged steps, only for tiles that intersect the band
+            int tj0 = (tr0 + tr) * TILE_R, tj1 = tj0 + TILE_R;
+            if (tj1 > band_r0 && tj0 < band_r1) atomicAdd(&counters[1], (unsigned long long)(s_ke - s_kb + 1));
+        }
+        tiles[tile] = ti;
+        atomicAdd(&counters[0], s_pairs);
+    }
+}
+
+// ------------------------------------------------------------ cubic fit
+__global__ void fit_kernel(GeomConst g, const double* __restrict__ t, const double* __restrict__ wire, int tr0,
+                           int n_tc, const TileInfo* __restrict__ tiles, float* __restrict__ coef,
+                           unsigned* __restrict__ flags, double* __restrict__ max_err) {
+    const int tile = blockIdx.x;
+    const int tr = tile / n_tc, tc = tile % n_tc;
+    const TileInfo ti = tiles[tile];
+    const int r = threadIdx.x;  // row in tile (32)
+    const int j = (tr0 + tr) * TILE_R + r;
+    double local_err = 0.0, local_model = 0.0;
+    for (int e = threadIdx.y; e < TILE_E; e += blockDim.y) {
+        const int eg = tc * TILE_C + e;  // global edge column
+        const int n_edges = g.point_mode ? g.C : g.C + 1;
+        float cf[NCOEF] = {0.f, 0.f, 0.f, 0.f};
+        if (ti.k_hi >= ti.k_lo && j < g.R && eg < n_edges) {
+            double Q[3];
+            edge_point(g, j, eg, Q);
+            const double sg = edge_sigma(g, Q);
+            const double h = 0.5 * (t[ti.k_hi] - t[ti.k_lo]);
+            double b[NCOEF] = {0, 0, 0, 0};
+            if (h > 0.0) {
+                // Chebyshev interpolation at the 4 first-kind nodes of [t_lo, t_hi]
+                double a[NCOEF] = {0, 0, 0, 0};
+                for (int n = 0; n < NCOEF; ++n) {
+                    const double th = M_PI * (2 * n + 1) / (2.0 * NCOEF);
+                    const double x = cos(th);
+                    const double tn = ti.t_ref + h * x;
+                    double W[3] = {g.w0[0] + tn * g.d[0], g.w0[1] + tn * g.d[1], g.w0[2] + tn * g.d[2]};
+                    const double u = tangent_u(g, Q, sg, W);
+                    if (isnan(u)) atomicOr(flags, FLAG_FIT_NAN);
+                    for (int m = 0; m < NCOEF; ++m) a[m] += u * cos(m * th);
+                }
+                for (int m = 0; m < NCOEF; ++m) a[m] *= (m == 0 ? 1.0 : 2.0) / NCOEF;
+                // Chebyshev -> monomial in x, then x = tau / h
+                const double bx[NCOEF] = {a[0] - a[2], a[1] - 3.0 * a[3], 2.0 * a[2], 4.0 * a[3]};
+                double hp = 1.0;
+                for (int m = 0; m < NCOEF; ++m) {
+                    b[m] = bx[m] / hp;
+                    hp *= h;
+                }
+            } else {
+                double W[3] = {g.w0[0] + ti.t_ref * g.d[0], g.w0[1] + ti.t_ref * g.d[1],
+                               g.w0[2] + ti.t_ref * g.d[2]};
+                b[0] = tangent_u(g, Q, sg, W);
+                if (isnan(b[0])) atomicOr(flags, FLAG_FIT_NAN);
+            }
+            for (int m = 0; m < NCOEF; ++m) cf[m] = (float)b[m];
+            // verify against the exact depth at every step the kernel can read:
+            //   model error  -- fp64 cubic (approximation quality, hard limit)
+            //   stored error -- what the kernel evaluates: fp32 coefficients, fp32 tau
+            for (int k = ti.k_lo; k <= ti.k_hi; ++k) {
+                const double ex = tangent_u(g, Q, sg, wire + 3 * k);
+                if (isnan(ex)) continue;
+                const double td = t[k] - ti.t_ref;
+                const double pm = b[0] + td * (b[1] + td * (b[2] + td * b[3]));
+                local_model = fmax(local_model, fabs(pm - ex));
+                const double tau = (double)(float)td;
+                const double p = (double)cf[0] + tau * ((double)cf[1] + tau * ((double)cf[2] + tau * (double)cf[3]));
+                local_err = fmax(local_err, fabs(p - ex));
+            }
+        }
+        for (int m = 0; m < NCOEF; ++m) coef[(((size_t)tile * NCOEF + m) * TILE_E + e) * TILE_R + r] = cf[m];
+    }
+    if (local_err > 0.0) atomic_max_pos_double(max_err, local_err);
+    if (local_model > 0.0) atomic_max_pos_double(max_err + 1, local_model);
+}
+
+daxm_status fail(daxm_plan* p, daxm_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (p)
+        p->err = buf;
+    else
+        g_create_err = buf;
+    return s;
+}
+
+bool finite3(const double* v) { return isfinite(v[0]) && isfinite(v[1]) && isfinite(v[2]); }
+double norm3(const double* v) { return sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]); }
+
+void rodrigues(const double R[3], double rho[9]) {
+    double th = norm3(R);
+    for (int i = 0; i < 9; ++i) rho[i] = (i % 4 == 0) ? 1.0 : 0.0;
+    if (th == 0.0) return;
+    double k[3] = {R[0] / th, R[1] / th, R[2] / th};
+    double K[9] = {0, -k[2], k[1], k[2], 0, -k[0], -k[1], k[0], 0};
+    double s = sin(th), c1 = 1.0 - cos(th);
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+            double k2 = 0;
+            for (int q = 0; q < 3; ++q) k2 += K[3 * r + q] * K[3 * q + c];
+            rho[3 * r + c] += s * K[3 * r + c] + c1 * k2;
+        }
+}
+
+void free_plan_memory(daxm_plan* p) {
+    cudaFree(p->d_t);
+    cudaFree(p->d_wire);
+    cudaFree(p->d_tiles);
+    cudaFree(p->d_win);
+    cudaFree(p->d_coef);
+    cudaFree(p->d_pdir);
+    cudaFree(p->d_stack_buf);
+    cudaFree(p->d_out_buf);
+    p->d_t = p->d_wire = nullptr;
+    p->d_tiles = nullptr;
+    p->d_win = nullptr;
+    p->d_coef = nullptr;
+    p->d_pdir = nullptr;
+    p->d_stack_buf = nullptr;
+    p->d_out_buf = nullptr;
+}
+
+#define CK(call)                                                                                  \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess) {                                                                  \
+            daxm_status s_ = e_ == cudaErrorMemoryAllocation ? DAXM_ERR_OUT_OF_MEMORY : DAXM_ERR_CUDA; \
+            fail(nullptr, s_, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);     \
+            cudaGetLastError();                                                                   \
+            return s_;                                                                            \
+        }                                                                                         \
+    } while (0)
+
+daxm_status host_prepare(daxm_plan* p) {
+    const daxm_geometry& g = p->g;
+    GeomConst& gc = p->gc;
+    // ---- host geometry: rotation, unit vectors, scan line
+    rodrigues(g.det_rot, gc.rho);
+    for (int c = 0; c < 3; ++c) gc.trans[c] = g.det_trans[c];
+    gc.pitch_col = g.pitch_col;
+    gc.pitch_row = g.pitch_row;
+    double na = norm3(g.wire_axis), nb = norm3(g.beam_dir);
+    for (int c = 0; c < 3; ++c) {
+        gc.axis[c] = g.wire_axis[c] / na;
+        gc.beam[c] = g.beam_dir[c] / nb;
+        gc.origin[c] = g.beam_origin[c];
+    }
+    const int S = g.n_steps;
+    const double* W = p->wire.data();
+    for (int c = 0; c < 3; ++c) gc.w0[c] = W[c];
+    std::vector<double> v(3 * (size_t)S);
+    for (int k = 0; k < S; ++k) {
+        double q[3] = {W[3 * k] - W[0], W[3 * k + 1] - W[1], W[3 * k + 2] - W[2]};
+        double pa = q[0] * gc.axis[0] + q[1] * gc.axis[1] + q[2] * gc.axis[2];
+        for (int c = 0; c < 3; ++c) v[3 * k + c] = q[c] - pa * gc.axis[c];
+    }
+    double dl = norm3(&v[3 * (S - 1)]);
+    if (!(dl > 0.0))
+        return fail(nullptr, DAXM_ERR_NONMONOTONE_SCAN, "first and last wire positions coincide (perpendicular to the axis)");
+    for (int c = 0; c < 3; ++c) gc.d[c] = v[3 * (S - 1) + c] / dl;
+    p->t.assign(S, 0.0);
+    for (int k = 0; k < S; ++k) {
+        double tk = v[3 * k] * gc.d[0] + v[3 * k + 1] * gc.d[1] + v[3 * k + 2] * gc.d[2];
+        double res[3] = {v[3 * k] - tk * gc.d[0], v[3 * k + 1] - tk * gc.d[1], v[3 * k + 2] - tk * gc.d[2]};
+        if (norm3(res) > 1e-6 + 1e-9 * fabs(tk))
+            return fail(nullptr, DAXM_ERR_GEOMETRY,
+                        "wire centre %d is %.3g um off the scan line (only straight scans are supported)", k,
+                        norm3(res));
+        p->t[k] = tk;
+        if (k > 0 && tk < p->t[k - 1])
+            return fail(nullptr, DAXM_ERR_NONMONOTONE_SCAN, "wire travel decreases between steps %d and %d", k - 1, k);
+    }
+    gc.r = g.wire_radius;
+    gc.dz = g.depth_res;
+    gc.lo0 = g.depth_start - 0.5 * g.depth_res;
+    gc.R = g.n_rows;
+    gc.C = g.n_cols;
+    gc.S = S;
+    gc.M = p->M;
+    gc.edge = g.edge;
+    gc.point_mode = g.pixel_model == DAXM_PIXEL_POINT;
+    gc.m_ref = p->M / 2;
+    return DAXM_OK;
+}
+
+daxm_status device_prepass(daxm_plan* p) {
+    const daxm_geometry& g = p->g;
+    GeomConst& gc = p->gc;
+    const int S = g.n_steps;
+    const double* W = p->wire.data();
+    // ---- tiling (global-aligned)
+    p->tr0 = g.row_begin / TILE_R;
+    const int tr1 = (g.row_end + TILE_R - 1) / TILE_R;
+    p->n_tr = tr1 - p->tr0;
+    p->n_tc = (g.n_cols + TILE_C - 1) / TILE_C;
+    p->pre_row0 = p->tr0 * TILE_R;
+    p->pre_rows = (tr1 * TILE_R < g.n_rows ? tr1 * TILE_R : g.n_rows) - p->pre_row0;
+    const size_t n_tiles = (size_t)p->n_tr * p->n_tc;
+
+    // ---- device allocations
+    CK(cudaMalloc(&p->d_t, sizeof(double) * S));
+    CK(cudaMalloc(&p->d_wire, sizeof(double) * 3 * S));
+    CK(cudaMalloc(&p->d_tiles, sizeof(TileInfo) * n_tiles));
+    CK(cudaMalloc(&p->d_win, sizeof(int2) * (size_t)p->pre_rows * g.n_cols));
+    CK(cudaMalloc(&p->d_pdir, (size_t)p->pre_rows * g.n_cols));
+    CK(cudaMalloc(&p->d_coef, sizeof(float) * n_tiles * NCOEF * TILE_E * TILE_R));
+    unsigned* d_flags = nullptr;
+    double* d_err = nullptr;
+    unsigned long long* d_cnt = nullptr;
+    CK(cudaMalloc(&d_flags, 64));
+    d_err = reinterpret_cast<double*>(reinterpret_cast<char*>(d_flags) + 8);
+    d_cnt = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(d_flags) + 24);
+    CK(cudaMemset(d_flags, 0, 64));
+    CK(cudaMemcpy(p->d_t, p->t.data(), sizeof(double) * S, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(p->d_wire, W, sizeof(double) * 3 * S, cudaMemcpyHostToDevice));
+
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, 0));
+    {
+        dim3 blk(128, 1), grd((g.n_cols + 127) / 128, p->pre_rows);
+        pixel_window_kernel<<<grd, blk>>>(gc, p->d_wire, p->pre_row0, p->pre_rows, g.row_begin, g.row_end,
+                                          p->d_win, p->d_pdir, d_flags, d_cnt);
+        CK(cudaGetLastError());
+        tile_kernel<<<(unsigned)n_tiles, dim3(TILE_C, TILE_R)>>>(gc, p->d_t, p->pre_row0, p->pre_rows, p->tr0,
+                                                                p->n_tc, g.row_begin, g.row_end, p->d_win,
+                                                                p->d_pdir, p->d_tiles, d_flags, d_cnt);
+        CK(cudaGetLastError());
+        fit_kernel<<<(unsigned)n_tiles, dim3(TILE_R, 8)>>>(gc, p->d_t, p->d_wire, p->tr0, p->n_tc, p->d_tiles,
+                                                          p->d_coef, d_flags, d_err);
+        CK(cudaGetLastError());
+    }
+    CK(cudaEventRecord(e1, 0));
+    CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    unsigned char hb[64];
+    CK(cudaMemcpy(hb, d_flags, 64, cudaMemcpyDeviceToHost));
+    cudaFree(d_flags);
+    unsigned flags;
+    double max_err, model_err;
+    unsigned long long cnt[4];
+    memcpy(&flags, hb, 4);
+    memcpy(&max_err, hb + 8, 8);
+    memcpy(&model_err, hb + 16, 8);
+    memcpy(cnt, hb + 24, 32);
+
+    daxm_plan_stats& st = p->stats;
+    st.n_bins = p->M;
+    st.rows = p->rows;
+    st.cols = g.n_cols;
+    st.n_steps = S;
+    st.window_pairs = (int64_t)cnt[0];
+    st.contrib_pairs = (int64_t)cnt[2];
+    st.contrib_pixels = (int64_t)cnt[3];
+    st.staged_steps = (int64_t)cnt[1];
+    st.n_tiles = (int64_t)n_tiles;
+    st.tile_rows = TILE_R;
+    st.tile_cols = TILE_C;
+    st.fit_max_err_bins = max_err;
+    st.fit_model_err_bins = model_err;
+    st.prepass_ms = ms;
+    st.device_bytes = (int64_t)(sizeof(double) * 4 * S + sizeof(TileInfo) * n_tiles +
+                                (sizeof(int2) + 1) * (size_t)p->pre_rows * g.n_cols +
+                                sizeof(float) * n_tiles * NCOEF * TILE_E * TILE_R);
+
+    if (flags & (FLAG_NONMONOTONE | FLAG_MIXED_DIR))
+        return fail(nullptr, DAXM_ERR_NONMONOTONE_SCAN,
+                    "a pixel edge's tangent depth is not monotone in the wire step inside its window (flags 0x%x)", flags);
+    if (flags & FLAG_NAN_IN_WINDOW)
+        return fail(nullptr, DAXM_ERR_GEOMETRY, "NaN tangent depth inside a pixel's contributing window");
+    if (flags & FLAG_FIT_NAN) return fail(nullptr, DAXM_ERR_GEOMETRY, "NaN tangent depth at a depth-model node");
+    if (!(model_err <= 1e-6))
+        return fail(nullptr, DAXM_ERR_GEOMETRY, "cubic depth model error %.3g bins exceeds 1e-6", model_err);
+    if (!(max_err <= 1e-3))
+        return fail(nullptr, DAXM_ERR_GEOMETRY, "fp32 depth model error %.3g bins exceeds 1e-3", max_err);
+    return DAXM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int daxm_abi_version(void) { return DAXM_ABI_VERSION; }
+
+const char* daxm_status_string(daxm_status s) {
+    switch (s) {
+        case DAXM_OK: return "ok";
+        case DAXM_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case DAXM_ERR_NONMONOTONE_SCAN: return "non-monotone scan";
+        case DAXM_ERR_GEOMETRY: return "geometry error";
+        case DAXM_ERR_OUT_OF_MEMORY: return "out of memory";
+        case DAXM_ERR_CUDA: return "CUDA error";
+    }
+    return "unknown status";
+}
+
+const char* daxm_create_error(void) { return g_create_err.c_str(); }
+
+const char* daxm_last_error(const daxm_plan* p) { return p ? p->err.c_str() : ""; }
+
+daxm_status daxm_create(const daxm_geometry* g, int cuda_device, daxm_plan** out) {
+    g_create_err.clear();
+    if (!out) return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    if (!g) return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "geometry is NULL");
+    if (g->n_steps < 2) return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "n_steps = %d < 2", g->n_steps);
+    if (g->n_rows < 1 || g->n_cols < 1)
+        return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "detector %d x %d", g->n_rows, g->n_cols);
+    if (g->row_begin < 0 || g->row_end > g->n_rows || g->row_begin >= g->row_end)
+        return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "row band [%d, %d) outside [0, %d)", g->row_begin, g->row_end,
+                    g->n_rows);
+    if (!g->wire_xyz) return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "wire_xyz is NULL");
+    if (!(isfinite(g->pitch_col) && g->pitch_col > 0 && isfinite(g->pitch_row) && g->pitch_row > 0))
+        return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "pixel pitch must be finite and > 0");
+    if (!finite3(g->det_rot) || !finite3(g->det_trans) || !finite3(g->beam_dir) || !finite3(g->beam_origin) ||
+        !finite3(g->wire_axis))
+        return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "non-finite geometry vector");
+    if (!(norm3(g->beam_dir) > 0) || !(norm3(g->wire_axis) > 0))
+        return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "zero-length beam or wire-axis vector");
+    if (!(isfinite(g->wire_radius) && g->wire_radius > 0))
+        return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "wire radius must be finite and > 0");
+    if (!(isfinite(g->depth_start) && isfinite(g->depth_end) && isfinite(g->depth_res) && g->depth_res > 0 &&
+          g->depth_end >= g->depth_start))
+        return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "depth range/resolution invalid");
+    const double nb = (g->depth_end - g->depth_start) / g->depth_res;
+    if (fabs(nb - nearbyint(nb)) > 1e-6 || nb > 1e7)
+        return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "(depth_end - depth_start)/depth_res = %.9g is not an integer",
+                    nb);
+    if (g->edge != DAXM_EDGE_LEADING && g->edge != DAXM_EDGE_TRAILING)
+        return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "unknown edge %d", g->edge);
+    if (g->pixel_model != DAXM_PIXEL_FINITE && g->pixel_model != DAXM_PIXEL_POINT)
+        return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "unknown pixel model %d", g->pixel_model);
+    for (int k = 0; k < 3 * g->n_steps; ++k)
+        if (!isfinite(g->wire_xyz[k])) return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "non-finite wire position");
+    {
+        const double* a = g->wire_axis;
+        const double* b = g->beam_dir;
+        double c[3] = {a[1] * b[2] - a[2] * b[1], a[2] * b[0] - a[0] * b[2], a[0] * b[1] - a[1] * b[0]};
+        if (norm3(c) < 1e-9 * norm3(a) * norm3(b))
+            return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "beam is parallel to the wire axis");
+    }
+    daxm_plan* p = new (std::nothrow) daxm_plan();
+    if (!p) return fail(nullptr, DAXM_ERR_OUT_OF_MEMORY, "host allocation failed");
+    p->device = cuda_device;
+    p->g = *g;
+    p->wire.assign(g->wire_xyz, g->wire_xyz + 3 * (size_t)g->n_steps);
+    p->g.wire_xyz = nullptr;
+    p->M = (int)nearbyint(nb) + 1;
+    p->rows = g->row_end - g->row_begin;
+    p->C = g->n_cols;
+    p->S = g->n_steps;
+    daxm_status s = host_prepare(p);  // scan line checks need no device
+    if (s == DAXM_OK) {
+        int n_dev = 0;
+        if (cudaGetDeviceCount(&n_dev) != cudaSuccess || cuda_device < 0 || cuda_device >= n_dev) {
+            cudaGetLastError();
+            s = fail(nullptr, DAXM_ERR_CUDA, "CUDA device %d not available (%d devices)", cuda_device, n_dev);
+        } else {
+            DeviceGuard guard(cuda_device);
+            s = device_prepass(p);
+            if (s != DAXM_OK) free_plan_memory(p);
+        }
+    }
+    if (s != DAXM_OK) {
+        delete p;
+        return s;
+    }
+    *out = p;
+    return DAXM_OK;
+}
+
+daxm_status daxm_plan_info(const daxm_plan* p, int64_t* n_bins, int64_t* rows, int64_t* cols) {
+    if (!p) return DAXM_ERR_INVALID_ARGUMENT;
+    if (n_bins) *n_bins = p->M;
+    if (rows) *rows = p->rows;
+    if (cols) *cols = p->C;
+    return DAXM_OK;
+}
+
+daxm_status daxm_plan_stats_get(const daxm_plan* p, daxm_plan_stats* st) {
+    if (!p || !st) return DAXM_ERR_INVALID_ARGUMENT;
+    *st = p->stats;
+    return DAXM_OK;
+}
+
+static DepositArgs make_args(const daxm_plan* p) {
+    DepositArgs a;
+    a.t = p->d_t;
+    a.tiles = p->d_tiles;
+    a.win = p->d_win;
+    a.coef = p->d_coef;
+    a.R = p->g.n_rows;
+    a.C = p->C;
+    a.S = p->S;
+    a.M = p->M;
+    a.row_begin = p->g.row_begin;
+    a.row_end = p->g.row_end;
+    a.pre_row0 = p->pre_row0;
+    a.tr0 = p->tr0;
+    a.n_tr = p->n_tr;
+    a.n_tc = p->n_tc;
+    a.m_ref = p->gc.m_ref;
+    a.point_mode = p->gc.point_mode;
+    a.sign = p->g.edge == DAXM_EDGE_TRAILING ? -1.f : 1.f;
+    return a;
+}
+
+daxm_status daxm_reconstruct(daxm_plan* p, const void* d_stack, daxm_dtype dt, float* d_out, void* cuda_stream) {
+    if (!p) return DAXM_ERR_INVALID_ARGUMENT;
+    p->err.clear();
+    if (!d_stack || !d_out) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "NULL stack or output pointer");
+    if (dt != DAXM_U16 && dt != DAXM_F32) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "unknown dtype %d", (int)dt);
+    if ((reinterpret_cast<uintptr_t>(d_stack) | reinterpret_cast<uintptr_t>(d_out)) & 15)
+        return fail(p, DAXM_ERR_INVALID_ARGUMENT, "stack and output must be 16-byte aligned");
+    DeviceGuard guard(p->device);
+    cudaError_t e = launch_deposit(make_args(p), d_stack, (int)dt, d_out, (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(p, DAXM_ERR_CUDA, "deposit launch: %s", cudaGetErrorString(e));
+    }
+    return DAXM_OK;
+}
+
+daxm_status daxm_reconstruct_host(daxm_plan* p, const void* h_stack, daxm_dtype dt, float* h_out, void* cuda_stream) {
+    if (!p) return DAXM_ERR_INVALID_ARGUMENT;
+    p->err.clear();
+    if (!h_stack || !h_out) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "NULL stack or output pointer");
+    if (dt != DAXM_U16 && dt != DAXM_F32) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "unknown dtype %d", (int)dt);
+    DeviceGuard guard(p->device);
+    const size_t plane = (size_t)p->rows * p->C;
+    const size_t in_bytes = plane * p->S * (dt == DAXM_U16 ? 2 : 4);
+    const size_t out_bytes = plane * p->M * sizeof(float);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    cudaError_t e = cudaSuccess;
+    if (p->stack_buf_bytes < in_bytes) {
+        cudaFree(p->d_stack_buf);
+        p->d_stack_buf = nullptr;
+        p->stack_buf_bytes = 0;
+        e = cudaMalloc(&p->d_stack_buf, in_bytes);
+        if (e != cudaSuccess) goto fail_cuda;
+        p->stack_buf_bytes = in_bytes;
+    }
+    if (p->out_buf_bytes < out_bytes) {
+        cudaFree(p->d_out_buf);
+        p->d_out_buf = nullptr;
+        p->out_buf_bytes = 0;
+        e = cudaMalloc(&p->d_out_buf, out_bytes);
+        if (e != cudaSuccess) goto fail_cuda;
+        p->out_buf_bytes = out_bytes;
+    }
+    e = cudaMemcpyAsync(p->d_stack_buf, h_stack, in_bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) goto fail_cuda;
+    e = launch_deposit(make_args(p), p->d_stack_buf, (int)dt, p->d_out_buf, st);
+    if (e != cudaSuccess) goto fail_cuda;
+    e = cudaMemcpyAsync(h_out, p->d_out_buf, out_bytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) goto fail_cuda;
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) goto fail_cuda;
+    return DAXM_OK;
+fail_cuda:
+    cudaGetLastError();
+    return fail(p, e == cudaErrorMemoryAllocation ? DAXM_ERR_OUT_OF_MEMORY : DAXM_ERR_CUDA, "host path: %s",
+                cudaGetErrorString(e));
+}
+
+void daxm_destroy(daxm_plan* p) {
+    if (!p) return;
+    {
+        DeviceGuard guard(p->device);
+        cudaDeviceSynchronize();
+        free_plan_memory(p);
+    }
+    delete p;
+}
+
+}  // extern "C"

@@ -1,0 +1,218 @@
+"""GPU vs fp64 oracle parity through the C ABI (BASELINE.json north_star tolerances).
+
+* element by element on every config that the oracle finishes in seconds
+  (C1, C2, C3 and ragged / banded / degenerate variants);
+* at BASELINE.json's full sizes (C4, C5) in the launch configuration bench.py
+  times, on sampled pixels the oracle computes one by one.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import parity
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def daxm():
+    import torch
+    from paper_2201_13309_b200 import _build
+    _build.build_library()
+    import paper_2201_13309_b200 as d
+    assert torch.cuda.is_available()
+    return d
+
+
+def run_gpu(daxm, g, host_stack, rows=None):
+    import torch
+    with daxm.create(g, device=0, rows=rows) as plan:
+        st = torch.from_numpy(np.ascontiguousarray(host_stack)).to("cuda:0")
+        out = plan.reconstruct(st)
+        torch.cuda.synchronize()
+        return out.cpu().numpy(), plan.stats()
+
+
+@pytest.mark.parametrize("edge", ["leading", "trailing"])
+@pytest.mark.parametrize("pixel_model", ["finite", "point"])
+@pytest.mark.parametrize("dtype", ["f32", "u16"])
+def test_c1_full(daxm, edge, pixel_model, dtype):
+    g = synth.geometry("C1", edge=edge, pixel_model=pixel_model)
+    maps = synth.make_maps("C1")
+    host = synth.stack_numpy(maps, dtype, noise=True)
+    gpu, st = run_gpu(daxm, g, host)
+    ref = oracle.reconstruct(g, host)
+    parity.check(gpu, ref, host, f"C1 {edge} {pixel_model} {dtype}")
+    assert st["fit_model_err_bins"] < 1e-6 and st["fit_max_err_bins"] < 1e-4
+
+
+@pytest.mark.parametrize("edge", ["leading", "trailing"])
+def test_c2_full(daxm, edge):
+    g = synth.geometry("C2", edge=edge)
+    maps = synth.make_maps("C2")
+    host = synth.stack_numpy(maps, "f32", noise=True)
+    gpu, _ = run_gpu(daxm, g, host)
+    ref = oracle.reconstruct(g, host)
+    parity.check(gpu, ref, host, f"C2 {edge}")
+
+
+def test_c2_peaks_only(daxm):
+    """No noise: background pixels must come out exactly zero, peak pixels within tolerance."""
+    g = synth.geometry("C2")
+    host = synth.stack_numpy(synth.make_maps("C2"), "f32", noise=False)
+    gpu, _ = run_gpu(daxm, g, host)
+    ref = oracle.reconstruct(g, host)
+    parity.check(gpu, ref, host, "C2 peaks")
+    flat = parity.abs_dI(host) == 0
+    assert (gpu[:, flat] == 0).all()
+    assert np.abs(gpu).max() > 100
+
+
+def test_c3_full_u16(daxm):
+    g = synth.geometry("C3")
+    maps = synth.make_maps("C3")
+    host = synth.stack_numpy(maps, "u16", noise=False)
+    gpu, _ = run_gpu(daxm, g, host)
+    ref = oracle.reconstruct(g, host)
+    parity.check(gpu, ref, host, "C3")
+
+
+def _sample_pixels(cfg, maps, n_rand, rng):
+    n = cfg.n
+    js = list(rng.integers(0, n, n_rand))
+    is_ = list(rng.integers(0, n, n_rand))
+    peak = np.argwhere(maps.amp > 0)
+    if len(peak):
+        sel = peak[rng.choice(len(peak), size=min(600, len(peak)), replace=False)]
+        js += list(sel[:, 0])
+        is_ += list(sel[:, 1])
+    for (j, i) in [(0, 0), (0, n - 1), (n - 1, 0), (n - 1, n - 1), (31, 32), (32, 31), (n // 2, n // 2)]:
+        js.append(j)
+        is_.append(i)
+    return np.array(js), np.array(is_)
+
+
+@pytest.mark.parametrize("name,noise", [("C3", True), ("C4", True), ("C5", False), ("C5", True)])
+def test_full_size_sampled(daxm, name, noise):
+    """BASELINE.json full sizes, stack generated on the GPU exactly as bench.py does;
+    sampled pixels recomputed by the oracle from the generator's per-pixel series."""
+    import torch
+    cfg = synth.get_config(name)
+    g = synth.geometry(cfg)
+    maps = synth.make_maps(cfg)
+    rng = np.random.default_rng(7 + cfg.number)
+    js, is_ = _sample_pixels(cfg, maps, 1500, rng)
+    with daxm.create(g, device=0) as plan:
+        stack = synth.stack_torch(maps, cfg.dtype, "cuda:0", noise=noise)
+        out = plan.reconstruct(stack)
+        torch.cuda.synchronize()
+        jt = torch.from_numpy(js).cuda()
+        it = torch.from_numpy(is_).cuda()
+        gpu = out[:, jt, it].cpu().numpy()  # [M, n]
+        del stack, out
+        torch.cuda.empty_cache()
+    series = synth.pixel_series(maps, js, is_, cfg.dtype, noise=noise)  # [n, S]
+    ref = oracle.reconstruct_pixels(g, js, is_, series).T
+    parity.check(gpu, ref, series.T, f"{name} sampled")
+
+
+# ------------------------------------------------------------------ edge cases
+
+def test_ragged_detector(daxm):
+    """Sizes that are not multiples of the 32x32 tile (partial tiles on both axes)."""
+    g = synth.geometry("C2", n_rows=77, n_cols=45)
+    g["wire_xyz"] = synth.wire_positions(61, t_range=(40.0, 1040.0))
+    rng = np.random.default_rng(3)
+    host = (1000 + rng.integers(-300, 300, (61, 77, 45))).astype(np.float32)
+    gpu, _ = run_gpu(daxm, g, host)
+    parity.check(gpu, oracle.reconstruct(g, host), host, "ragged")
+
+
+def test_row_bands_bit_exact(daxm):
+    """Row bands (the multi-GPU sharding) reproduce the full-detector plan bit for bit,
+    including bands that start/end inside a tile."""
+    g = synth.geometry("C2")
+    host = synth.stack_numpy(synth.make_maps("C2"), "f32", noise=True)
+    full, _ = run_gpu(daxm, g, host)
+    for (r0, r1) in [(0, 256), (256, 512), (100, 300), (511, 512), (5, 37)]:
+        band, _ = run_gpu(daxm, g, host[:, r0:r1], rows=(r0, r1))
+        assert np.array_equal(band, full[:, r0:r1]), (r0, r1)
+
+
+def test_no_pixel_reaches_the_bins(daxm):
+    g = synth.geometry("C1")
+    g["depth_start"], g["depth_end"] = 5000.0, 5100.0
+    host = synth.stack_numpy(synth.make_maps("C1"), "f32", noise=True)
+    gpu, st = run_gpu(daxm, g, host)
+    assert not gpu.any() and st["contrib_pairs"] == 0
+
+
+def test_single_bin_and_two_steps(daxm):
+    g = synth.geometry("C1")
+    g["depth_start"] = g["depth_end"] = 3.0
+    g["depth_res"] = 40.0
+    host = synth.stack_numpy(synth.make_maps("C1"), "f32", noise=True)
+    gpu, _ = run_gpu(daxm, g, host)
+    parity.check(gpu, oracle.reconstruct(g, host), host, "M=1")
+    g2 = synth.geometry("C1")
+    g2["wire_xyz"] = g2["wire_xyz"][[8, 12]].copy()
+    h2 = host[[8, 12]].copy()
+    gpu2, _ = run_gpu(daxm, g2, h2)
+    parity.check(gpu2, oracle.reconstruct(g2, h2), h2, "S=2")
+
+
+@pytest.mark.parametrize("pixel_model", ["finite", "point"])
+def test_repeated_wire_positions(daxm, pixel_model):
+    """Zero-travel pairs: POINT mode gives the degenerate delta (z1 == z4, reading R8)."""
+    g = synth.geometry("C1", pixel_model=pixel_model)
+    W = g["wire_xyz"]
+    g["wire_xyz"] = W[[0, 1, 2, 3, 4, 5, 6, 7, 8, 8, 9, 10, 10, 11, 12, 13, 14, 15, 16, 17, 18]].copy()
+    host = synth.stack_numpy(synth.make_maps("C1"), "f32", noise=True)
+    gpu, _ = run_gpu(daxm, g, host)
+    parity.check(gpu, oracle.reconstruct(g, host), host, f"repeated {pixel_model}")
+
+
+def test_reversed_scan_direction(daxm):
+    """Wire moving the other way (depth decreasing with the step index)."""
+    g = synth.geometry("C2", edge="leading")
+    g["wire_xyz"] = g["wire_xyz"][::-1].copy()
+    host = synth.stack_numpy(synth.make_maps("C2"), "f32", noise=True)[::-1].copy()
+    gpu, _ = run_gpu(daxm, g, host)
+    parity.check(gpu, oracle.reconstruct(g, host), host, "reversed")
+
+
+def test_u16_extremes(daxm):
+    g = synth.geometry("C1")
+    rng = np.random.default_rng(5)
+    host = rng.choice(np.array([0, 65535, 1, 65534], dtype=np.uint16), size=(21, 64, 64))
+    gpu, _ = run_gpu(daxm, g, host)
+    parity.check(gpu, oracle.reconstruct(g, host), host, "u16 extremes")
+
+
+def test_host_path_matches_device_path(daxm):
+    import torch
+    g = synth.geometry("C2")
+    host = synth.stack_numpy(synth.make_maps("C2"), "u16", noise=True)
+    with daxm.create(g, device=0) as plan:
+        dev = plan.reconstruct(torch.from_numpy(host).cuda())
+        torch.cuda.synchronize()
+        hp = plan.reconstruct_host(torch.from_numpy(host).pin_memory())
+        assert torch.equal(dev.cpu(), hp)
+
+
+def test_bad_pointers_on_device(daxm):
+    import torch
+    g = synth.geometry("C1")
+    with daxm.create(g, device=0) as plan:
+        st = torch.zeros((21, 64, 64), dtype=torch.float32, device="cuda")
+        with pytest.raises(ValueError):
+            plan.reconstruct(st.to(torch.float64))
+        with pytest.raises(ValueError):
+            plan.reconstruct(st, out=torch.empty((3, 3), device="cuda"))
+        with pytest.raises(daxm.DaxmError):
+            daxm.lib()  # library present
+            import ctypes as C
+            st_code = daxm.lib().daxm_reconstruct(plan._h, C.c_void_p(st.data_ptr() + 4), 1,
+                                                  C.c_void_p(st.data_ptr()), None)
+            plan._check(st_code)
