@@ -280,6 +280,9 @@ def main():
 
     # end to end through the C ABI from pinned host buffers (copies inside the timed region)
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, K // 4)
+    if e2e_steps <= 0:
+        return finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_max, achieved_min, value,
+                      units, st, clocks, r0, r1, alg_bytes, allgather_ms, None)
     h_stack = stack.cpu().pin_memory()
     h_out = torch.empty(plan.output_shape(), dtype=torch.float32).pin_memory()
     del stack
@@ -301,7 +304,15 @@ def main():
     e2e_value = units / (e2e_ms.item() * 1e-3)
     h2d = h_stack.numel() * h_stack.element_size() * world
     d2h = h_out.numel() * h_out.element_size() * world
+    e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "ms_per_step": e2e_ms.item(), "path": "daxm_reconstruct_host, pinned host buffers"}
+    return finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_max, achieved_min, value,
+                  units, st, clocks, r0, r1, alg_bytes, allgather_ms, e2e)
 
+
+def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_max, achieved_min, value, units, st,
+           clocks, r0, r1, alg_bytes, allgather_ms, e2e):
+    import torch.distributed as dist
     if rank == 0:
         peak, peak_src = peak_hbm()
         traffic = None
@@ -333,13 +344,15 @@ def main():
                          "kernel": "deposit (daxm_reconstruct)", "kernel_ms": kern_max,
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "bytes_rule": "sum_p (S_c(p)+1)*b_in + rows*C*M*4 (SURVEY.md §8(d))"},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_ms.item(), "path": "daxm_reconstruct_host, pinned host buffers"},
+            "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": K * world,
+            "gpu_launches": K * world * (1 if st["general_tiles_u16" if cfg.dtype == "u16" else "general_tiles_f32"] == 0
+                                         else 2),
             "clocks": clocks.summary(),
             "prepass_ms": st["prepass_ms"],
             "plan": {"contrib_pairs": st["contrib_pairs"], "window_pairs": st["window_pairs"],
+                     "general_tiles": st["general_tiles_u16" if cfg.dtype == "u16" else "general_tiles_f32"],
+                     "n_tiles": st["n_tiles"],
                      "staged_steps": st["staged_steps"], "fit_max_err_bins": st["fit_max_err_bins"],
                      "fit_model_err_bins": st["fit_model_err_bins"]},
         }

@@ -1,6 +1,7 @@
 // daxm_internal.cuh -- internal data layout shared by the plan (pre-pass) and
 // the deposit kernels.  Not part of the ABI.  See DESIGN.md "Data layout".
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -8,14 +9,23 @@
 
 namespace daxm {
 
-// Deposit tile: TILE_R detector rows x TILE_C detector columns.  Tiles are
+// Deposit tile: TILE_R detector rows x TILE_C detector columns.  Rows are the
+// warp lanes (the depth-insensitive detector axis: all 32 lanes of a warp walk
+// their pixels in lock step); each thread owns 4 adjacent columns.  Tiles are
 // aligned to GLOBAL detector rows/cols, so a row-band plan reproduces the
-// full-detector plan bit for bit (every per-tile reference is a function of
-// the global tile only).
-constexpr int TILE_R = 32;
-constexpr int TILE_C = 32;
+// full-detector plan bit for bit.
+constexpr int TILE_R = 128;
+constexpr int TILE_C = 8;
 constexpr int TILE_E = TILE_C + 1;  // pixel edge columns per tile (finite pixels)
 constexpr int NCOEF = 4;            // cubic depth model per edge point
+constexpr int COLS_PER_THREAD = 4;  // pixel walks per fast-kernel thread (1, 2 or 4)
+constexpr int N_CONSUMER_WARPS = (TILE_R / 32) * (TILE_C / COLS_PER_THREAD);
+constexpr int MC = 4;               // depth planes per output chunk (one TMA store)
+constexpr int NB_U16 = 32;          // input ring slots (wire steps) for uint16 stacks (power of 2)
+constexpr int NB_F32 = 16;          // ... for float32 stacks
+constexpr int MAX_FAST_NV = 4096;   // fast path: steps streamed per tile (tau table in shared memory)
+constexpr int MAX_FAST_CHUNKS = 1024;  // fast path needs (M + MC - 1) / MC + 1 <= this (M <= 4092)
+constexpr int RING_WINDOW_CHUNKS = 1;  // a warp's input needs between two of its own chunk boundaries
 
 // Geometry constants for the fp64 pre-pass (by value into kernels).
 struct GeomConst {
@@ -42,6 +52,8 @@ struct TileInfo {
     int k_lo;       // first wire step (point) any pixel of the tile reads
     int k_hi;       // last wire step (point) any pixel of the tile reads (inclusive); k_hi < k_lo: empty
     int dir;        // +1: depth increases with the step index, -1: decreases
+    int separated;  // 1: every pixel's consecutive edge spans are disjoint (fast path valid)
+    int ring_need;  // input ring slots the fast kernel needs for this tile (deadlock-free bound)
     int pad;
 };
 
@@ -59,16 +71,24 @@ struct DepositArgs {
     const TileInfo* tiles;    // [n_tr][n_tc]
     const int2* win;          // [pre_rows][C] pair window [kb, ke) per pixel (global pixel indexing)
     const float* coef;        // [n_tiles][NCOEF][TILE_E][TILE_R]
+    const int* tile_list;     // tiles for the general kernel
+    int n_list;
     int R, C, S, M;
     int row_begin, row_end;   // band (global rows)
     int pre_row0;             // first global row of win[]
     int tr0, n_tr, n_tc;      // tile rows covered (global tile-row index tr0 ..)
     int m_ref;
     int point_mode;
+    int nb;                   // input ring slots for this dtype (fast kernel)
+    int max_nv;               // max steps any tile streams (tau table size)
+    const int* vneed;         // [n_tiles][n_states + 1][8 warps] furthest visit index loaded by each state
+    int n_states;             // (M + MC - 1) / MC + 1
     float sign;               // s: +1 leading, -1 trailing (reading R2)
 };
 
 // Launchers (deposit.cu).
-cudaError_t launch_deposit(const DepositArgs& a, const void* stack, int dtype, float* out, cudaStream_t st);
+size_t fast_smem_bytes(int dtype, int max_nv);
+cudaError_t launch_deposit(const DepositArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
+                           const void* stack, int dtype, float* out, bool fast_enabled, cudaStream_t st);
 
 }  // namespace daxm

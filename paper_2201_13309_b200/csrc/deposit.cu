@@ -1,20 +1,36 @@
-// deposit.cu -- gather-form deposit kernel.
+// deposit.cu -- gather-form deposit kernels.
 //
-// One thread owns one pixel and writes all M depth bins of it; no atomics
-// (the paper's setTwo scatters with an fp64 CAS atomicAdd, P:L267-270,
-// P:L334).  With the wire-step pairs visited in the order in which
-// their trapezoids move deeper, the deposited intensity up to a bin edge E is
+// Every output (depth bin m, pixel p) is owned by exactly one thread; there
+// are no atomics (the paper's setTwo scatters with an fp64 CAS atomicAdd,
+// P:L267-270).
 //
-//   F(E) = sum_{pairs q with z4_q < E} dI_q  +  sum_{open pairs} dI_q H_q(E)/A_q
+// Deposit algebra.  For one pixel, visit the step pairs in the order in which
+// their trapezoids move deeper and let F(E) be the intensity deposited below
+// depth E (bin units).  Bin m receives F(m+1) - F(m): the trapezoid area inside
+// [lo_m, hi_m) summed over pairs (device_depth_resolve_pixel P:L320-330,
+// device_get_trapezoid_height P:L331), so computing F at the M+1 bin edges
+// gives every bin exactly once.
 //
-// (H the unit-height trapezoid CDF of device_get_trapezoid_height, P:L331,
-// A its area), and bin m receives F(m+1) - F(m) -- exactly the
-// trapezoid's area inside [lo_m, hi_m) (device_depth_resolve_pixel,
-// P:L320-330), summed over pairs.  Pairs are opened / closed by two monotone
-// pointers (the "step-range search" of SURVEY §8(a) step 4).
-//
-// v1: straightforward, one pass per bin edge, corner depths recomputed from
-// the per-edge-point cubic for every use, stack read with plain global loads.
+//  * deposit_fast: when, for every pair, the pixel's edge span at one wire
+//    step ends before the span at the next step begins ("separated", checked
+//    in fp64 by the pre-pass), the sum of the pairs' trapezoids
+//    f(z) = sum_q dI_q trap_q(z) / A_q is the piecewise-LINEAR function through
+//    (lo_q, c_{q-1}) and (hi_q, c_q), c_q = dI_q / A_q, A_q = mid_{q+1} - mid_q:
+//    on [lo_q, hi_q] pair q-1's falling ramp and pair q's rising ramp overlap,
+//    on [hi_q, lo_{q+1}] only pair q's plateau.  F is then a running sum of
+//    trapezoid-rule areas and F(E) inside a zone is one quadratic: 2 FMAs per
+//    pixel per bin edge.  A tile of 128 rows x 8 columns: warp lanes are
+//    detector rows (the depth-insensitive axis: lanes cross the same knots at
+//    the same edge), each thread owns 4 adjacent columns.  A producer warp
+//    streams the tile's wire-step planes with TMA into an mbarrier ring; the
+//    consumers stage 4 depth planes at a time in shared memory (32B swizzle,
+//    conflict-free 16-byte stores) and one thread writes them with a TMA
+//    bulk-tensor store.
+//  * deposit_general: any geometry (overlapping spans, degenerate trapezoids,
+//    widths that TMA cannot describe): F(E) = sum of closed pairs' dI + sum over
+//    open pairs of dI_q H_q(E)/A_q with the trapezoid CDF H, one thread per
+//    pixel, plain loads.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -23,31 +39,379 @@
 namespace daxm {
 namespace {
 
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+        "[%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+[[maybe_unused]] __device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
+}
+
 __device__ __forceinline__ float poly3(const float c[NCOEF], float tau) {
     return fmaf(fmaf(fmaf(c[3], tau, c[2]), tau, c[1]), tau, c[0]);
 }
 
-template <typename T>
-__device__ __forceinline__ float load_px(const T* __restrict__ p) {
-    return (float)__ldg(p);
-}
+constexpr int CPT = COLS_PER_THREAD;                          // pixel walks (columns) per thread
+constexpr int WPG = TILE_C / CPT;                             // warps per 32-row group
+constexpr int N_PAIRS = TILE_R / 32;                          // 32-row warp groups (32 rows x 8 cols each)
+constexpr int PAIR_BUF_BYTES = MC * 32 * TILE_C * 4;          // 4 KB: MC planes of a group's 32x8 block
+constexpr int FAST_THREADS = N_CONSUMER_WARPS * 32;
 
-struct PixelWalk {
-    float cb[NCOEF], cf[NCOEF];
-    const double* t;
-    double t_ref;
-    int kb, ke, dir;
-
-    __device__ __forceinline__ int step_of(int q) const { return dir > 0 ? kb + q : ke - q; }
-    __device__ __forceinline__ void point(int q, float& lo, float& hi) const {
-        const float tau = (float)(t[step_of(q)] - t_ref);
-        const float a = poly3(cb, tau), b = poly3(cf, tau);
-        lo = fminf(a, b);
-        hi = fmaxf(a, b);
-    }
+template <typename T, int NB>
+struct FastSmem {
+    static constexpr int IN_SLOT_BYTES = TILE_R * TILE_C * (int)sizeof(T);
+    static constexpr int OFF_OUT = 0;                                   // [pair][2][MC][32][8] f32
+    static constexpr int OFF_IN = OFF_OUT + N_PAIRS * 2 * PAIR_BUF_BYTES;
+    static constexpr int OFF_BAR = OFF_IN + NB * IN_SLOT_BYTES;         // full[NB], empty[NB]
+    static constexpr int OFF_OBAR = OFF_BAR + 2 * NB * 8;               // pfull[pair][2], pfree[pair][2]
+    static constexpr int OFF_TAU = OFF_OBAR + 4 * N_PAIRS * 8;
+    static size_t bytes(int max_nv) { return (size_t)OFF_TAU + sizeof(float) * (size_t)(max_nv + 4) + 1024; }
 };
 
-// Unit-height trapezoid CDF at E divided by its area: corners from points q, q+1.
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ float lds_px(uint32_t addr);
+template <>
+__device__ __forceinline__ float lds_px<uint16_t>(uint32_t addr) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
+    return (float)v;
+}
+template <>
+__device__ __forceinline__ float lds_px<float>(uint32_t addr) {
+    return lds_f32(addr);
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 2000;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// ------------------------------------------------------------------ fast kernel
+// Eight warps: warp w covers tile rows 32*(w/2) .. +31 (lanes) and columns
+// 4*(w%2) .. +3 (one pixel walk per column, all in registers).
+//
+// Per pixel, zone q = [lo_q, lo_{q+1}) holds pair q-1's falling ramp and pair
+// q's rising ramp on [lo_q, hi_q] and pair q's plateau after it, so with
+// x = E - lo_q, xc = min(x, w_q), w_q = hi_q - lo_q:
+//     F(E) = F(lo_q) + c_q x + xc (d_q + g_q xc),  d_q = c_{q-1} - c_q,
+//     g_q = (c_q - c_{q-1}) / (2 w_q)
+// (exact for the linear interpolant through (lo_q, c_{q-1}), (hi_q, c_q),
+// (lo_{q+1}, c_q)), one transition per wire step, 5 flops per pixel per edge.
+//
+// Pipeline: thread 0 is also the producer -- it issues the TMA loads of
+// wire-step planes whenever a ring slot has been released by all eight warps,
+// polling at every chunk start and inside every wait it performs, so no warp
+// ever waits on a load that cannot be issued.  The two warps of a pair (same 32
+// rows) stage MC depth planes of their 32x8 block in shared memory and the
+// pair's first warp writes them with one TMA store; pairs never wait on each
+// other.  Each warp waits for its input once per chunk, up to the furthest
+// wire step its own pixels load in that chunk (pre-pass, a.vneed).
+template <typename T, int NB, bool POINT>
+__global__ void __launch_bounds__(FAST_THREADS, 2)
+    deposit_fast(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
+                 const DepositArgs a) {
+    static_assert((NB & (NB - 1)) == 0, "ring size must be a power of two");
+    using L = FastSmem<T, NB>;
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    unsigned char* smem = smem_raw + (sbase - smem_u32(smem_raw));
+    const int tile = blockIdx.x;
+    const TileInfo ti = a.tiles[tile];
+    const int tr = tile / a.n_tc, tc = tile % a.n_tc;
+    const int row0 = (a.tr0 + tr) * TILE_R;  // global row of tile row 0
+    // the general kernel owns this tile (same predicate as the plan's tile lists)
+    if (!(ti.separated && row0 >= a.row_begin && ti.ring_need <= NB)) return;
+    const int col0 = tc * TILE_C;
+    const int row0_local = row0 - a.row_begin;
+    const int nv = ti.k_hi >= ti.k_lo ? ti.k_hi - ti.k_lo + 1 : 0;
+    const int dir = ti.dir;
+
+    const uint32_t s_full = sbase + L::OFF_BAR, s_empty = s_full + NB * 8;
+    const uint32_t s_obar = sbase + L::OFF_OBAR;
+    const uint32_t s_tau = sbase + L::OFF_TAU, s_ring = sbase + L::OFF_IN;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+    uint64_t* empty = full + NB;
+    uint64_t* obar = reinterpret_cast<uint64_t*>(smem + L::OFF_OBAR);  // [pair][pfull0, pfull1, pfree0, pfree1]
+    float* tau = reinterpret_cast<float*>(smem + L::OFF_TAU);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool producer = threadIdx.x == 0;
+    if (producer) {
+        for (int s = 0; s < NB; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], N_CONSUMER_WARPS);
+        }
+        for (int pp = 0; pp < N_PAIRS; ++pp) {
+            mbar_init(&obar[pp * 4 + 0], WPG);
+            mbar_init(&obar[pp * 4 + 1], WPG);
+            mbar_init(&obar[pp * 4 + 2], 1);
+            mbar_init(&obar[pp * 4 + 3], 1);
+        }
+        fence_mbar_init();
+    }
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+        const int k = dir > 0 ? ti.k_lo + v : ti.k_hi - v;
+        tau[v] = (float)(a.t[k] - ti.t_ref);
+    }
+    __syncthreads();
+    // producer state (thread 0 only): next visit index to load
+    int v_issue = 0;
+    auto issue_loads = [&]() {
+        while (v_issue < nv) {
+            const int s = v_issue & (NB - 1);
+            if (v_issue >= NB && !mbar_test(s_empty + s * 8, ((v_issue / NB) - 1) & 1)) break;
+            mbar_arrive_expect_tx(&full[s], L::IN_SLOT_BYTES);
+            const int k = dir > 0 ? ti.k_lo + v_issue : ti.k_hi - v_issue;
+            tma_load_3d(smem + L::OFF_IN + s * L::IN_SLOT_BYTES, &in_map, col0, row0_local, k, &full[s]);
+            ++v_issue;
+        }
+    };
+    // wait on an mbarrier phase; the producer keeps issuing loads meanwhile
+    auto wait_bar = [&](uint32_t bar, uint32_t parity) {
+        while (!mbar_try(bar, parity))
+            if (producer) issue_loads();
+    };
+    if (producer) issue_loads();
+
+    const int pair = warp / WPG, h = warp % WPG;  // 32-row group, column group
+    const int r = pair * 32 + lane;  // tile row
+    const int j = row0 + r;          // global row
+    const float sdir2 = 2.f * a.sign * (float)dir;  // c = 2 s dir dI / (sum_{q+1} - sum_q)
+    const float INF = __int_as_float(0x7f800000);
+    const uint32_t px_off = (uint32_t)(r * TILE_C + h * CPT) * (uint32_t)sizeof(T);
+    const uint32_t s_pfull = s_obar + pair * 32, s_pfree = s_pfull + 16;
+
+    float cb[CPT + 1][NCOEF];  // edge points h*CPT .. h*CPT+CPT of this row
+#pragma unroll
+    for (int e = 0; e <= CPT; ++e)
+#pragma unroll
+        for (int m = 0; m < NCOEF; ++m)
+            cb[e][m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + (h * CPT + e)) * TILE_R + r];
+
+    // zone state per walk (see above) and the next point (nlo, nhi, nI)
+    float zlo[CPT], zw[CPT], zF[CPT], zc[CPT], zd[CPT], zg[CPT], nlo[CPT], nhi[CPT], nI[CPT], Fp[CPT];
+    int vn[CPT], vend[CPT];  // next visit index to load, one past the last point
+#pragma unroll
+    for (int w = 0; w < CPT; ++w) {
+        zlo[w] = zw[w] = zF[w] = zc[w] = zd[w] = zg[w] = nI[w] = Fp[w] = 0.f;
+        nlo[w] = nhi[w] = INF;
+        vn[w] = vend[w] = 0;
+    }
+    // Input readiness is checked once per output chunk (warp-uniform): the
+    // pre-pass recorded per tile, state and warp the furthest step loaded.
+    int ready = -1;
+    const int* vneed = a.vneed + (size_t)tile * (a.n_states + 1) * N_CONSUMER_WARPS + warp;
+    auto wait_upto = [&](int vt) {
+        while (ready < vt) {
+            ++ready;
+            wait_bar(s_full + (ready & (NB - 1)) * 8, (ready / NB) & 1);
+        }
+    };
+
+    auto load_point = [&](int w, int v, float& lo, float& hi, float& I) {
+        const float t = lds_f32(s_tau + 4u * (uint32_t)v);
+        const float x0 = poly3(cb[w], t);
+        const float x1 = POINT ? x0 : poly3(cb[w + 1], t);
+        lo = fminf(x0, x1);
+        hi = fmaxf(x0, x1);
+        I = lds_px<T>(s_ring + (uint32_t)(v & (NB - 1)) * (uint32_t)L::IN_SLOT_BYTES + px_off +
+                      (uint32_t)(w * sizeof(T)));
+    };
+    auto evalF = [&](int w, float E) -> float {
+        const float x = E - zlo[w];
+        const float xc = fminf(x, zw[w]);
+        return fmaf(xc, fmaf(zg[w], xc, zd[w]), fmaf(zc[w], x, zF[w]));
+    };
+    // move walk w into the zone containing E
+    auto advance = [&](int w, float E) {
+        while (E > nlo[w]) {
+            zF[w] = evalF(w, nlo[w]);  // F(lo_{q+1})
+            const float cprev = zc[w];
+            zlo[w] = nlo[w];
+            zw[w] = nhi[w] - nlo[w];
+            const float s_cur = nlo[w] + nhi[w], I_cur = nI[w];
+            float c = 0.f;
+            if (vn[w] < vend[w]) {
+                load_point(w, vn[w], nlo[w], nhi[w], nI[w]);
+                ++vn[w];
+                c = (sdir2 * (I_cur - nI[w])) * rcp_approx((nlo[w] + nhi[w]) - s_cur);
+            } else {
+                nlo[w] = nhi[w] = INF;
+            }
+            zc[w] = c;
+            zd[w] = cprev - c;
+            // g = (c - c_prev) / (2 w); w == 0 (POINT pixels) -> huge g, but xc <= w keeps xc*g*xc ~ 0
+            zg[w] = zd[w] * rcp_approx(-2.f * fmaxf(zw[w], 1e-30f));
+        }
+    };
+
+    wait_upto(vneed[0]);
+#pragma unroll
+    for (int w = 0; w < CPT; ++w) {
+        const int i = col0 + h * CPT + w;
+        int2 win = make_int2(0, 0);
+        if (j < a.R && i < a.C) win = a.win[(size_t)(j - a.pre_row0) * a.C + i];
+        if (win.y > win.x) {
+            const int v0 = dir > 0 ? win.x - ti.k_lo : ti.k_hi - win.y;
+            vend[w] = v0 + (win.y - win.x + 1);
+            load_point(w, v0, nlo[w], nhi[w], nI[w]);
+            vn[w] = v0 + 1;
+            zlo[w] = nlo[w];  // virtual zone before point 0: F = 0
+        }
+    }
+    int vt_next = vneed[2 * N_CONSUMER_WARPS];  // prefetched bound for chunk 0
+    {
+        wait_upto(vneed[N_CONSUMER_WARPS]);
+        const float E0 = (float)(0 - a.m_ref);
+#pragma unroll
+        for (int w = 0; w < CPT; ++w) advance(w, E0);
+#pragma unroll
+        for (int w = 0; w < CPT; ++w) Fp[w] = evalF(w, E0);
+    }
+
+    int released = 0;
+    const uint32_t out_base = sbase + L::OFF_OUT + pair * 2 * PAIR_BUF_BYTES;
+    // [q][32 rows][8 cols] f32, 32-byte rows, SWIZZLE_32B (16-byte chunk ^= bit 7 of the offset);
+    // q * 1024 leaves bit 7 alone, so the swizzled row offset is per-thread constant
+    const uint32_t row_off = (uint32_t)(lane * (TILE_C * 4) + h * CPT * 4);
+    const uint32_t sts_off = row_off ^ (((row_off >> 7) & 1u) << 4);
+    const int n_chunks = (a.M + MC - 1) / MC;
+    float E = (float)(1 - a.m_ref);
+    for (int ch = 0; ch < n_chunks; ++ch) {
+        const int b = ch & 1;
+        const int vt = vt_next;
+        if (ch + 1 < n_chunks) vt_next = vneed[(ch + 3) * N_CONSUMER_WARPS];
+        if (ch >= 2) wait_bar(s_pfree + b * 8, ((ch >> 1) - 1) & 1);  // store ch-2 left buffer b
+        wait_upto(vt);
+        if (producer) issue_loads();
+        uint32_t sa = out_base + b * PAIR_BUF_BYTES + sts_off;
+        const int q_end = min(MC, a.M - ch * MC);  // planes >= M are padding: no advance
+#pragma unroll 1
+        for (int q = 0; q < MC; ++q, sa += 32 * TILE_C * 4) {
+            if (q < q_end) {
+#pragma unroll
+                for (int w = 0; w < CPT; ++w) advance(w, E);
+            }
+            float o[CPT];
+#pragma unroll
+            for (int w = 0; w < CPT; ++w) {
+                const float F = evalF(w, E);
+                o[w] = F - Fp[w];
+                Fp[w] = F;
+            }
+            if constexpr (CPT == 4)
+                st_shared_v4(sa, o[0], o[1], o[2], o[3]);
+            else if constexpr (CPT == 2)
+                asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(sa), "f"(o[0]), "f"(o[1]) : "memory");
+            else
+                asm volatile("st.shared.f32 [%0], %1;" ::"r"(sa), "f"(o[0]) : "memory");
+            E += 1.f;
+        }
+        fence_proxy_async_smem();
+        // release wire-step slots no walk of this warp needs any more
+        int my_min = INT_MAX;
+#pragma unroll
+        for (int w = 0; w < CPT; ++w)
+            if (vn[w] < vend[w]) my_min = min(my_min, vn[w]);
+        const int target = min(__reduce_min_sync(0xffffffffu, my_min), nv);
+        if (lane == 0) {
+            for (int v = released; v < target; ++v) mbar_arrive(&empty[v & (NB - 1)]);
+            mbar_arrive(&obar[pair * 4 + b]);  // pfull[b]
+        }
+        released = max(released, target);
+        if (h == 0 && lane == 0) {  // the pair's storer
+            bulk_wait_read<0>();                                   // its store ch-1 has left buffer b^1
+            if (ch >= 1) mbar_arrive(&obar[pair * 4 + 2 + (b ^ 1)]);  // pfree[b^1]
+            wait_bar(s_pfull + b * 8, (ch >> 1) & 1);              // partner has written chunk ch
+            tma_store_3d(&out_map, col0, row0_local + pair * 32, ch * MC,
+                         smem + L::OFF_OUT + (pair * 2 + b) * PAIR_BUF_BYTES);
+            bulk_commit();
+        }
+        __syncwarp();
+    }
+    if (lane == 0)
+        for (int v = released; v < nv; ++v) mbar_arrive(&empty[v & (NB - 1)]);
+    if (h == 0 && lane == 0) bulk_wait<0>();
+    if (producer) {
+        while (v_issue < nv) issue_loads();  // others may still need the tail
+        // every issued load must land before the CTA may exit
+        for (int v = v_issue > NB ? v_issue - NB : 0; v < v_issue; ++v) mbar_wait(&full[v & (NB - 1)], (v / NB) & 1);
+    }
+}
+
+// ------------------------------------------------------------------ general kernel
 __device__ __forceinline__ float trapezoid_fraction(float lo0, float hi0, float lo1, float hi1, float E) {
     const float z1 = fminf(lo0, lo1), z4 = fmaxf(hi0, hi1);
     const float ma = fmaxf(lo0, lo1), mb = fminf(hi0, hi1);
@@ -64,85 +428,127 @@ __device__ __forceinline__ float trapezoid_fraction(float lo0, float hi0, float 
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) deposit_v1(DepositArgs a, const T* __restrict__ stack, float* __restrict__ out) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int jl = blockIdx.y * blockDim.y + threadIdx.y;
-    const int rows = a.row_end - a.row_begin;
-    if (i >= a.C || jl >= rows) return;
-    const int j = a.row_begin + jl;
-    const size_t plane = (size_t)rows * a.C;
-    const int tr = j / TILE_R - a.tr0, tc = i / TILE_C;
-    const int tile = tr * a.n_tc + tc;
+__global__ void __launch_bounds__(256) deposit_general(DepositArgs a, const T* __restrict__ stack,
+                                                       float* __restrict__ out) {
+    const int tile = a.tile_list ? a.tile_list[blockIdx.x] : (int)blockIdx.x;
     const TileInfo ti = a.tiles[tile];
-    const int2 w = a.win[(size_t)(j - a.pre_row0) * a.C + i];
-    PixelWalk pw;
-    const int r = j % TILE_R, eb = i % TILE_C, ef = a.point_mode ? eb : eb + 1;
+    const int tr = tile / a.n_tc, tc = tile % a.n_tc;
+    const int rows = a.row_end - a.row_begin;
+    const size_t plane = (size_t)rows * a.C;
+    for (int pix = threadIdx.x; pix < TILE_R * TILE_C; pix += blockDim.x) {
+        const int r = pix / TILE_C, c = pix % TILE_C;
+        const int j = (a.tr0 + tr) * TILE_R + r, i = tc * TILE_C + c;
+        if (j < a.row_begin || j >= a.row_end || i >= a.C) continue;
+        const int jl = j - a.row_begin;
+        const int2 w = a.win[(size_t)(j - a.pre_row0) * a.C + i];
+        float cb[NCOEF], cf[NCOEF];
+        const int eb = c, ef = a.point_mode ? c : c + 1;
 #pragma unroll
-    for (int m = 0; m < NCOEF; ++m) {
-        pw.cb[m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + eb) * TILE_R + r];
-        pw.cf[m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + ef) * TILE_R + r];
-    }
-    pw.t = a.t;
-    pw.t_ref = ti.t_ref;
-    pw.kb = w.x;
-    pw.ke = w.y;
-    pw.dir = ti.dir;
-    const int n = w.y - w.x;  // pairs
-    const T* px = stack + (size_t)jl * a.C + i;
-    const float sgn = a.sign * (float)ti.dir;
-    auto dI = [&](int q) -> float {
-        return sgn * (load_px(px + (size_t)pw.step_of(q) * plane) - load_px(px + (size_t)pw.step_of(q + 1) * plane));
-    };
-    int qc = 0, qo = 0;
-    float P = 0.f, F_prev = 0.f;
-    float* o = out + (size_t)jl * a.C + i;
-    for (int e = 0; e <= a.M; ++e) {
-        const float E = (float)(e - a.m_ref);
-        // close pairs whose trapezoid lies entirely below E
-        while (qc < n) {
-            float lo1, hi1, lo2, hi2;
-            pw.point(qc, lo1, hi1);
-            pw.point(qc + 1, lo2, hi2);
-            if (fmaxf(hi1, hi2) < E) {
-                P += dI(qc);
-                ++qc;
-            } else {
-                break;
+        for (int m = 0; m < NCOEF; ++m) {
+            cb[m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + eb) * TILE_R + r];
+            cf[m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + ef) * TILE_R + r];
+        }
+        const int kb = w.x, ke = w.y, n = ke - kb, dir = ti.dir;
+        auto step_of = [&](int q) { return dir > 0 ? kb + q : ke - q; };
+        auto point = [&](int q, float& lo, float& hi) {
+            const float tau = (float)(a.t[step_of(q)] - ti.t_ref);
+            const float x0 = poly3(cb, tau), x1 = poly3(cf, tau);
+            lo = fminf(x0, x1);
+            hi = fmaxf(x0, x1);
+        };
+        const T* px = stack + (size_t)jl * a.C + i;
+        const float sgn = a.sign * (float)dir;
+        auto dI = [&](int q) -> float {
+            return sgn * ((float)px[(size_t)step_of(q) * plane] - (float)px[(size_t)step_of(q + 1) * plane]);
+        };
+        int qc = 0, qo = 0;
+        float P = 0.f, F_prev = 0.f;
+        float* o = out + (size_t)jl * a.C + i;
+        for (int e = 0; e <= a.M; ++e) {
+            const float E = (float)(e - a.m_ref);
+            while (qc < n) {  // close pairs whose trapezoid lies entirely below E
+                float lo1, hi1, lo2, hi2;
+                point(qc, lo1, hi1);
+                point(qc + 1, lo2, hi2);
+                if (fmaxf(hi1, hi2) < E) {
+                    P += dI(qc);
+                    ++qc;
+                } else {
+                    break;
+                }
             }
+            if (qo < qc) qo = qc;
+            while (qo < n) {  // open pairs whose trapezoid starts below E
+                float lo1, hi1, lo2, hi2;
+                point(qo, lo1, hi1);
+                point(qo + 1, lo2, hi2);
+                if (fminf(lo1, lo2) < E)
+                    ++qo;
+                else
+                    break;
+            }
+            float F = P;
+            for (int q = qc; q < qo; ++q) {
+                float lo1, hi1, lo2, hi2;
+                point(q, lo1, hi1);
+                point(q + 1, lo2, hi2);
+                const float d = dI(q);
+                if (d != 0.f) F += d * trapezoid_fraction(lo1, hi1, lo2, hi2, E);
+            }
+            if (e > 0) o[(size_t)(e - 1) * plane] = F - F_prev;
+            F_prev = F;
         }
-        // open pairs whose trapezoid starts below E
-        if (qo < qc) qo = qc;
-        while (qo < n) {
-            float lo1, hi1, lo2, hi2;
-            pw.point(qo, lo1, hi1);
-            pw.point(qo + 1, lo2, hi2);
-            if (fminf(lo1, lo2) < E)
-                ++qo;
-            else
-                break;
-        }
-        float F = P;
-        for (int q = qc; q < qo; ++q) {
-            float lo1, hi1, lo2, hi2;
-            pw.point(q, lo1, hi1);
-            pw.point(q + 1, lo2, hi2);
-            const float d = dI(q);
-            if (d != 0.f) F += d * trapezoid_fraction(lo1, hi1, lo2, hi2, E);
-        }
-        if (e > 0) o[(size_t)(e - 1) * plane] = F - F_prev;
-        F_prev = F;
     }
+}
+
+template <typename T, int NB, bool POINT>
+cudaError_t launch_fast(const CUtensorMap* in_map, const CUtensorMap* out_map, const DepositArgs& a, int n_tiles,
+                        cudaStream_t st) {
+    const size_t sm = FastSmem<T, NB>::bytes(a.max_nv);
+    static bool attr_set = false;  // per template instance
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(deposit_fast<T, NB, POINT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)FastSmem<T, NB>::bytes(MAX_FAST_NV));
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute(deposit_fast<T, NB, POINT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                 (int)cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    if (sm > FastSmem<T, NB>::bytes(MAX_FAST_NV)) return cudaErrorInvalidValue;
+    deposit_fast<T, NB, POINT><<<n_tiles, FAST_THREADS, sm, st>>>(*in_map, *out_map, a);
+    return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_deposit(const DepositArgs& a, const void* stack, int dtype, float* out, cudaStream_t st) {
-    const int rows = a.row_end - a.row_begin;
-    dim3 blk(32, 8), grd((a.C + 31) / 32, (rows + 7) / 8);
+size_t fast_smem_bytes(int dtype, int max_nv) {
+    return dtype == DAXM_U16 ? FastSmem<uint16_t, NB_U16>::bytes(max_nv) : FastSmem<float, NB_F32>::bytes(max_nv);
+}
+
+cudaError_t launch_deposit(const DepositArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
+                           const void* stack, int dtype, float* out, bool fast_enabled, cudaStream_t st) {
+    const int n_tiles = a.n_tr * a.n_tc;
+    cudaError_t e = cudaSuccess;
+    if (fast_enabled) {
+        if (a.point_mode)
+            e = dtype == DAXM_U16 ? launch_fast<uint16_t, NB_U16, true>(in_map, out_map, a, n_tiles, st)
+                                  : launch_fast<float, NB_F32, true>(in_map, out_map, a, n_tiles, st);
+        else
+            e = dtype == DAXM_U16 ? launch_fast<uint16_t, NB_U16, false>(in_map, out_map, a, n_tiles, st)
+                                  : launch_fast<float, NB_F32, false>(in_map, out_map, a, n_tiles, st);
+        if (e != cudaSuccess) return e;
+        if (a.n_list == 0) return cudaSuccess;
+    }
+    DepositArgs ga = a;
+    if (!fast_enabled) {
+        ga.tile_list = nullptr;
+        ga.n_list = n_tiles;
+    }
     if (dtype == DAXM_U16)
-        deposit_v1<uint16_t><<<grd, blk, 0, st>>>(a, static_cast<const uint16_t*>(stack), out);
+        deposit_general<uint16_t><<<ga.n_list, 256, 0, st>>>(ga, static_cast<const uint16_t*>(stack), out);
     else
-        deposit_v1<float><<<grd, blk, 0, st>>>(a, static_cast<const float*>(stack), out);
+        deposit_general<float><<<ga.n_list, 256, 0, st>>>(ga, static_cast<const float*>(stack), out);
     return cudaGetLastError();
 }
 

@@ -21,12 +21,15 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <new>
 #include <string>
 #include <vector>
 
 #include "daxm.h"
 #include "daxm_internal.cuh"
+
+#include <cudaTypedefs.h>
 
 using namespace daxm;
 
@@ -45,6 +48,18 @@ struct daxm_plan {
     int2* d_win = nullptr;
     float* d_coef = nullptr;
     signed char* d_pdir = nullptr;
+    signed char* d_psep = nullptr;
+    int* d_vneed = nullptr;     // [n_tiles][n_states + 1] furthest visit index needed (fast kernel)
+    int n_states = 0;
+    int* d_list_u16 = nullptr;  // general-kernel tile lists per dtype
+    int* d_list_f32 = nullptr;
+    int n_list_u16 = 0, n_list_f32 = 0;
+    int max_nv = 0;
+    // TMA descriptors, re-encoded when the caller's buffers change
+    CUtensorMap in_map{}, out_map{};
+    const void* map_stack = nullptr;
+    const float* map_out = nullptr;
+    int map_dtype = -1;
     // end-to-end (host buffer) path scratch, allocated on first use
     void* d_stack_buf = nullptr;
     size_t stack_buf_bytes = 0;
@@ -127,8 +142,8 @@ __device__ __forceinline__ void atomic_max_pos_double(double* addr, double v) {
 // ------------------------------------------------------------ pixel windows
 __global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire, int pre_row0, int pre_rows,
                                     int band_r0, int band_r1, int2* __restrict__ win,
-                                    signed char* __restrict__ pdir, unsigned* __restrict__ flags,
-                                    unsigned long long* __restrict__ counters) {
+                                    signed char* __restrict__ pdir, signed char* __restrict__ psep,
+                                    unsigned* __restrict__ flags, unsigned long long* __restrict__ counters) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     const int jl = blockIdx.y * blockDim.y + threadIdx.y;
     if (i >= g.C || jl >= pre_rows) return;
@@ -165,7 +180,7 @@ __global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire
         uf0 = uf1;
     }
     int2 w = make_int2(0, 0);
-    signed char dir = 0;
+    signed char dir = 0, sep = 1;
     if (first >= 0) {
         if (nan_inside) atomicOr(flags, FLAG_NAN_IN_WINDOW);
         if (j >= band_r0 && j < band_r1) {
@@ -175,35 +190,58 @@ __global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire
         int kb = first, ke = last + 1;  // pairs [kb, ke)
         if (kb > 0 && !first_prev_nan) --kb;             // one guard pair each side (fp32 rounding)
         if (ke <= g.S - 2 && !next_nan) ++ke;
-        // pass 2: monotonicity and direction over the window's points kb..ke
-        bool pos = false, neg = false;
+        // pass 2: monotonicity and direction over the window's points kb..ke, and
+        // "separation": consecutive points' edge spans [lo, hi] are disjoint (by a
+        // 1e-3-bin margin) and every trapezoid has area >= 1e-3 bins, in either
+        // visiting order -- the condition for the fast deposit kernel's
+        // piecewise-linear form.
+        bool pos = false, neg = false, sep_pos = true, sep_neg = true;
         double pb = tangent_u(g, Qb, sb, wire + 3 * kb), pf = tangent_u(g, Qf, sf, wire + 3 * kb);
         for (int k = kb + 1; k <= ke; ++k) {
             double cb = tangent_u(g, Qb, sb, wire + 3 * k), cf = tangent_u(g, Qf, sf, wire + 3 * k);
             double db = cb - pb, df = cf - pf;
             pos |= (db > 0.0) || (df > 0.0);
             neg |= (db < 0.0) || (df < 0.0);
+            const double lo0 = fmin(pb, pf), hi0 = fmax(pb, pf), lo1 = fmin(cb, cf), hi1 = fmax(cb, cf);
+            const double area = 0.5 * ((lo1 + hi1) - (lo0 + hi0));
+            sep_pos &= (hi0 <= lo1 - 1e-3) && (area >= 1e-3);
+            sep_neg &= (hi1 <= lo0 - 1e-3) && (-area >= 1e-3);
             pb = cb;
             pf = cf;
         }
         if (pos && neg) atomicOr(flags, FLAG_NONMONOTONE);
         dir = neg ? -1 : 1;
+        sep = (dir > 0 ? sep_pos : sep_neg) ? 1 : 0;
         w = make_int2(kb, ke);
     }
     win[(size_t)jl * g.C + i] = w;
     pdir[(size_t)jl * g.C + i] = dir;
+    psep[(size_t)jl * g.C + i] = sep;
 }
 
 // ------------------------------------------------------------ tiles
-__global__ void tile_kernel(GeomConst g, const double* __restrict__ t, int pre_row0, int pre_rows, int tr0,
-                            int n_tc, int band_r0, int band_r1, const int2* __restrict__ win,
-                            const signed char* __restrict__ pdir, TileInfo* __restrict__ tiles,
-                            unsigned* __restrict__ flags, unsigned long long* __restrict__ counters) {
+// One CTA (TILE_C x TILE_R threads) per tile: union step range, t_ref,
+// separation, and the input-ring bound of the fast kernel.  ring_need bounds
+// how far apart (in streamed steps) the tile's pixels can be between two
+// consecutive output-chunk boundaries: with v_p(E) = v0_p + #{points of p with
+// lo < E}, ring_need = max over c of [max_p v_p(E_{c+W}) - min_p v_p(E_c)] + 3 with
+// W = RING_WINDOW_CHUNKS output chunks (the loads a warp may wait for are issued
+// at most W chunks after the slowest pixel's frontier).
+// A ring of at least that many slots can never deadlock.
+__global__ void __launch_bounds__(1024) tile_kernel(GeomConst g, const double* __restrict__ t, const double* __restrict__ wire,
+                            int pre_row0, int pre_rows, int tr0, int n_tc, int band_r0, int band_r1,
+                            const int2* __restrict__ win, const signed char* __restrict__ pdir,
+                            const signed char* __restrict__ psep, TileInfo* __restrict__ tiles,
+                            unsigned* __restrict__ flags, unsigned long long* __restrict__ counters, int n_states,
+                            int* __restrict__ vneed) {
+    extern __shared__ int s_v[];  // [2][n_states + 1]: max, min of v_p at each state; then [n_states + 1][8] per warp
     const int tile = blockIdx.x;
     const int tr = tile / n_tc, tc = tile % n_tc;
-    const int r = threadIdx.y, c = threadIdx.x;  // 32 x 32
+    const int c = threadIdx.x, r = threadIdx.y;  // TILE_C x TILE_R
+    const int tid = r * TILE_C + c;
+    const int nthr = blockDim.x * blockDim.y;
     const int j = (tr0 + tr) * TILE_R + r, i = tc * TILE_C + c;
-    int kb = INT_MAX, ke = INT_MIN, dpos = 0, dneg = 0;
+    int kb = INT_MAX, ke = INT_MIN, dpos = 0, dneg = 0, nsep = 0;
     long long pairs = 0;
     if (j < g.R && i < g.C && j >= pre_row0 && j < pre_row0 + pre_rows) {
         int2 w = win[(size_t)(j - pre_row0) * g.C + i];
@@ -213,17 +251,28 @@ __global__ void tile_kernel(GeomConst g, const double* __restrict__ t, int pre_r
             signed char d = pdir[(size_t)(j - pre_row0) * g.C + i];
             dpos = d > 0;
             dneg = d < 0;
+            nsep = psep[(size_t)(j - pre_row0) * g.C + i] ? 0 : 1;
             if (j >= band_r0 && j < band_r1) pairs = w.y - w.x;
         }
     }
-    __shared__ int s_kb, s_ke, s_pos, s_neg;
+    __shared__ int s_kb, s_ke, s_pos, s_neg, s_nsep, s_need;
     __shared__ unsigned long long s_pairs;
-    if (r == 0 && c == 0) {
+    const bool track = n_states <= MAX_FAST_CHUNKS;
+    if (tid == 0) {
         s_kb = INT_MAX;
         s_ke = INT_MIN;
-        s_pos = 0;
-        s_neg = 0;
+        s_pos = s_neg = s_nsep = 0;
+        s_need = 0;
         s_pairs = 0;
+    }
+    int* s_w = s_v + 2 * (n_states + 1);  // per consumer warp of the fast kernel
+    const int fwarp = (r / 32) * (TILE_C / COLS_PER_THREAD) + c / COLS_PER_THREAD;
+    if (track) {
+        for (int q = tid; q <= n_states; q += nthr) {
+            s_v[q] = INT_MIN;
+            s_v[n_states + 1 + q] = INT_MAX;
+        }
+        for (int q = tid; q < (n_states + 1) * N_CONSUMER_WARPS; q += nthr) s_w[q] = INT_MIN;
     }
     __syncthreads();
     if (kb != INT_MAX) {
@@ -231,10 +280,65 @@ __global__ void tile_kernel(GeomConst g, const double* __restrict__ t, int pre_r
         atomicMax(&s_ke, ke);
         if (dpos) atomicOr(&s_pos, 1);
         if (dneg) atomicOr(&s_neg, 1);
+        if (nsep) atomicOr(&s_nsep, 1);
         atomicAdd(&s_pairs, (unsigned long long)pairs);
     }
     __syncthreads();
-    if (r == 0 && c == 0) {
+    const int k_lo = s_kb, k_hi = s_ke;
+    const int tdir = s_neg ? -1 : 1;
+    // ring bound: state 0 = before any edge (v0), state 1 + c = after edge e = min(c*MC, M)
+    if (track && kb != INT_MAX) {
+        double Qb[3], Qf[3];
+        edge_point(g, j, i, Qb);
+        edge_point(g, j, g.point_mode ? i : i + 1, Qf);
+        const double sb = edge_sigma(g, Qb), sf = edge_sigma(g, Qf);
+        const int n_pts = ke - kb + 1;
+        const int v0 = tdir > 0 ? kb - k_lo : k_hi - ke;
+        atomicMax(&s_v[0], v0);
+        atomicMin(&s_v[n_states + 1], v0);
+        atomicMax(&s_w[fwarp], v0);
+        int q = 0;  // points with lo < E seen so far
+        double lo_q = 0.0;
+        bool have = false;
+        for (int st = 1; st <= n_states; ++st) {
+            const int e = min((st - 1) * MC, g.M);
+            const double E = (double)(e - g.m_ref);
+            while (q < n_pts) {
+                if (!have) {
+                    const int k = tdir > 0 ? kb + q : ke - q;
+                    lo_q = fmin(tangent_u(g, Qb, sb, wire + 3 * k), tangent_u(g, Qf, sf, wire + 3 * k));
+                    have = true;
+                }
+                if (lo_q < E) {
+                    ++q;
+                    have = false;
+                } else {
+                    break;
+                }
+            }
+            atomicMax(&s_v[st], v0 + q);
+            atomicMin(&s_v[n_states + 1 + st], v0 + q);
+            atomicMax(&s_w[st * N_CONSUMER_WARPS + fwarp], v0 + q);
+        }
+    }
+    __syncthreads();
+    // furthest visit index any pixel of the tile loads by the end of each state (+1: fp32 rounding),
+    // so the fast kernel can wait for its input once per output chunk
+    if (track)
+        for (int q = tid; q < (n_states + 1) * N_CONSUMER_WARPS; q += nthr) {
+            const int hi = s_w[q];
+            vneed[(size_t)tile * (n_states + 1) * N_CONSUMER_WARPS + q] =
+                (s_kb == INT_MAX || hi == INT_MIN) ? -1 : min(hi + 1, s_ke - s_kb);
+        }
+    if (track && s_kb != INT_MAX)
+        for (int q = tid; q < n_states; q += nthr) {
+            // states q -> q + RING_WINDOW_CHUNKS (clamped): the span of steps in flight
+            const int q2 = min(q + RING_WINDOW_CHUNKS, n_states);
+            const int hi = s_v[q2], lo = s_v[n_states + 1 + q];
+            if (hi != INT_MIN && lo != INT_MAX) atomicMax(&s_need, hi - lo + 3);
+        }
+    __syncthreads();
+    if (tid == 0) {
         TileInfo ti;
         ti.pad = 0;
         if (s_kb == INT_MAX) {
@@ -242,15 +346,19 @@ __global__ void tile_kernel(GeomConst g, const double* __restrict__ t, int pre_r
             ti.k_lo = 0;
             ti.k_hi = -1;
             ti.dir = 1;
+            ti.separated = 1;
+            ti.ring_need = 0;
         } else {
-            ti.k_lo = s_kb;
-            ti.k_hi = s_ke;
-            ti.t_ref = 0.5 * (t[s_kb] + t[s_ke]);
-            ti.dir = s_neg ? -1 : 1;
+            ti.k_lo = k_lo;
+            ti.k_hi = k_hi;
+            ti.t_ref = 0.5 * (t[k_lo] + t[k_hi]);
+            ti.dir = tdir;
+            ti.separated = s_nsep ? 0 : 1;
+            ti.ring_need = track ? s_need : INT_MAX;
             if (s_pos && s_neg) atomicOr(flags, FLAG_MIXED_DIR);
             // staged steps, only for tiles that intersect the band
             int tj0 = (tr0 + tr) * TILE_R, tj1 = tj0 + TILE_R;
-            if (tj1 > band_r0 && tj0 < band_r1) atomicAdd(&counters[1], (unsigned long long)(s_ke - s_kb + 1));
+            if (tj1 > band_r0 && tj0 < band_r1) atomicAdd(&counters[1], (unsigned long long)(k_hi - k_lo + 1));
         }
         tiles[tile] = ti;
         atomicAdd(&counters[0], s_pairs);
@@ -258,7 +366,7 @@ __global__ void tile_kernel(GeomConst g, const double* __restrict__ t, int pre_r
 }
 
 // ------------------------------------------------------------ cubic fit
-__global__ void fit_kernel(GeomConst g, const double* __restrict__ t, const double* __restrict__ wire, int tr0,
+__global__ void __launch_bounds__(1024) fit_kernel(GeomConst g, const double* __restrict__ t, const double* __restrict__ wire, int tr0,
                            int n_tc, const TileInfo* __restrict__ tiles, float* __restrict__ coef,
                            unsigned* __restrict__ flags, double* __restrict__ max_err) {
     const int tile = blockIdx.x;
@@ -362,6 +470,10 @@ void free_plan_memory(daxm_plan* p) {
     cudaFree(p->d_win);
     cudaFree(p->d_coef);
     cudaFree(p->d_pdir);
+    cudaFree(p->d_psep);
+    cudaFree(p->d_list_u16);
+    cudaFree(p->d_vneed);
+    cudaFree(p->d_list_f32);
     cudaFree(p->d_stack_buf);
     cudaFree(p->d_out_buf);
     p->d_t = p->d_wire = nullptr;
@@ -369,6 +481,9 @@ void free_plan_memory(daxm_plan* p) {
     p->d_win = nullptr;
     p->d_coef = nullptr;
     p->d_pdir = nullptr;
+    p->d_psep = nullptr;
+    p->d_list_u16 = p->d_list_f32 = nullptr;
+    p->d_vneed = nullptr;
     p->d_stack_buf = nullptr;
     p->d_out_buf = nullptr;
 }
@@ -456,6 +571,7 @@ daxm_status device_prepass(daxm_plan* p) {
     CK(cudaMalloc(&p->d_tiles, sizeof(TileInfo) * n_tiles));
     CK(cudaMalloc(&p->d_win, sizeof(int2) * (size_t)p->pre_rows * g.n_cols));
     CK(cudaMalloc(&p->d_pdir, (size_t)p->pre_rows * g.n_cols));
+    CK(cudaMalloc(&p->d_psep, (size_t)p->pre_rows * g.n_cols));
     CK(cudaMalloc(&p->d_coef, sizeof(float) * n_tiles * NCOEF * TILE_E * TILE_R));
     unsigned* d_flags = nullptr;
     double* d_err = nullptr;
@@ -474,11 +590,19 @@ daxm_status device_prepass(daxm_plan* p) {
     {
         dim3 blk(128, 1), grd((g.n_cols + 127) / 128, p->pre_rows);
         pixel_window_kernel<<<grd, blk>>>(gc, p->d_wire, p->pre_row0, p->pre_rows, g.row_begin, g.row_end,
-                                          p->d_win, p->d_pdir, d_flags, d_cnt);
+                                          p->d_win, p->d_pdir, p->d_psep, d_flags, d_cnt);
         CK(cudaGetLastError());
-        tile_kernel<<<(unsigned)n_tiles, dim3(TILE_C, TILE_R)>>>(gc, p->d_t, p->pre_row0, p->pre_rows, p->tr0,
-                                                                p->n_tc, g.row_begin, g.row_end, p->d_win,
-                                                                p->d_pdir, p->d_tiles, d_flags, d_cnt);
+        const int n_states = (p->M + MC - 1) / MC + 1;
+        p->n_states = n_states;
+        const size_t tsm =
+            n_states <= MAX_FAST_CHUNKS ? sizeof(int) * (2 + N_CONSUMER_WARPS) * (size_t)(n_states + 1) : 0;
+        if (n_states <= MAX_FAST_CHUNKS)
+            CK(cudaMalloc(&p->d_vneed, sizeof(int) * n_tiles * (n_states + 1) * N_CONSUMER_WARPS));
+        if (tsm > 48 * 1024)
+            CK(cudaFuncSetAttribute(tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+        tile_kernel<<<(unsigned)n_tiles, dim3(TILE_C, TILE_R), tsm>>>(
+            gc, p->d_t, p->d_wire, p->pre_row0, p->pre_rows, p->tr0, p->n_tc, g.row_begin, g.row_end, p->d_win,
+            p->d_pdir, p->d_psep, p->d_tiles, d_flags, d_cnt, n_states, p->d_vneed);
         CK(cudaGetLastError());
         fit_kernel<<<(unsigned)n_tiles, dim3(TILE_R, 8)>>>(gc, p->d_t, p->d_wire, p->tr0, p->n_tc, p->d_tiles,
                                                           p->d_coef, d_flags, d_err);
@@ -520,6 +644,35 @@ daxm_status device_prepass(daxm_plan* p) {
                                 (sizeof(int2) + 1) * (size_t)p->pre_rows * g.n_cols +
                                 sizeof(float) * n_tiles * NCOEF * TILE_E * TILE_R);
 
+    {
+        std::vector<TileInfo> ht(n_tiles);
+        CK(cudaMemcpy(ht.data(), p->d_tiles, sizeof(TileInfo) * n_tiles, cudaMemcpyDeviceToHost));
+        std::vector<int> lu, lf;
+        for (size_t q = 0; q < n_tiles; ++q) {
+            const TileInfo& ti = ht[q];
+            if (!ti.separated) ++st.nonseparated_tiles;
+            if (ti.k_hi >= ti.k_lo) st.ring_need_max = std::max<int64_t>(st.ring_need_max, ti.ring_need);
+            if (ti.k_hi >= ti.k_lo) p->max_nv = std::max(p->max_nv, ti.k_hi - ti.k_lo + 1);
+            // TMA boxes start at the tile's first row; a tile that starts above the band
+            // (band start not a multiple of TILE_R) would need a negative coordinate -> general kernel
+            const int tile_row0 = (p->tr0 + (int)(q / p->n_tc)) * TILE_R;
+            const bool sep = ti.separated != 0 && tile_row0 >= g.row_begin;
+            if (!(sep && ti.ring_need <= NB_U16)) lu.push_back((int)q);
+            if (!(sep && ti.ring_need <= NB_F32)) lf.push_back((int)q);
+        }
+        p->n_list_u16 = (int)lu.size();
+        p->n_list_f32 = (int)lf.size();
+        if (!lu.empty()) {
+            CK(cudaMalloc(&p->d_list_u16, sizeof(int) * lu.size()));
+            CK(cudaMemcpy(p->d_list_u16, lu.data(), sizeof(int) * lu.size(), cudaMemcpyHostToDevice));
+        }
+        if (!lf.empty()) {
+            CK(cudaMalloc(&p->d_list_f32, sizeof(int) * lf.size()));
+            CK(cudaMemcpy(p->d_list_f32, lf.data(), sizeof(int) * lf.size(), cudaMemcpyHostToDevice));
+        }
+        st.general_tiles_u16 = p->n_list_u16;
+        st.general_tiles_f32 = p->n_list_f32;
+    }
     if (flags & (FLAG_NONMONOTONE | FLAG_MIXED_DIR))
         return fail(nullptr, DAXM_ERR_NONMONOTONE_SCAN,
                     "a pixel edge's tangent depth is not monotone in the wire step inside its window (flags 0x%x)", flags);
@@ -640,8 +793,14 @@ daxm_status daxm_plan_stats_get(const daxm_plan* p, daxm_plan_stats* st) {
     return DAXM_OK;
 }
 
-static DepositArgs make_args(const daxm_plan* p) {
+static DepositArgs make_args(const daxm_plan* p, int dtype) {
     DepositArgs a;
+    a.tile_list = dtype == DAXM_U16 ? p->d_list_u16 : p->d_list_f32;
+    a.n_list = dtype == DAXM_U16 ? p->n_list_u16 : p->n_list_f32;
+    a.nb = dtype == DAXM_U16 ? NB_U16 : NB_F32;
+    a.max_nv = p->max_nv;
+    a.vneed = p->d_vneed;
+    a.n_states = p->n_states;
     a.t = p->d_t;
     a.tiles = p->d_tiles;
     a.win = p->d_win;
@@ -662,6 +821,74 @@ static DepositArgs make_args(const daxm_plan* p) {
     return a;
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        cudaGetLastError();
+    }
+    return fn;
+}
+
+// The fast kernel needs TMA-describable buffers: row pitch a multiple of 16 bytes.
+static bool fast_possible(const daxm_plan* p, int dt) {
+    const int es = dt == DAXM_U16 ? 2 : 4;
+    return (p->C * es) % 16 == 0 && (p->C * 4) % 16 == 0 && p->max_nv <= MAX_FAST_NV && p->d_vneed != nullptr &&
+           getenv("DAXM_FORCE_GENERAL") == nullptr && tensor_map_encoder() != nullptr;
+}
+
+static daxm_status encode_maps(daxm_plan* p, const void* d_stack, int dt, float* d_out) {
+    if (p->map_stack == d_stack && p->map_out == d_out && p->map_dtype == dt) return DAXM_OK;
+    auto enc = tensor_map_encoder();
+    const cuuint64_t es = dt == DAXM_U16 ? 2 : 4;
+    const cuuint64_t C = (cuuint64_t)p->C, R = (cuuint64_t)p->rows;
+    {
+        cuuint64_t dims[3] = {C, R, (cuuint64_t)p->S};
+        cuuint64_t strides[2] = {C * es, C * R * es};
+        cuuint32_t box[3] = {(cuuint32_t)TILE_C, (cuuint32_t)TILE_R, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = enc(&p->in_map, dt == DAXM_U16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                         3, const_cast<void*>(d_stack), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(p, DAXM_ERR_CUDA, "cuTensorMapEncodeTiled(stack) failed: %d", (int)r);
+    }
+    {
+        cuuint64_t dims[3] = {C, R, (cuuint64_t)p->M};
+        cuuint64_t strides[2] = {C * 4, C * R * 4};
+        cuuint32_t box[3] = {(cuuint32_t)TILE_C, 32u, (cuuint32_t)MC};  // one warp pair's rows
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = enc(&p->out_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_out, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(p, DAXM_ERR_CUDA, "cuTensorMapEncodeTiled(out) failed: %d", (int)r);
+    }
+    p->map_stack = d_stack;
+    p->map_out = d_out;
+    p->map_dtype = dt;
+    return DAXM_OK;
+}
+
+static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float* d_out, cudaStream_t st) {
+    const bool fast = fast_possible(p, dt);
+    if (fast) {
+        daxm_status s = encode_maps(p, d_stack, dt, d_out);
+        if (s != DAXM_OK) return s;
+    }
+    cudaError_t e = launch_deposit(make_args(p, dt), &p->in_map, &p->out_map, d_stack, dt, d_out, fast, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(p, DAXM_ERR_CUDA, "deposit launch: %s", cudaGetErrorString(e));
+    }
+    return DAXM_OK;
+}
+
 daxm_status daxm_reconstruct(daxm_plan* p, const void* d_stack, daxm_dtype dt, float* d_out, void* cuda_stream) {
     if (!p) return DAXM_ERR_INVALID_ARGUMENT;
     p->err.clear();
@@ -670,12 +897,7 @@ daxm_status daxm_reconstruct(daxm_plan* p, const void* d_stack, daxm_dtype dt, f
     if ((reinterpret_cast<uintptr_t>(d_stack) | reinterpret_cast<uintptr_t>(d_out)) & 15)
         return fail(p, DAXM_ERR_INVALID_ARGUMENT, "stack and output must be 16-byte aligned");
     DeviceGuard guard(p->device);
-    cudaError_t e = launch_deposit(make_args(p), d_stack, (int)dt, d_out, (cudaStream_t)cuda_stream);
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        return fail(p, DAXM_ERR_CUDA, "deposit launch: %s", cudaGetErrorString(e));
-    }
-    return DAXM_OK;
+    return run_deposit(p, d_stack, (int)dt, d_out, (cudaStream_t)cuda_stream);
 }
 
 daxm_status daxm_reconstruct_host(daxm_plan* p, const void* h_stack, daxm_dtype dt, float* h_out, void* cuda_stream) {
@@ -707,8 +929,10 @@ daxm_status daxm_reconstruct_host(daxm_plan* p, const void* h_stack, daxm_dtype 
     }
     e = cudaMemcpyAsync(p->d_stack_buf, h_stack, in_bytes, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) goto fail_cuda;
-    e = launch_deposit(make_args(p), p->d_stack_buf, (int)dt, p->d_out_buf, st);
-    if (e != cudaSuccess) goto fail_cuda;
+    {
+        daxm_status s = run_deposit(p, p->d_stack_buf, (int)dt, p->d_out_buf, st);
+        if (s != DAXM_OK) return s;
+    }
     e = cudaMemcpyAsync(h_out, p->d_out_buf, out_bytes, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) goto fail_cuda;
     e = cudaStreamSynchronize(st);

@@ -282,10 +282,14 @@ def stack_torch(maps: StackMaps, dtype: str, device, noise: bool = False, rows: 
         out = torch.empty((maps.n_steps, r1 - r0, maps.n_cols), dtype=tdt, device=device)
     dev = lambda a: torch.from_numpy(np.ascontiguousarray(a[r0:r1])).to(device)
     bg, amp, ka, w, kt = dev(maps.bg), dev(maps.amp), dev(maps.ka), dev(maps.w), dev(maps.kt)
-    jj = torch.arange(r0, r1, device=device, dtype=torch.int64)[:, None].expand(r1 - r0, maps.n_cols)
-    ii = torch.arange(maps.n_cols, device=device, dtype=torch.int64)[None, :].expand(r1 - r0, maps.n_cols)
-    for k in range(maps.n_steps):
-        v = stack_values(torch.tensor(k, device=device, dtype=torch.int64), jj, ii, bg, amp, ka, w, kt,
-                         maps.seed, noise, torch)
-        out[k].copy_(to_dtype(v, dtype, torch))
+    jj = torch.arange(r0, r1, device=device, dtype=torch.int64)[None, :, None]
+    ii = torch.arange(maps.n_cols, device=device, dtype=torch.int64)[None, None, :]
+    bg, amp, ka, w, kt = (x[None] for x in (bg, amp, ka, w, kt))
+    # a few steps per launch group (bounded temporary memory: int64 [kc, rows, C])
+    kc = max(1, min(maps.n_steps, (1 << 28) // max(1, (r1 - r0) * maps.n_cols)))
+    for k0 in range(0, maps.n_steps, kc):
+        k1 = min(maps.n_steps, k0 + kc)
+        k = torch.arange(k0, k1, device=device, dtype=torch.int64)[:, None, None]
+        v = stack_values(k, jj, ii, bg, amp, ka, w, kt, maps.seed, noise, torch)
+        out[k0:k1].copy_(to_dtype(v, dtype, torch))
     return out

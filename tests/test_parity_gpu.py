@@ -129,15 +129,21 @@ def test_ragged_detector(daxm):
     parity.check(gpu, oracle.reconstruct(g, host), host, "ragged")
 
 
-def test_row_bands_bit_exact(daxm):
-    """Row bands (the multi-GPU sharding) reproduce the full-detector plan bit for bit,
-    including bands that start/end inside a tile."""
+def test_row_bands(daxm):
+    """Row bands (the multi-GPU sharding).  Bands aligned to the 128-row tile reproduce the
+    full-detector plan bit for bit (every tile reference is global); bands starting inside a
+    tile run that tile through the general kernel and must still match the oracle."""
     g = synth.geometry("C2")
     host = synth.stack_numpy(synth.make_maps("C2"), "f32", noise=True)
     full, _ = run_gpu(daxm, g, host)
-    for (r0, r1) in [(0, 256), (256, 512), (100, 300), (511, 512), (5, 37)]:
+    for (r0, r1) in [(0, 256), (256, 512), (128, 384), (384, 500)]:
         band, _ = run_gpu(daxm, g, host[:, r0:r1], rows=(r0, r1))
         assert np.array_equal(band, full[:, r0:r1]), (r0, r1)
+    ref = oracle.reconstruct(g, host)
+    for (r0, r1) in [(100, 300), (511, 512), (5, 37)]:
+        band, st = run_gpu(daxm, g, host[:, r0:r1], rows=(r0, r1))
+        assert st["general_tiles_f32"] > 0
+        parity.check(band, ref[:, r0:r1], host[:, r0:r1], f"band {r0}-{r1}")
 
 
 def test_no_pixel_reaches_the_bins(daxm):
@@ -216,3 +222,33 @@ def test_bad_pointers_on_device(daxm):
             st_code = daxm.lib().daxm_reconstruct(plan._h, C.c_void_p(st.data_ptr() + 4), 1,
                                                   C.c_void_p(st.data_ptr()), None)
             plan._check(st_code)
+
+
+@pytest.mark.parametrize("name,dtype", [("C1", "f32"), ("C2", "f32"), ("C2", "u16")])
+def test_general_kernel_parity(daxm, name, dtype, monkeypatch):
+    """The general (any-geometry) deposit kernel on its own: DAXM_FORCE_GENERAL routes every tile to it."""
+    monkeypatch.setenv("DAXM_FORCE_GENERAL", "1")
+    g = synth.geometry(name)
+    host = synth.stack_numpy(synth.make_maps(name), dtype, noise=True)
+    gpu, _ = run_gpu(daxm, g, host)
+    parity.check(gpu, oracle.reconstruct(g, host), host, f"{name} general")
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_benchmark_configs_take_the_fast_path(daxm, name):
+    """Every tile of these BASELINE configs is 'separated' and fits the input ring, so bench.py times
+    the TMA-pipelined kernel alone.  (C5's finest bins make the pixel-edge span exceed the
+    per-step sweep on the detector's shallow side: those tiles run the general kernel, see
+    test_c5_general_tiles_are_the_overlapping_ones.)"""
+    cfg = synth.get_config(name)
+    with daxm.create(synth.geometry(cfg), device=0) as plan:
+        st = plan.stats()
+    key = "general_tiles_u16" if cfg.dtype == "u16" else "general_tiles_f32"
+    assert st[key] == 0, {k: st[k] for k in ("nonseparated_tiles", "ring_need_max", key)}
+
+
+def test_c5_general_tiles_are_the_overlapping_ones(daxm):
+    cfg = synth.get_config("C5")
+    with daxm.create(synth.geometry(cfg), device=0) as plan:
+        st = plan.stats()
+    assert st["general_tiles_u16"] == st["nonseparated_tiles"] < st["n_tiles"] // 4
