@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "libdaxm.so")
+# DAXM_LIBRARY selects an alternative build of the same library (kernel-variant experiments)
+_LIB_PATH = os.environ.get("DAXM_LIBRARY") or os.path.join(_PKG, "libdaxm.so")
 
 EDGE = {"leading": 0, "trailing": 1}
 PIXEL_MODEL = {"finite": 0, "point": 1}

@@ -17,10 +17,18 @@ namespace daxm {
 constexpr int TILE_R = 128;
 constexpr int TILE_C = 8;
 constexpr int TILE_E = TILE_C + 1;  // pixel edge columns per tile (finite pixels)
-constexpr int NCOEF = 4;            // cubic depth model per edge point
+constexpr int NCOEF = 3;            // depth model per edge point: polynomial of degree NCOEF-1 in wire travel
+// fp64 approximation error allowed for the depth model (bins); the fp32 evaluation adds ~ulp(M/2)
+constexpr double MODEL_ERR_MAX = NCOEF >= 4 ? 1e-6 : 2e-5;
 constexpr int COLS_PER_THREAD = 4;  // pixel walks per fast-kernel thread (1, 2 or 4)
 constexpr int N_CONSUMER_WARPS = (TILE_R / 32) * (TILE_C / COLS_PER_THREAD);
-constexpr int MC = 4;               // depth planes per output chunk (one TMA store)
+#ifndef DAXM_MC
+#define DAXM_MC 4
+#endif
+#ifndef DAXM_PREFETCH
+#define DAXM_PREFETCH 1
+#endif
+constexpr int MC = DAXM_MC;         // depth planes per output chunk (one TMA store)
 constexpr int NB_U16 = 32;          // input ring slots (wire steps) for uint16 stacks (power of 2)
 constexpr int NB_F32 = 16;          // ... for float32 stacks
 constexpr int MAX_FAST_NV = 4096;   // fast path: steps streamed per tile (tau table in shared memory)

@@ -97,7 +97,10 @@ __device__ __forceinline__ void fence_mbar_init() {
 }
 
 __device__ __forceinline__ float poly3(const float c[NCOEF], float tau) {
-    return fmaf(fmaf(fmaf(c[3], tau, c[2]), tau, c[1]), tau, c[0]);
+    float p = c[NCOEF - 1];
+#pragma unroll
+    for (int m = NCOEF - 2; m >= 0; --m) p = fmaf(p, tau, c[m]);
+    return p;
 }
 
 constexpr int CPT = COLS_PER_THREAD;                          // pixel walks (columns) per thread
@@ -260,12 +263,15 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
         for (int m = 0; m < NCOEF; ++m)
             cb[e][m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + (h * CPT + e)) * TILE_R + r];
 
-    // zone state per walk (see above) and the next point (nlo, nhi, nI)
+    // zone state per walk (see above), the next point P1 = (nlo, nhi, nI) and the raw
+    // inputs (tau, intensity) of the point after it, prefetched one transition ahead so
+    // the shared-memory latency is off the transition's critical path
     float zlo[CPT], zw[CPT], zF[CPT], zc[CPT], zd[CPT], zg[CPT], nlo[CPT], nhi[CPT], nI[CPT], Fp[CPT];
-    int vn[CPT], vend[CPT];  // next visit index to load, one past the last point
+    float pt[CPT], pI[CPT];
+    int vn[CPT], vend[CPT];  // visit index of the prefetched point, one past the last point
 #pragma unroll
     for (int w = 0; w < CPT; ++w) {
-        zlo[w] = zw[w] = zF[w] = zc[w] = zd[w] = zg[w] = nI[w] = Fp[w] = 0.f;
+        zlo[w] = zw[w] = zF[w] = zc[w] = zd[w] = zg[w] = nI[w] = Fp[w] = pt[w] = pI[w] = 0.f;
         nlo[w] = nhi[w] = INF;
         vn[w] = vend[w] = 0;
     }
@@ -279,15 +285,16 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
             wait_bar(s_full + (ready & (NB - 1)) * 8, (ready / NB) & 1);
         }
     };
-
-    auto load_point = [&](int w, int v, float& lo, float& hi, float& I) {
-        const float t = lds_f32(s_tau + 4u * (uint32_t)v);
+    auto fetch_raw = [&](int w, int v) {
+        pt[w] = lds_f32(s_tau + 4u * (uint32_t)v);
+        pI[w] = lds_px<T>(s_ring + (uint32_t)(v & (NB - 1)) * (uint32_t)L::IN_SLOT_BYTES + px_off +
+                          (uint32_t)(w * sizeof(T)));
+    };
+    auto depths = [&](int w, float t, float& lo, float& hi) {
         const float x0 = poly3(cb[w], t);
         const float x1 = POINT ? x0 : poly3(cb[w + 1], t);
         lo = fminf(x0, x1);
         hi = fmaxf(x0, x1);
-        I = lds_px<T>(s_ring + (uint32_t)(v & (NB - 1)) * (uint32_t)L::IN_SLOT_BYTES + px_off +
-                      (uint32_t)(w * sizeof(T)));
     };
     auto evalF = [&](int w, float E) -> float {
         const float x = E - zlo[w];
@@ -304,8 +311,16 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
             const float s_cur = nlo[w] + nhi[w], I_cur = nI[w];
             float c = 0.f;
             if (vn[w] < vend[w]) {
-                load_point(w, vn[w], nlo[w], nhi[w], nI[w]);
+#if DAXM_PREFETCH
+                depths(w, pt[w], nlo[w], nhi[w]);
+                nI[w] = pI[w];
+                if (++vn[w] < vend[w]) fetch_raw(w, vn[w]);
+#else
+                fetch_raw(w, vn[w]);
+                depths(w, pt[w], nlo[w], nhi[w]);
+                nI[w] = pI[w];
                 ++vn[w];
+#endif
                 c = (sdir2 * (I_cur - nI[w])) * rcp_approx((nlo[w] + nhi[w]) - s_cur);
             } else {
                 nlo[w] = nhi[w] = INF;
@@ -326,8 +341,13 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
         if (win.y > win.x) {
             const int v0 = dir > 0 ? win.x - ti.k_lo : ti.k_hi - win.y;
             vend[w] = v0 + (win.y - win.x + 1);
-            load_point(w, v0, nlo[w], nhi[w], nI[w]);
+            fetch_raw(w, v0);
+            depths(w, pt[w], nlo[w], nhi[w]);
+            nI[w] = pI[w];
             vn[w] = v0 + 1;
+#if DAXM_PREFETCH
+            fetch_raw(w, v0 + 1);  // windows hold >= 2 points
+#endif
             zlo[w] = nlo[w];  // virtual zone before point 0: F = 0
         }
     }

@@ -328,14 +328,14 @@ __global__ void __launch_bounds__(1024) tile_kernel(GeomConst g, const double* _
         for (int q = tid; q < (n_states + 1) * N_CONSUMER_WARPS; q += nthr) {
             const int hi = s_w[q];
             vneed[(size_t)tile * (n_states + 1) * N_CONSUMER_WARPS + q] =
-                (s_kb == INT_MAX || hi == INT_MIN) ? -1 : min(hi + 1, s_ke - s_kb);
+                (s_kb == INT_MAX || hi == INT_MIN) ? -1 : min(hi + 2, s_ke - s_kb);  // +1 prefetch, +1 fp32
         }
     if (track && s_kb != INT_MAX)
         for (int q = tid; q < n_states; q += nthr) {
             // states q -> q + RING_WINDOW_CHUNKS (clamped): the span of steps in flight
             const int q2 = min(q + RING_WINDOW_CHUNKS, n_states);
             const int hi = s_v[q2], lo = s_v[n_states + 1 + q];
-            if (hi != INT_MIN && lo != INT_MAX) atomicMax(&s_need, hi - lo + 3);
+            if (hi != INT_MIN && lo != INT_MAX) atomicMax(&s_need, hi - lo + 4);
         }
     __syncthreads();
     if (tid == 0) {
@@ -378,16 +378,19 @@ __global__ void __launch_bounds__(1024) fit_kernel(GeomConst g, const double* __
     for (int e = threadIdx.y; e < TILE_E; e += blockDim.y) {
         const int eg = tc * TILE_C + e;  // global edge column
         const int n_edges = g.point_mode ? g.C : g.C + 1;
-        float cf[NCOEF] = {0.f, 0.f, 0.f, 0.f};
+        float cf[NCOEF];
+        for (int m = 0; m < NCOEF; ++m) cf[m] = 0.f;
         if (ti.k_hi >= ti.k_lo && j < g.R && eg < n_edges) {
             double Q[3];
             edge_point(g, j, eg, Q);
             const double sg = edge_sigma(g, Q);
             const double h = 0.5 * (t[ti.k_hi] - t[ti.k_lo]);
-            double b[NCOEF] = {0, 0, 0, 0};
+            double b[NCOEF];
+            for (int m = 0; m < NCOEF; ++m) b[m] = 0.0;
             if (h > 0.0) {
-                // Chebyshev interpolation at the 4 first-kind nodes of [t_lo, t_hi]
-                double a[NCOEF] = {0, 0, 0, 0};
+                // Chebyshev interpolation at the NCOEF first-kind nodes of [t_lo, t_hi]
+                double a[NCOEF];
+                for (int m = 0; m < NCOEF; ++m) a[m] = 0.0;
                 for (int n = 0; n < NCOEF; ++n) {
                     const double th = M_PI * (2 * n + 1) / (2.0 * NCOEF);
                     const double x = cos(th);
@@ -398,8 +401,22 @@ __global__ void __launch_bounds__(1024) fit_kernel(GeomConst g, const double* __
                     for (int m = 0; m < NCOEF; ++m) a[m] += u * cos(m * th);
                 }
                 for (int m = 0; m < NCOEF; ++m) a[m] *= (m == 0 ? 1.0 : 2.0) / NCOEF;
-                // Chebyshev -> monomial in x, then x = tau / h
-                const double bx[NCOEF] = {a[0] - a[2], a[1] - 3.0 * a[3], 2.0 * a[2], 4.0 * a[3]};
+                // Chebyshev -> monomial in x (T_{n+1} = 2x T_n - T_{n-1}), then x = tau / h
+                double Tm[NCOEF], Tc[NCOEF], Tn[NCOEF], bx[NCOEF];
+                for (int m = 0; m < NCOEF; ++m) Tm[m] = Tc[m] = bx[m] = 0.0;
+                Tm[0] = 1.0;           // T_0
+                if (NCOEF > 1) Tc[1] = 1.0;  // T_1
+                for (int m = 0; m < NCOEF; ++m) bx[m] += a[0] * Tm[m];
+                if (NCOEF > 1)
+                    for (int m = 0; m < NCOEF; ++m) bx[m] += a[1] * Tc[m];
+                for (int n = 2; n < NCOEF; ++n) {
+                    for (int m = 0; m < NCOEF; ++m) Tn[m] = (m > 0 ? 2.0 * Tc[m - 1] : 0.0) - Tm[m];
+                    for (int m = 0; m < NCOEF; ++m) {
+                        bx[m] += a[n] * Tn[m];
+                        Tm[m] = Tc[m];
+                        Tc[m] = Tn[m];
+                    }
+                }
                 double hp = 1.0;
                 for (int m = 0; m < NCOEF; ++m) {
                     b[m] = bx[m] / hp;
@@ -419,10 +436,13 @@ __global__ void __launch_bounds__(1024) fit_kernel(GeomConst g, const double* __
                 const double ex = tangent_u(g, Q, sg, wire + 3 * k);
                 if (isnan(ex)) continue;
                 const double td = t[k] - ti.t_ref;
-                const double pm = b[0] + td * (b[1] + td * (b[2] + td * b[3]));
-                local_model = fmax(local_model, fabs(pm - ex));
                 const double tau = (double)(float)td;
-                const double p = (double)cf[0] + tau * ((double)cf[1] + tau * ((double)cf[2] + tau * (double)cf[3]));
+                double pm = b[NCOEF - 1], p = (double)cf[NCOEF - 1];
+                for (int m = NCOEF - 2; m >= 0; --m) {
+                    pm = b[m] + td * pm;
+                    p = (double)cf[m] + tau * p;
+                }
+                local_model = fmax(local_model, fabs(pm - ex));
                 local_err = fmax(local_err, fabs(p - ex));
             }
         }
@@ -679,8 +699,9 @@ daxm_status device_prepass(daxm_plan* p) {
     if (flags & FLAG_NAN_IN_WINDOW)
         return fail(nullptr, DAXM_ERR_GEOMETRY, "NaN tangent depth inside a pixel's contributing window");
     if (flags & FLAG_FIT_NAN) return fail(nullptr, DAXM_ERR_GEOMETRY, "NaN tangent depth at a depth-model node");
-    if (!(model_err <= 1e-6))
-        return fail(nullptr, DAXM_ERR_GEOMETRY, "cubic depth model error %.3g bins exceeds 1e-6", model_err);
+    if (!(model_err <= MODEL_ERR_MAX))
+        return fail(nullptr, DAXM_ERR_GEOMETRY, "depth model (degree %d) error %.3g bins exceeds %.3g", NCOEF - 1,
+                    model_err, MODEL_ERR_MAX);
     if (!(max_err <= 1e-3))
         return fail(nullptr, DAXM_ERR_GEOMETRY, "fp32 depth model error %.3g bins exceeds 1e-3", max_err);
     return DAXM_OK;
