@@ -218,7 +218,8 @@ def main():
     noise = (not cfg.sparse) if args.noise is None else args.noise
     g = synth.geometry(cfg)
     R = cfg.n
-    r0, r1 = rank * R // world, (rank + 1) * R // world
+    from paper_2201_13309_b200 import multi
+    r0, r1 = multi.my_band(rank, world, R)  # tile-aligned row band
     maps = synth.make_maps(cfg)
     stack = synth.stack_torch(maps, cfg.dtype, dev, noise=noise, rows=(r0, r1))
     plan = daxm.create(g, device=local, rows=(r0, r1))
@@ -265,18 +266,20 @@ def main():
 
     # optional all-gather of the output planes (timed separately, not in value)
     allgather_ms = None
-    if args.all_gather and world > 1 and R % world == 0:
-        gathered = torch.empty((world,) + tuple(out.shape), dtype=out.dtype, device=dev)
-        dist.all_gather_into_tensor(gathered, out)
+    if args.all_gather and world > 1:
+        bands = multi.row_bands(world, R)
+        full = multi.gather_rows(out, bands)  # warm
+        del full
         torch.cuda.synchronize(dev)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         dist.barrier()
         a.record(stream)
-        dist.all_gather_into_tensor(gathered, out)
+        full = multi.gather_rows(out, bands)
         b.record(stream)
         torch.cuda.synchronize(dev)
-        allgather_ms = a.elapsed_time(b)
-        del gathered
+        allgather_ms = multi.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
+        del full
+        torch.cuda.empty_cache()
 
     # end to end through the C ABI from pinned host buffers (copies inside the timed region)
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, K // 4)

@@ -20,7 +20,10 @@ constexpr int TILE_E = TILE_C + 1;  // pixel edge columns per tile (finite pixel
 constexpr int NCOEF = 3;            // depth model per edge point: polynomial of degree NCOEF-1 in wire travel
 // fp64 approximation error allowed for the depth model (bins); the fp32 evaluation adds ~ulp(M/2)
 constexpr double MODEL_ERR_MAX = NCOEF >= 4 ? 1e-6 : 2e-5;
-constexpr int COLS_PER_THREAD = 4;  // pixel walks per fast-kernel thread (1, 2 or 4)
+#ifndef DAXM_CPT
+#define DAXM_CPT 4
+#endif
+constexpr int COLS_PER_THREAD = DAXM_CPT;  // pixel walks per fast-kernel thread (1, 2 or 4)
 constexpr int N_CONSUMER_WARPS = (TILE_R / 32) * (TILE_C / COLS_PER_THREAD);
 #ifndef DAXM_MC
 #define DAXM_MC 4
