@@ -151,6 +151,17 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 2000;\n"
+        " @!p bra WAIT_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
 __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -241,10 +252,15 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
             ++v_issue;
         }
     };
-    // wait on an mbarrier phase; the producer keeps issuing loads meanwhile
+    // wait on an mbarrier phase; in warp 0 the producer lane keeps issuing loads meanwhile
+    // (warp-uniform split, so the other warps spin on a plain suspend-hinted try_wait)
     auto wait_bar = [&](uint32_t bar, uint32_t parity) {
-        while (!mbar_try(bar, parity))
-            if (producer) issue_loads();
+        if (warp == 0) {
+            while (!mbar_try(bar, parity))
+                if (producer) issue_loads();
+        } else {
+            mbar_wait_u32(bar, parity);
+        }
     };
     if (producer) issue_loads();
 
@@ -263,26 +279,35 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
         for (int m = 0; m < NCOEF; ++m)
             cb[e][m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + (h * CPT + e)) * TILE_R + r];
 
-    // zone state per walk (see above), the next point P1 = (nlo, nhi, nI) and the raw
+    // Zone state per walk (see above), the next point P1 = (nlo, nhi, nI) and the raw
     // inputs (tau, intensity) of the point after it, prefetched one transition ahead so
-    // the shared-memory latency is off the transition's critical path
+    // the shared-memory latency is off the transition's critical path.  Past the end of
+    // the window the prefetch index is clamped and the point is replaced by +INF depths,
+    // which makes c = 0 (rcp(inf) = 0) and stops further transitions: no branch.
     float zlo[CPT], zw[CPT], zF[CPT], zc[CPT], zd[CPT], zg[CPT], nlo[CPT], nhi[CPT], nI[CPT], Fp[CPT];
     float pt[CPT], pI[CPT];
-    int vn[CPT], vend[CPT];  // visit index of the prefetched point, one past the last point
+    int vn[CPT], vlast[CPT];  // visit index of the prefetched point, last point of the window
 #pragma unroll
     for (int w = 0; w < CPT; ++w) {
         zlo[w] = zw[w] = zF[w] = zc[w] = zd[w] = zg[w] = nI[w] = Fp[w] = pt[w] = pI[w] = 0.f;
         nlo[w] = nhi[w] = INF;
-        vn[w] = vend[w] = 0;
+        vn[w] = 1;
+        vlast[w] = 0;
     }
     // Input readiness is checked once per output chunk (warp-uniform): the
     // pre-pass recorded per tile, state and warp the furthest step loaded.
     int ready = -1;
+    uint32_t ready_bar = s_full + (NB - 1) * 8, ready_par = 1;  // barrier / parity of visit `ready`
     const int* vneed = a.vneed + (size_t)tile * (a.n_states + 1) * N_CONSUMER_WARPS + warp;
     auto wait_upto = [&](int vt) {
         while (ready < vt) {
             ++ready;
-            wait_bar(s_full + (ready & (NB - 1)) * 8, (ready / NB) & 1);
+            ready_bar += 8;
+            if (ready_bar == s_full + NB * 8) {
+                ready_bar = s_full;
+                ready_par ^= 1u;
+            }
+            wait_bar(ready_bar, ready_par);
         }
     };
     auto fetch_raw = [&](int w, int v) {
@@ -301,34 +326,32 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
         const float xc = fminf(x, zw[w]);
         return fmaf(xc, fmaf(zg[w], xc, zd[w]), fmaf(zc[w], x, zF[w]));
     };
-    // move walk w into the zone containing E
+    // one zone transition of walk w (E passed lo of the next point)
+    auto transition = [&](int w) {
+        // F(lo_{q+1}): x = lo_{q+1} - lo_q >= w_q in a separated zone, so
+        // F = F0 + c x + w (d + g w) = F0 + c x + w d / 2
+        zF[w] = fmaf(zc[w], nlo[w] - zlo[w], fmaf(0.5f * zw[w], zd[w], zF[w]));
+        zlo[w] = nlo[w];
+        zw[w] = nhi[w] - nlo[w];
+        const float s_cur = nlo[w] + nhi[w], I_cur = nI[w];
+        const bool more = vn[w] <= vlast[w];
+        float lo, hi;
+        depths(w, pt[w], lo, hi);
+        nlo[w] = more ? lo : INF;
+        nhi[w] = more ? hi : INF;
+        nI[w] = pI[w];
+        ++vn[w];
+        fetch_raw(w, min(vn[w], vlast[w]));
+        const float c = (sdir2 * (I_cur - nI[w])) * rcp_approx((nlo[w] + nhi[w]) - s_cur);
+        zd[w] = zc[w] - c;
+        zc[w] = c;
+        // g = (c - c_prev) / (2 w); w == 0 (POINT pixels) -> huge g, but xc <= w keeps xc*g*xc ~ 0
+        zg[w] = zd[w] * rcp_approx(-2.f * fmaxf(zw[w], 1e-30f));
+    };
     auto advance = [&](int w, float E) {
-        while (E > nlo[w]) {
-            zF[w] = evalF(w, nlo[w]);  // F(lo_{q+1})
-            const float cprev = zc[w];
-            zlo[w] = nlo[w];
-            zw[w] = nhi[w] - nlo[w];
-            const float s_cur = nlo[w] + nhi[w], I_cur = nI[w];
-            float c = 0.f;
-            if (vn[w] < vend[w]) {
-#if DAXM_PREFETCH
-                depths(w, pt[w], nlo[w], nhi[w]);
-                nI[w] = pI[w];
-                if (++vn[w] < vend[w]) fetch_raw(w, vn[w]);
-#else
-                fetch_raw(w, vn[w]);
-                depths(w, pt[w], nlo[w], nhi[w]);
-                nI[w] = pI[w];
-                ++vn[w];
-#endif
-                c = (sdir2 * (I_cur - nI[w])) * rcp_approx((nlo[w] + nhi[w]) - s_cur);
-            } else {
-                nlo[w] = nhi[w] = INF;
-            }
-            zc[w] = c;
-            zd[w] = cprev - c;
-            // g = (c - c_prev) / (2 w); w == 0 (POINT pixels) -> huge g, but xc <= w keeps xc*g*xc ~ 0
-            zg[w] = zd[w] * rcp_approx(-2.f * fmaxf(zw[w], 1e-30f));
+        if (E > nlo[w]) {  // zones are longer than a bin in practice: one transition, rarely more
+            transition(w);
+            while (E > nlo[w]) transition(w);
         }
     };
 
@@ -340,15 +363,13 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
         if (j < a.R && i < a.C) win = a.win[(size_t)(j - a.pre_row0) * a.C + i];
         if (win.y > win.x) {
             const int v0 = dir > 0 ? win.x - ti.k_lo : ti.k_hi - win.y;
-            vend[w] = v0 + (win.y - win.x + 1);
+            vlast[w] = v0 + (win.y - win.x);
             fetch_raw(w, v0);
             depths(w, pt[w], nlo[w], nhi[w]);
             nI[w] = pI[w];
             vn[w] = v0 + 1;
-#if DAXM_PREFETCH
             fetch_raw(w, v0 + 1);  // windows hold >= 2 points
-#endif
-            zlo[w] = nlo[w];  // virtual zone before point 0: F = 0
+            zlo[w] = nlo[w];       // virtual zone before point 0: F = 0
         }
     }
     int vt_next = vneed[2 * N_CONSUMER_WARPS];  // prefetched bound for chunk 0
@@ -377,13 +398,12 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
         wait_upto(vt);
         if (producer) issue_loads();
         uint32_t sa = out_base + b * PAIR_BUF_BYTES + sts_off;
-        const int q_end = min(MC, a.M - ch * MC);  // planes >= M are padding: no advance
+        // planes >= M (last chunk) are padding: their walks may read steps nobody waited for,
+        // harmless -- the TMA store clips them and releases are capped at `ready` below
 #pragma unroll 1
         for (int q = 0; q < MC; ++q, sa += 32 * TILE_C * 4) {
-            if (q < q_end) {
 #pragma unroll
-                for (int w = 0; w < CPT; ++w) advance(w, E);
-            }
+            for (int w = 0; w < CPT; ++w) advance(w, E);
             float o[CPT];
 #pragma unroll
             for (int w = 0; w < CPT; ++w) {
@@ -404,10 +424,18 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
         int my_min = INT_MAX;
 #pragma unroll
         for (int w = 0; w < CPT; ++w)
-            if (vn[w] < vend[w]) my_min = min(my_min, vn[w]);
-        const int target = min(__reduce_min_sync(0xffffffffu, my_min), nv);
+            if (vn[w] <= vlast[w]) my_min = min(my_min, vn[w]);  // slot vn may still be in flight (LDS)
+        // never release a slot this warp has not waited for (a premature arrive would
+        // complete the slot's previous phase for the producer)
+        const int target = min(min(__reduce_min_sync(0xffffffffu, my_min), nv), ready + 1);
         if (lane == 0) {
-            for (int v = released; v < target; ++v) mbar_arrive(&empty[v & (NB - 1)]);
+            if (released < target) {
+                uint32_t ea = s_empty + (uint32_t)(released & (NB - 1)) * 8;
+                for (int v = released; v < target; ++v) {
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(ea) : "memory");
+                    ea = (ea + 8 == s_empty + NB * 8) ? s_empty : ea + 8;
+                }
+            }
             mbar_arrive(&obar[pair * 4 + b]);  // pfull[b]
         }
         released = max(released, target);
