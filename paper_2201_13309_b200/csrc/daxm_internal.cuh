@@ -32,8 +32,18 @@ constexpr int N_CONSUMER_WARPS = (TILE_R / 32) * (TILE_C / COLS_PER_THREAD);
 #define DAXM_PREFETCH 1
 #endif
 constexpr int MC = DAXM_MC;         // depth planes per output chunk (one TMA store)
-constexpr int NB_U16 = 32;          // input ring slots (wire steps) for uint16 stacks (power of 2)
-constexpr int NB_F32 = 16;          // ... for float32 stacks
+#ifndef DAXM_NB_U16
+#define DAXM_NB_U16 32
+#endif
+#ifndef DAXM_NB_F32
+#define DAXM_NB_F32 16
+#endif
+#ifndef DAXM_OB
+#define DAXM_OB 2
+#endif
+constexpr int NB_U16 = DAXM_NB_U16;  // input ring slots (wire steps) for uint16 stacks (power of 2)
+constexpr int NB_F32 = DAXM_NB_F32;  // ... for float32 stacks
+constexpr int OUT_BUFS = DAXM_OB;    // output staging buffers per 32-row warp group (slack between its warps)
 constexpr int MAX_FAST_NV = 4096;   // fast path: steps streamed per tile (tau table in shared memory)
 constexpr int MAX_FAST_CHUNKS = 1024;  // fast path needs (M + MC - 1) / MC + 1 <= this (M <= 4092)
 constexpr int RING_WINDOW_CHUNKS = 1;  // a warp's input needs between two of its own chunk boundaries

@@ -113,10 +113,10 @@ template <typename T, int NB>
 struct FastSmem {
     static constexpr int IN_SLOT_BYTES = TILE_R * TILE_C * (int)sizeof(T);
     static constexpr int OFF_OUT = 0;                                   // [pair][2][MC][32][8] f32
-    static constexpr int OFF_IN = OFF_OUT + N_PAIRS * 2 * PAIR_BUF_BYTES;
+    static constexpr int OFF_IN = OFF_OUT + N_PAIRS * OUT_BUFS * PAIR_BUF_BYTES;
     static constexpr int OFF_BAR = OFF_IN + NB * IN_SLOT_BYTES;         // full[NB], empty[NB]
-    static constexpr int OFF_OBAR = OFF_BAR + 2 * NB * 8;               // pfull[pair][2], pfree[pair][2]
-    static constexpr int OFF_TAU = OFF_OBAR + 4 * N_PAIRS * 8;
+    static constexpr int OFF_OBAR = OFF_BAR + 2 * NB * 8;     // [pair][pfull[OUT_BUFS], pfree[OUT_BUFS]]
+    static constexpr int OFF_TAU = OFF_OBAR + 2 * OUT_BUFS * N_PAIRS * 8;
     static size_t bytes(int max_nv) { return (size_t)OFF_TAU + sizeof(float) * (size_t)(max_nv + 4) + 1024; }
 };
 
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
     const uint32_t s_tau = sbase + L::OFF_TAU, s_ring = sbase + L::OFF_IN;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
     uint64_t* empty = full + NB;
-    uint64_t* obar = reinterpret_cast<uint64_t*>(smem + L::OFF_OBAR);  // [pair][pfull0, pfull1, pfree0, pfree1]
+    uint64_t* obar = reinterpret_cast<uint64_t*>(smem + L::OFF_OBAR);  // [pair][pfull[OB], pfree[OB]]
     float* tau = reinterpret_cast<float*>(smem + L::OFF_TAU);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -228,10 +228,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
             mbar_init(&empty[s], N_CONSUMER_WARPS);
         }
         for (int pp = 0; pp < N_PAIRS; ++pp) {
-            mbar_init(&obar[pp * 4 + 0], WPG);
-            mbar_init(&obar[pp * 4 + 1], WPG);
-            mbar_init(&obar[pp * 4 + 2], 1);
-            mbar_init(&obar[pp * 4 + 3], 1);
+            for (int bb = 0; bb < OUT_BUFS; ++bb) {
+                mbar_init(&obar[pp * 2 * OUT_BUFS + bb], WPG);
+                mbar_init(&obar[pp * 2 * OUT_BUFS + OUT_BUFS + bb], 1);
+            }
         }
         fence_mbar_init();
     }
@@ -270,7 +270,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
     const float sdir2 = 2.f * a.sign * (float)dir;  // c = 2 s dir dI / (sum_{q+1} - sum_q)
     const float INF = __int_as_float(0x7f800000);
     const uint32_t px_off = (uint32_t)(r * TILE_C + h * CPT) * (uint32_t)sizeof(T);
-    const uint32_t s_pfull = s_obar + pair * 32, s_pfree = s_pfull + 16;
+    const uint32_t s_pfull = s_obar + pair * 2 * OUT_BUFS * 8, s_pfree = s_pfull + OUT_BUFS * 8;
 
     float cb[CPT + 1][NCOEF];  // edge points h*CPT .. h*CPT+CPT of this row
 #pragma unroll
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
     }
 
     int released = 0;
-    const uint32_t out_base = sbase + L::OFF_OUT + pair * 2 * PAIR_BUF_BYTES;
+    const uint32_t out_base = sbase + L::OFF_OUT + pair * OUT_BUFS * PAIR_BUF_BYTES;
     // [q][32 rows][8 cols] f32, 32-byte rows, SWIZZLE_32B (16-byte chunk ^= bit 7 of the offset);
     // q * 1024 leaves bit 7 alone, so the swizzled row offset is per-thread constant
     const uint32_t row_off = (uint32_t)(lane * (TILE_C * 4) + h * CPT * 4);
@@ -391,10 +391,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
     const int n_chunks = (a.M + MC - 1) / MC;
     float E = (float)(1 - a.m_ref);
     for (int ch = 0; ch < n_chunks; ++ch) {
-        const int b = ch & 1;
+        const int b = ch % OUT_BUFS;
         const int vt = vt_next;
         if (ch + 1 < n_chunks) vt_next = vneed[(ch + 3) * N_CONSUMER_WARPS];
-        if (ch >= 2) wait_bar(s_pfree + b * 8, ((ch >> 1) - 1) & 1);  // store ch-2 left buffer b
+        if (ch >= OUT_BUFS) wait_bar(s_pfree + b * 8, ((ch / OUT_BUFS) - 1) & 1);  // store ch-OB left buffer b
         wait_upto(vt);
         if (producer) issue_loads();
         uint32_t sa = out_base + b * PAIR_BUF_BYTES + sts_off;
@@ -436,15 +436,16 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
                     ea = (ea + 8 == s_empty + NB * 8) ? s_empty : ea + 8;
                 }
             }
-            mbar_arrive(&obar[pair * 4 + b]);  // pfull[b]
+            mbar_arrive(&obar[pair * 2 * OUT_BUFS + b]);  // pfull[b]
         }
         released = max(released, target);
         if (h == 0 && lane == 0) {  // the pair's storer
-            bulk_wait_read<0>();                                   // its store ch-1 has left buffer b^1
-            if (ch >= 1) mbar_arrive(&obar[pair * 4 + 2 + (b ^ 1)]);  // pfree[b^1]
-            wait_bar(s_pfull + b * 8, (ch >> 1) & 1);              // partner has written chunk ch
+            bulk_wait_read<OUT_BUFS - 2>();  // store ch+1-OB has left its buffer ...
+            if (ch + 1 >= OUT_BUFS)          // ... which chunk ch+1 reuses
+                mbar_arrive(&obar[pair * 2 * OUT_BUFS + OUT_BUFS + (ch + 1) % OUT_BUFS]);
+            wait_bar(s_pfull + b * 8, (ch / OUT_BUFS) & 1);  // partner has written chunk ch
             tma_store_3d(&out_map, col0, row0_local + pair * 32, ch * MC,
-                         smem + L::OFF_OUT + (pair * 2 + b) * PAIR_BUF_BYTES);
+                         smem + L::OFF_OUT + (pair * OUT_BUFS + b) * PAIR_BUF_BYTES);
             bulk_commit();
         }
         __syncwarp();
