@@ -98,6 +98,7 @@ struct DepositArgs {
     int row_begin, row_end;   // band (global rows)
     int pre_row0;             // first global row of win[]
     int tr0, n_tr, n_tc;      // tile rows covered (global tile-row index tr0 ..)
+    int tr_begin, tr_end;     // tile rows (relative) this launch processes (row-band pipelining)
     int m_ref;
     int point_mode;
     int nb;                   // input ring slots for this dtype (fast kernel)

@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
     extern __shared__ unsigned char smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
     unsigned char* smem = smem_raw + (sbase - smem_u32(smem_raw));
-    const int tile = blockIdx.x;
+    const int tile = a.tr_begin * a.n_tc + (int)blockIdx.x;
     const TileInfo ti = a.tiles[tile];
     const int tr = tile / a.n_tc, tc = tile % a.n_tc;
     const int row0 = (a.tr0 + tr) * TILE_R;  // global row of tile row 0
@@ -479,9 +479,10 @@ __device__ __forceinline__ float trapezoid_fraction(float lo0, float hi0, float 
 template <typename T>
 __global__ void __launch_bounds__(256) deposit_general(DepositArgs a, const T* __restrict__ stack,
                                                        float* __restrict__ out) {
-    const int tile = a.tile_list ? a.tile_list[blockIdx.x] : (int)blockIdx.x;
+    const int tile = a.tile_list ? a.tile_list[blockIdx.x] : a.tr_begin * a.n_tc + (int)blockIdx.x;
     const TileInfo ti = a.tiles[tile];
     const int tr = tile / a.n_tc, tc = tile % a.n_tc;
+    if (tr < a.tr_begin || tr >= a.tr_end) return;  // row-band launch: not this band
     const int rows = a.row_end - a.row_begin;
     const size_t plane = (size_t)rows * a.C;
     for (int pix = threadIdx.x; pix < TILE_R * TILE_C; pix += blockDim.x) {
@@ -577,7 +578,8 @@ size_t fast_smem_bytes(int dtype, int max_nv) {
 
 cudaError_t launch_deposit(const DepositArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
                            const void* stack, int dtype, float* out, bool fast_enabled, cudaStream_t st) {
-    const int n_tiles = a.n_tr * a.n_tc;
+    const int n_tiles = (a.tr_end - a.tr_begin) * a.n_tc;
+    if (n_tiles <= 0) return cudaSuccess;
     cudaError_t e = cudaSuccess;
     if (fast_enabled) {
         if (a.point_mode)

@@ -65,6 +65,8 @@ struct daxm_plan {
     size_t stack_buf_bytes = 0;
     float* d_out_buf = nullptr;
     size_t out_buf_bytes = 0;
+    cudaStream_t st_in = nullptr, st_out = nullptr;  // host-path pipeline streams
+    std::vector<cudaEvent_t> ev;
     daxm_plan_stats stats{};
     std::string err;
 };
@@ -496,6 +498,11 @@ void free_plan_memory(daxm_plan* p) {
     cudaFree(p->d_list_f32);
     cudaFree(p->d_stack_buf);
     cudaFree(p->d_out_buf);
+    if (p->st_in) cudaStreamDestroy(p->st_in);
+    if (p->st_out) cudaStreamDestroy(p->st_out);
+    p->st_in = p->st_out = nullptr;
+    for (cudaEvent_t ev : p->ev) cudaEventDestroy(ev);
+    p->ev.clear();
     p->d_t = p->d_wire = nullptr;
     p->d_tiles = nullptr;
     p->d_win = nullptr;
@@ -836,6 +843,8 @@ static DepositArgs make_args(const daxm_plan* p, int dtype) {
     a.tr0 = p->tr0;
     a.n_tr = p->n_tr;
     a.n_tc = p->n_tc;
+    a.tr_begin = 0;
+    a.tr_end = p->n_tr;
     a.m_ref = p->gc.m_ref;
     a.point_mode = p->gc.point_mode;
     a.sign = p->g.edge == DAXM_EDGE_TRAILING ? -1.f : 1.f;
@@ -896,13 +905,17 @@ static daxm_status encode_maps(daxm_plan* p, const void* d_stack, int dt, float*
     return DAXM_OK;
 }
 
-static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float* d_out, cudaStream_t st) {
+static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float* d_out, cudaStream_t st,
+                               int tr_begin = 0, int tr_end = -1) {
     const bool fast = fast_possible(p, dt);
     if (fast) {
         daxm_status s = encode_maps(p, d_stack, dt, d_out);
         if (s != DAXM_OK) return s;
     }
-    cudaError_t e = launch_deposit(make_args(p, dt), &p->in_map, &p->out_map, d_stack, dt, d_out, fast, st);
+    DepositArgs a = make_args(p, dt);
+    a.tr_begin = tr_begin;
+    a.tr_end = tr_end < 0 ? p->n_tr : tr_end;
+    cudaError_t e = launch_deposit(a, &p->in_map, &p->out_map, d_stack, dt, d_out, fast, st);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(p, DAXM_ERR_CUDA, "deposit launch: %s", cudaGetErrorString(e));
@@ -948,16 +961,67 @@ daxm_status daxm_reconstruct_host(daxm_plan* p, const void* h_stack, daxm_dtype 
         if (e != cudaSuccess) goto fail_cuda;
         p->out_buf_bytes = out_bytes;
     }
-    e = cudaMemcpyAsync(p->d_stack_buf, h_stack, in_bytes, cudaMemcpyHostToDevice, st);
-    if (e != cudaSuccess) goto fail_cuda;
+    // Row-band pipeline: band b's host->device copy, its deposit and its
+    // device->host copy run on three streams, so the two PCIe directions and the GPU overlap.
     {
-        daxm_status s = run_deposit(p, p->d_stack_buf, (int)dt, p->d_out_buf, st);
-        if (s != DAXM_OK) return s;
+        if (!p->st_in) {
+            e = cudaStreamCreateWithFlags(&p->st_in, cudaStreamNonBlocking);
+            if (e != cudaSuccess) goto fail_cuda;
+            e = cudaStreamCreateWithFlags(&p->st_out, cudaStreamNonBlocking);
+            if (e != cudaSuccess) goto fail_cuda;
+        }
+        const int n_bands = p->n_tr < 8 ? p->n_tr : 8;
+        while ((int)p->ev.size() < 2 * n_bands) {
+            cudaEvent_t ev;
+            e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+            if (e != cudaSuccess) goto fail_cuda;
+            p->ev.push_back(ev);
+        }
+        // the caller's stream must reach this point before the copies start
+        e = cudaEventRecord(p->ev[0], st);
+        if (e != cudaSuccess) goto fail_cuda;
+        e = cudaStreamWaitEvent(p->st_in, p->ev[0], 0);
+        if (e != cudaSuccess) goto fail_cuda;
+        const size_t es = dt == DAXM_U16 ? 2 : 4;
+        const size_t row_in = (size_t)p->C * es, row_out = (size_t)p->C * sizeof(float);
+        for (int b = 0; b < n_bands; ++b) {
+            const int t0 = b * p->n_tr / n_bands, t1 = (b + 1) * p->n_tr / n_bands;
+            int r0 = (p->tr0 + t0) * TILE_R - p->g.row_begin, r1 = (p->tr0 + t1) * TILE_R - p->g.row_begin;
+            r0 = r0 < 0 ? 0 : r0;
+            r1 = r1 > p->rows ? p->rows : r1;
+            if (r1 <= r0) continue;
+            const size_t w_in = (size_t)(r1 - r0) * row_in, w_out = (size_t)(r1 - r0) * row_out;
+            e = cudaMemcpy2DAsync(static_cast<char*>(p->d_stack_buf) + r0 * row_in, p->rows * row_in,
+                                  static_cast<const char*>(h_stack) + r0 * row_in, p->rows * row_in, w_in, p->S,
+                                  cudaMemcpyHostToDevice, p->st_in);
+            if (e != cudaSuccess) goto fail_cuda;
+            e = cudaEventRecord(p->ev[2 * b], p->st_in);
+            if (e != cudaSuccess) goto fail_cuda;
+            e = cudaStreamWaitEvent(st, p->ev[2 * b], 0);
+            if (e != cudaSuccess) goto fail_cuda;
+            {
+                daxm_status s = run_deposit(p, p->d_stack_buf, (int)dt, p->d_out_buf, st, t0, t1);
+                if (s != DAXM_OK) return s;
+            }
+            e = cudaEventRecord(p->ev[2 * b + 1], st);
+            if (e != cudaSuccess) goto fail_cuda;
+            e = cudaStreamWaitEvent(p->st_out, p->ev[2 * b + 1], 0);
+            if (e != cudaSuccess) goto fail_cuda;
+            e = cudaMemcpy2DAsync(reinterpret_cast<char*>(h_out) + r0 * row_out, p->rows * row_out,
+                                  reinterpret_cast<char*>(p->d_out_buf) + r0 * row_out, p->rows * row_out, w_out,
+                                  p->M, cudaMemcpyDeviceToHost, p->st_out);
+            if (e != cudaSuccess) goto fail_cuda;
+        }
+        // join: the caller's stream sees the last copy; then wait for completion
+        e = cudaEventRecord(p->ev[1], p->st_out);
+        if (e != cudaSuccess) goto fail_cuda;
+        e = cudaStreamWaitEvent(st, p->ev[1], 0);
+        if (e != cudaSuccess) goto fail_cuda;
+        e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) goto fail_cuda;
     }
-    e = cudaMemcpyAsync(h_out, p->d_out_buf, out_bytes, cudaMemcpyDeviceToHost, st);
-    if (e != cudaSuccess) goto fail_cuda;
-    e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) goto fail_cuda;
+    (void)in_bytes;
+    (void)out_bytes;
     return DAXM_OK;
 fail_cuda:
     cudaGetLastError();
