@@ -90,7 +90,8 @@ typedef struct {
     int64_t n_tiles;           /* deposit tiles covering the band                                         */
     int64_t general_tiles_u16; /* tiles the general (non-separated) deposit kernel handles, uint16 stacks  */
     int64_t general_tiles_f32; /* ... float32 stacks (the rest run the TMA-pipelined fast kernel)          */
-    int64_t nonseparated_tiles; /* tiles whose consecutive pixel-edge spans overlap (general kernel)      */
+    int64_t nonseparated_tiles; /* tiles not in the separated-span regime                                */
+    int64_t overlap_tiles;     /* of which every pixel's consecutive edge spans overlap (fast kernel, dual walk) */
     int64_t ring_need_max;     /* largest input-ring demand of a tile (fast path needs <= ring slots)     */
     int32_t tile_rows, tile_cols;
     double fit_max_err_bins;   /* max |fp32-stored cubic (fp32 tau) - exact fp64 depth| over every edge  */

@@ -48,7 +48,7 @@ class PlanStats(C.Structure):
         ("n_bins", C.c_int64), ("rows", C.c_int64), ("cols", C.c_int64), ("n_steps", C.c_int64),
         ("contrib_pairs", C.c_int64), ("contrib_pixels", C.c_int64), ("window_pairs", C.c_int64), ("staged_steps", C.c_int64), ("n_tiles", C.c_int64),
         ("general_tiles_u16", C.c_int64), ("general_tiles_f32", C.c_int64),
-        ("nonseparated_tiles", C.c_int64), ("ring_need_max", C.c_int64),
+        ("nonseparated_tiles", C.c_int64), ("overlap_tiles", C.c_int64), ("ring_need_max", C.c_int64),
         ("tile_rows", C.c_int32), ("tile_cols", C.c_int32),
         ("fit_max_err_bins", C.c_double), ("fit_model_err_bins", C.c_double), ("prepass_ms", C.c_double), ("device_bytes", C.c_int64),
     ]

@@ -73,10 +73,14 @@ struct TileInfo {
     int k_lo;       // first wire step (point) any pixel of the tile reads
     int k_hi;       // last wire step (point) any pixel of the tile reads (inclusive); k_hi < k_lo: empty
     int dir;        // +1: depth increases with the step index, -1: decreases
-    int separated;  // 1: every pixel's consecutive edge spans are disjoint (fast path valid)
+    int separated;  // deposit mode: MODE_SEPARATED / MODE_OVERLAP (fast kernel) or MODE_GENERAL
     int ring_need;  // input ring slots the fast kernel needs for this tile (deadlock-free bound)
     int pad;
 };
+
+// Per-tile deposit mode (pre-pass, fp64): every pixel's consecutive edge spans are
+// disjoint (SEPARATED) or every pixel's overlap (OVERLAP) -> fast kernel; else GENERAL.
+enum : int { MODE_GENERAL = 0, MODE_SEPARATED = 1, MODE_OVERLAP = 2 };
 
 // Pre-pass failure flags (device word, read back by the host).
 enum : unsigned {
@@ -101,6 +105,7 @@ struct DepositArgs {
     int tr_begin, tr_end;     // tile rows (relative) this launch processes (row-band pipelining)
     int m_ref;
     int point_mode;
+    int has_overlap;          // any MODE_OVERLAP tile (second fast-kernel launch)
     int nb;                   // input ring slots for this dtype (fast kernel)
     int max_nv;               // max steps any tile streams (tau table size)
     const int* vneed;         // [n_tiles][n_states + 1][8 warps] furthest visit index loaded by each state

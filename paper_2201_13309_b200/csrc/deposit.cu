@@ -192,7 +192,7 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
 // pair's first warp writes them with one TMA store; pairs never wait on each
 // other.  Each warp waits for its input once per chunk, up to the furthest
 // wire step its own pixels load in that chunk (pre-pass, a.vneed).
-template <typename T, int NB, bool POINT>
+template <typename T, int NB, bool POINT, int MODE>
 __global__ void __launch_bounds__(FAST_THREADS, 2)
     deposit_fast(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
                  const DepositArgs a) {
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
     const int tr = tile / a.n_tc, tc = tile % a.n_tc;
     const int row0 = (a.tr0 + tr) * TILE_R;  // global row of tile row 0
     // the general kernel owns this tile (same predicate as the plan's tile lists)
-    if (!(ti.separated && row0 >= a.row_begin && ti.ring_need <= NB)) return;
+    if (!(ti.separated == MODE && row0 >= a.row_begin && ti.ring_need <= NB)) return;
     const int col0 = tc * TILE_C;
     const int row0_local = row0 - a.row_begin;
     const int nv = ti.k_hi >= ti.k_lo ? ti.k_hi - ti.k_lo + 1 : 0;
@@ -298,7 +298,10 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
     // pre-pass recorded per tile, state and warp the furthest step loaded.
     int ready = -1;
     uint32_t ready_bar = s_full + (NB - 1) * 8, ready_par = 1;  // barrier / parity of visit `ready`
-    const int* vneed = a.vneed + (size_t)tile * (a.n_states + 1) * N_CONSUMER_WARPS + warp;
+    constexpr int VN = N_CONSUMER_WARPS + 1;  // per state: 8 warps + the tile-wide max
+    const int* vneed = a.vneed + (size_t)tile * (a.n_states + 1) * VN + warp;
+    const int* vneed_tile = a.vneed + (size_t)tile * (a.n_states + 1) * VN + N_CONSUMER_WARPS;
+    bool idle = false;  // all of this warp's walks finished: follow the tile-wide horizon
     auto wait_upto = [&](int vt) {
         while (ready < vt) {
             ++ready;
@@ -355,9 +358,117 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
         }
     };
 
-    wait_upto(vneed[0]);
+    // ---- dual mode (MODE_OVERLAP tiles: any pixel whose spans overlap somewhere): for every
+    // pair, trap_q = R_q - U_q with R_q a unit ramp over [lo_q, m_q], m_q = min(hi_q, lo_{q+1})
+    // (= z1..z2) and U_q over [M_q, hi_{q+1}], M_q = max(hi_q, lo_{q+1}) (= z3..z4).  The R
+    // ramps are disjoint and ordered, so are the U ramps: f = sum c_q R_q - sum c_q U_q is
+    // walked by a "lo walk" (ramp / gap phases) and a "hi walk" sharing one quadratic
+    // accumulator F = F0 + f0 x + (sL - sU) x^2 / 2 between consecutive events.
+    float oz0[CPT], oF0[CPT], of0[CPT], osL[CPT], osU[CPT];
+    float llo[CPT], lhi[CPT], lI[CPT], lev[CPT];         // lo walk: point A, next event
+    float hlo[CPT], hhi[CPT], hI[CPT], hev[CPT], hsl[CPT];  // hi walk: point A, next event, pending slope
+    int lvn[CPT], hvn[CPT];                              // next visit index to load
+    bool lramp[CPT], hramp[CPT];                         // lo walk in a ramp / hi walk before a ramp
 #pragma unroll
     for (int w = 0; w < CPT; ++w) {
+        oz0[w] = oF0[w] = of0[w] = osL[w] = osU[w] = lI[w] = hI[w] = hsl[w] = 0.f;
+        llo[w] = lhi[w] = hlo[w] = hhi[w] = lev[w] = hev[w] = INF;
+        lvn[w] = hvn[w] = 1;
+        lramp[w] = hramp[w] = false;
+    }
+    auto load_pt = [&](int w, int v, float& lo, float& hi, float& I) {
+        depths(w, lds_f32(s_tau + 4u * (uint32_t)v), lo, hi);
+        I = lds_px<T>(s_ring + (uint32_t)(v & (NB - 1)) * (uint32_t)L::IN_SLOT_BYTES + px_off +
+                      (uint32_t)(w * sizeof(T)));
+    };
+    // load the point B after A = (alo, ahi, aI) (clamped; INF past the window) and return
+    // c_AB / 2 * (...) pieces: c = s dir (I_A - I_B) / Area, Area = (hi_B + M - m - lo_A) / 2
+    auto pair_load = [&](int w, float& alo, float& ahi, float& aI, int& vnx, float& m, float& M, float& hb,
+                         float& c) -> bool {
+        const bool more = vnx <= vlast[w];
+        float blo, bhi, bI;
+        load_pt(w, min(vnx, vlast[w]), blo, bhi, bI);
+        ++vnx;
+        m = fminf(ahi, blo);
+        M = fmaxf(ahi, blo);
+        hb = bhi;
+        c = (sdir2 * (aI - bI)) * rcp_approx((bhi + M) - (m + alo));
+        alo = more ? blo : INF;
+        ahi = more ? bhi : INF;
+        aI = bI;
+        return more;
+    };
+    auto lo_event = [&](int w) {
+        if (!lramp[w]) {  // ramp R_q starts at lo_A: it ends at m_q
+            float m, M, hb, c;
+            const float a_lo = llo[w];
+            const bool more = pair_load(w, llo[w], lhi[w], lI[w], lvn[w], m, M, hb, c);
+            osL[w] = more ? c * rcp_approx(m - a_lo) : 0.f;
+            lev[w] = more ? m : INF;
+            lramp[w] = more;
+        } else {          // ramp ends: gap until the next ramp starts at lo_{q+1}
+            osL[w] = 0.f;
+            lev[w] = llo[w];
+            lramp[w] = false;
+        }
+    };
+    auto hi_event = [&](int w) {
+        if (!hramp[w]) {  // U_{q-1} ended at hi_A: gap until M_q, then U_q rises to hi_{q+1}
+            float m, M, hb, c;
+            const bool more = pair_load(w, hlo[w], hhi[w], hI[w], hvn[w], m, M, hb, c);
+            osU[w] = 0.f;
+            hsl[w] = more ? c * rcp_approx(hb - M) : 0.f;
+            hev[w] = more ? M : INF;
+            hramp[w] = more;
+        } else {          // U_q starts at M_q
+            osU[w] = hsl[w];
+            hev[w] = hhi[w];
+            hramp[w] = false;
+        }
+    };
+    auto advance_o = [&](int w, float E) {
+        while (true) {
+            const float k = fminf(lev[w], hev[w]);
+            if (!(E > k)) break;
+            const float Lz = k - oz0[w], sl = osL[w] - osU[w];
+            oF0[w] = fmaf(Lz, fmaf(0.5f * sl, Lz, of0[w]), oF0[w]);
+            of0[w] = fmaf(sl, Lz, of0[w]);
+            oz0[w] = k;
+            if (lev[w] <= hev[w])
+                lo_event(w);
+            else
+                hi_event(w);
+        }
+    };
+    auto evalF_o = [&](int w, float E) -> float {
+        const float x = E - oz0[w];
+        return fmaf(x, fmaf(0.5f * (osL[w] - osU[w]), x, of0[w]), oF0[w]);
+    };
+
+    wait_upto(vneed[0]);
+    if constexpr (MODE == MODE_OVERLAP) {
+#pragma unroll
+        for (int w = 0; w < CPT; ++w) {
+            const int i = col0 + h * CPT + w;
+            int2 win = make_int2(0, 0);
+            if (j < a.R && i < a.C) win = a.win[(size_t)(j - a.pre_row0) * a.C + i];
+            if (win.y > win.x) {
+                const int v0 = dir > 0 ? win.x - ti.k_lo : ti.k_hi - win.y;
+                vlast[w] = v0 + (win.y - win.x);
+                load_pt(w, v0, llo[w], lhi[w], lI[w]);
+                hlo[w] = llo[w];
+                hhi[w] = lhi[w];
+                hI[w] = lI[w];
+                lvn[w] = hvn[w] = v0 + 1;
+                lev[w] = llo[w];  // first rising ramp starts at lo_0
+                hev[w] = hhi[w];  // no falling ramp before hi_0
+                oz0[w] = llo[w];  // F = 0 before the first event
+            }
+        }
+    }
+#pragma unroll
+    for (int w = 0; w < CPT; ++w) {
+        if constexpr (MODE != MODE_SEPARATED) break;
         const int i = col0 + h * CPT + w;
         int2 win = make_int2(0, 0);
         if (j < a.R && i < a.C) win = a.win[(size_t)(j - a.pre_row0) * a.C + i];
@@ -372,14 +483,19 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
             zlo[w] = nlo[w];       // virtual zone before point 0: F = 0
         }
     }
-    int vt_next = vneed[2 * N_CONSUMER_WARPS];  // prefetched bound for chunk 0
+    int vt_next = vneed[2 * VN], vt_next_tile = vneed_tile[2 * VN];  // prefetched bounds for chunk 0
     {
-        wait_upto(vneed[N_CONSUMER_WARPS]);
+        wait_upto(vneed[VN]);
         const float E0 = (float)(0 - a.m_ref);
 #pragma unroll
-        for (int w = 0; w < CPT; ++w) advance(w, E0);
+        for (int w = 0; w < CPT; ++w) {
+            if constexpr (MODE == MODE_OVERLAP)
+                advance_o(w, E0);
+            else
+                advance(w, E0);
+        }
 #pragma unroll
-        for (int w = 0; w < CPT; ++w) Fp[w] = evalF(w, E0);
+        for (int w = 0; w < CPT; ++w) Fp[w] = MODE == MODE_OVERLAP ? evalF_o(w, E0) : evalF(w, E0);
     }
 
     int released = 0;
@@ -392,8 +508,11 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
     float E = (float)(1 - a.m_ref);
     for (int ch = 0; ch < n_chunks; ++ch) {
         const int b = ch % OUT_BUFS;
-        const int vt = vt_next;
-        if (ch + 1 < n_chunks) vt_next = vneed[(ch + 3) * N_CONSUMER_WARPS];
+        const int vt = idle ? vt_next_tile : vt_next;
+        if (ch + 1 < n_chunks) {
+            vt_next = vneed[(ch + 3) * VN];
+            vt_next_tile = vneed_tile[(ch + 3) * VN];
+        }
         if (ch >= OUT_BUFS) wait_bar(s_pfree + b * 8, ((ch / OUT_BUFS) - 1) & 1);  // store ch-OB left buffer b
         wait_upto(vt);
         if (producer) issue_loads();
@@ -403,11 +522,16 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
 #pragma unroll 1
         for (int q = 0; q < MC; ++q, sa += 32 * TILE_C * 4) {
 #pragma unroll
-            for (int w = 0; w < CPT; ++w) advance(w, E);
+            for (int w = 0; w < CPT; ++w) {
+                if constexpr (MODE == MODE_OVERLAP)
+                    advance_o(w, E);
+                else
+                    advance(w, E);
+            }
             float o[CPT];
 #pragma unroll
             for (int w = 0; w < CPT; ++w) {
-                const float F = evalF(w, E);
+                const float F = MODE == MODE_OVERLAP ? evalF_o(w, E) : evalF(w, E);
                 o[w] = F - Fp[w];
                 Fp[w] = F;
             }
@@ -424,10 +548,17 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
         int my_min = INT_MAX;
 #pragma unroll
         for (int w = 0; w < CPT; ++w)
-            if (vn[w] <= vlast[w]) my_min = min(my_min, vn[w]);  // slot vn may still be in flight (LDS)
+            if constexpr (MODE == MODE_OVERLAP) {
+                const int vmin = min(lvn[w], hvn[w]);
+                if (vmin <= vlast[w]) my_min = min(my_min, vmin);
+            } else {
+                if (vn[w] <= vlast[w]) my_min = min(my_min, vn[w]);  // slot vn may still be in flight (LDS)
+            }
         // never release a slot this warp has not waited for (a premature arrive would
         // complete the slot's previous phase for the producer)
-        const int target = min(min(__reduce_min_sync(0xffffffffu, my_min), nv), ready + 1);
+        const int wmin = __reduce_min_sync(0xffffffffu, my_min);
+        idle = wmin == INT_MAX;
+        const int target = min(min(wmin, nv), ready + 1);
         if (lane == 0) {
             if (released < target) {
                 uint32_t ea = s_empty + (uint32_t)(released & (NB - 1)) * 8;
@@ -450,8 +581,12 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
         }
         __syncwarp();
     }
-    if (lane == 0)
-        for (int v = released; v < nv; ++v) mbar_arrive(&empty[v & (NB - 1)]);
+    // release the rest; an arrive for visit v must follow v's fill (else it would count toward
+    // the slot's previous phase), so wait for each visit first
+    for (int v = released; v < nv; ++v) {
+        wait_upto(v);
+        if (lane == 0) mbar_arrive(&empty[v & (NB - 1)]);
+    }
     if (h == 0 && lane == 0) bulk_wait<0>();
     if (producer) {
         while (v_issue < nv) issue_loads();  // others may still need the tail
@@ -551,23 +686,34 @@ __global__ void __launch_bounds__(256) deposit_general(DepositArgs a, const T* _
     }
 }
 
-template <typename T, int NB, bool POINT>
+template <typename T, int NB, bool POINT, int MODE>
 cudaError_t launch_fast(const CUtensorMap* in_map, const CUtensorMap* out_map, const DepositArgs& a, int n_tiles,
                         cudaStream_t st) {
     const size_t sm = FastSmem<T, NB>::bytes(a.max_nv);
     static bool attr_set = false;  // per template instance
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(deposit_fast<T, NB, POINT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(deposit_fast<T, NB, POINT, MODE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)FastSmem<T, NB>::bytes(MAX_FAST_NV));
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(deposit_fast<T, NB, POINT>, cudaFuncAttributePreferredSharedMemoryCarveout,
+        e = cudaFuncSetAttribute(deposit_fast<T, NB, POINT, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                  (int)cudaSharedmemCarveoutMaxShared);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
     if (sm > FastSmem<T, NB>::bytes(MAX_FAST_NV)) return cudaErrorInvalidValue;
-    deposit_fast<T, NB, POINT><<<n_tiles, FAST_THREADS, sm, st>>>(*in_map, *out_map, a);
+    deposit_fast<T, NB, POINT, MODE><<<n_tiles, FAST_THREADS, sm, st>>>(*in_map, *out_map, a);
     return cudaGetLastError();
+}
+
+template <typename T, int NB>
+cudaError_t launch_fast_modes(const CUtensorMap* in_map, const CUtensorMap* out_map, const DepositArgs& a,
+                              int n_tiles, cudaStream_t st) {
+    cudaError_t e = a.point_mode ? launch_fast<T, NB, true, MODE_SEPARATED>(in_map, out_map, a, n_tiles, st)
+                                 : launch_fast<T, NB, false, MODE_SEPARATED>(in_map, out_map, a, n_tiles, st);
+    if (e != cudaSuccess || !a.has_overlap) return e;
+    return a.point_mode ? launch_fast<T, NB, true, MODE_OVERLAP>(in_map, out_map, a, n_tiles, st)
+                        : launch_fast<T, NB, false, MODE_OVERLAP>(in_map, out_map, a, n_tiles, st);
 }
 
 }  // namespace
@@ -582,12 +728,8 @@ cudaError_t launch_deposit(const DepositArgs& a, const CUtensorMap* in_map, cons
     if (n_tiles <= 0) return cudaSuccess;
     cudaError_t e = cudaSuccess;
     if (fast_enabled) {
-        if (a.point_mode)
-            e = dtype == DAXM_U16 ? launch_fast<uint16_t, NB_U16, true>(in_map, out_map, a, n_tiles, st)
-                                  : launch_fast<float, NB_F32, true>(in_map, out_map, a, n_tiles, st);
-        else
-            e = dtype == DAXM_U16 ? launch_fast<uint16_t, NB_U16, false>(in_map, out_map, a, n_tiles, st)
-                                  : launch_fast<float, NB_F32, false>(in_map, out_map, a, n_tiles, st);
+        e = dtype == DAXM_U16 ? launch_fast_modes<uint16_t, NB_U16>(in_map, out_map, a, n_tiles, st)
+                              : launch_fast_modes<float, NB_F32>(in_map, out_map, a, n_tiles, st);
         if (e != cudaSuccess) return e;
         if (a.n_list == 0) return cudaSuccess;
     }

@@ -182,7 +182,7 @@ __global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire
         uf0 = uf1;
     }
     int2 w = make_int2(0, 0);
-    signed char dir = 0, sep = 1;
+    signed char dir = 0, sep = 3;
     if (first >= 0) {
         if (nan_inside) atomicOr(flags, FLAG_NAN_IN_WINDOW);
         if (j >= band_r0 && j < band_r1) {
@@ -197,7 +197,7 @@ __global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire
         // 1e-3-bin margin) and every trapezoid has area >= 1e-3 bins, in either
         // visiting order -- the condition for the fast deposit kernel's
         // piecewise-linear form.
-        bool pos = false, neg = false, sep_pos = true, sep_neg = true;
+        bool pos = false, neg = false, sep_pos = true, sep_neg = true, ovl_pos = true, ovl_neg = true;
         double pb = tangent_u(g, Qb, sb, wire + 3 * kb), pf = tangent_u(g, Qf, sf, wire + 3 * kb);
         for (int k = kb + 1; k <= ke; ++k) {
             double cb = tangent_u(g, Qb, sb, wire + 3 * k), cf = tangent_u(g, Qf, sf, wire + 3 * k);
@@ -208,12 +208,19 @@ __global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire
             const double area = 0.5 * ((lo1 + hi1) - (lo0 + hi0));
             sep_pos &= (hi0 <= lo1 - 1e-3) && (area >= 1e-3);
             sep_neg &= (hi1 <= lo0 - 1e-3) && (-area >= 1e-3);
+            // dual-walk mode (any span/sweep relation): rising ramp [lo_a, min(hi_a, lo_b)] and
+            // falling ramp [max(hi_a, lo_b), hi_b] of nonzero length, area >= 1e-3 bins
+            ovl_pos &= (fmin(hi0, lo1) >= lo0 + 1e-3) && (hi1 >= fmax(hi0, lo1) + 1e-3) &&
+                       (0.5 * (hi1 + fmax(hi0, lo1) - fmin(hi0, lo1) - lo0) >= 1e-3);
+            ovl_neg &= (fmin(hi1, lo0) >= lo1 + 1e-3) && (hi0 >= fmax(hi1, lo0) + 1e-3) &&
+                       (0.5 * (hi0 + fmax(hi1, lo0) - fmin(hi1, lo0) - lo1) >= 1e-3);
             pb = cb;
             pf = cf;
         }
         if (pos && neg) atomicOr(flags, FLAG_NONMONOTONE);
         dir = neg ? -1 : 1;
-        sep = (dir > 0 ? sep_pos : sep_neg) ? 1 : 0;
+        // bit 0: separated (single zone walk), bit 1: dual walk applicable
+        sep = ((dir > 0 ? sep_pos : sep_neg) ? 1 : 0) | ((dir > 0 ? ovl_pos : ovl_neg) ? 2 : 0);
         w = make_int2(kb, ke);
     }
     win[(size_t)jl * g.C + i] = w;
@@ -243,7 +250,7 @@ __global__ void __launch_bounds__(1024) tile_kernel(GeomConst g, const double* _
     const int tid = r * TILE_C + c;
     const int nthr = blockDim.x * blockDim.y;
     const int j = (tr0 + tr) * TILE_R + r, i = tc * TILE_C + c;
-    int kb = INT_MAX, ke = INT_MIN, dpos = 0, dneg = 0, nsep = 0;
+    int kb = INT_MAX, ke = INT_MIN, dpos = 0, dneg = 0, nsep = 0, novl = 0;
     long long pairs = 0;
     if (j < g.R && i < g.C && j >= pre_row0 && j < pre_row0 + pre_rows) {
         int2 w = win[(size_t)(j - pre_row0) * g.C + i];
@@ -253,17 +260,19 @@ __global__ void __launch_bounds__(1024) tile_kernel(GeomConst g, const double* _
             signed char d = pdir[(size_t)(j - pre_row0) * g.C + i];
             dpos = d > 0;
             dneg = d < 0;
-            nsep = psep[(size_t)(j - pre_row0) * g.C + i] ? 0 : 1;
+            const signed char m = psep[(size_t)(j - pre_row0) * g.C + i];
+            nsep = (m & 1) ? 0 : 1;
+            novl = (m & 2) ? 0 : 1;
             if (j >= band_r0 && j < band_r1) pairs = w.y - w.x;
         }
     }
-    __shared__ int s_kb, s_ke, s_pos, s_neg, s_nsep, s_need;
+    __shared__ int s_kb, s_ke, s_pos, s_neg, s_nsep, s_novl, s_need;
     __shared__ unsigned long long s_pairs;
     const bool track = n_states <= MAX_FAST_CHUNKS;
     if (tid == 0) {
         s_kb = INT_MAX;
         s_ke = INT_MIN;
-        s_pos = s_neg = s_nsep = 0;
+        s_pos = s_neg = s_nsep = s_novl = 0;
         s_need = 0;
         s_pairs = 0;
     }
@@ -283,6 +292,7 @@ __global__ void __launch_bounds__(1024) tile_kernel(GeomConst g, const double* _
         if (dpos) atomicOr(&s_pos, 1);
         if (dneg) atomicOr(&s_neg, 1);
         if (nsep) atomicOr(&s_nsep, 1);
+        if (novl) atomicOr(&s_novl, 1);
         atomicAdd(&s_pairs, (unsigned long long)pairs);
     }
     __syncthreads();
@@ -326,10 +336,13 @@ __global__ void __launch_bounds__(1024) tile_kernel(GeomConst g, const double* _
     __syncthreads();
     // furthest visit index any pixel of the tile loads by the end of each state (+1: fp32 rounding),
     // so the fast kernel can wait for its input once per output chunk
+    // [state][warp 0..7, tile-wide max]: a warp whose pixels are all finished (or that has none)
+    // follows the tile-wide horizon so it keeps releasing ring slots in step with the others
     if (track)
-        for (int q = tid; q < (n_states + 1) * N_CONSUMER_WARPS; q += nthr) {
-            const int hi = s_w[q];
-            vneed[(size_t)tile * (n_states + 1) * N_CONSUMER_WARPS + q] =
+        for (int q = tid; q < (n_states + 1) * (N_CONSUMER_WARPS + 1); q += nthr) {
+            const int st = q / (N_CONSUMER_WARPS + 1), wq = q % (N_CONSUMER_WARPS + 1);
+            const int hi = wq < N_CONSUMER_WARPS ? s_w[st * N_CONSUMER_WARPS + wq] : s_v[st];
+            vneed[(size_t)tile * (n_states + 1) * (N_CONSUMER_WARPS + 1) + q] =
                 (s_kb == INT_MAX || hi == INT_MIN) ? -1 : min(hi + 2, s_ke - s_kb);  // +1 prefetch, +1 fp32
         }
     if (track && s_kb != INT_MAX)
@@ -348,15 +361,16 @@ __global__ void __launch_bounds__(1024) tile_kernel(GeomConst g, const double* _
             ti.k_lo = 0;
             ti.k_hi = -1;
             ti.dir = 1;
-            ti.separated = 1;
+            ti.separated = MODE_SEPARATED;
             ti.ring_need = 0;
         } else {
             ti.k_lo = k_lo;
             ti.k_hi = k_hi;
             ti.t_ref = 0.5 * (t[k_lo] + t[k_hi]);
             ti.dir = tdir;
-            ti.separated = s_nsep ? 0 : 1;
-            ti.ring_need = track ? s_need : INT_MAX;
+            ti.separated = !s_nsep ? MODE_SEPARATED : !s_novl ? MODE_OVERLAP : MODE_GENERAL;
+            // the overlap walk's hi ramps lag the lo ramps by up to two points
+            ti.ring_need = track ? s_need + (ti.separated == MODE_OVERLAP ? 2 : 0) : INT_MAX;
             if (s_pos && s_neg) atomicOr(flags, FLAG_MIXED_DIR);
             // staged steps, only for tiles that intersect the band
             int tj0 = (tr0 + tr) * TILE_R, tj1 = tj0 + TILE_R;
@@ -624,7 +638,7 @@ daxm_status device_prepass(daxm_plan* p) {
         const size_t tsm =
             n_states <= MAX_FAST_CHUNKS ? sizeof(int) * (2 + N_CONSUMER_WARPS) * (size_t)(n_states + 1) : 0;
         if (n_states <= MAX_FAST_CHUNKS)
-            CK(cudaMalloc(&p->d_vneed, sizeof(int) * n_tiles * (n_states + 1) * N_CONSUMER_WARPS));
+            CK(cudaMalloc(&p->d_vneed, sizeof(int) * n_tiles * (n_states + 1) * (N_CONSUMER_WARPS + 1)));
         if (tsm > 48 * 1024)
             CK(cudaFuncSetAttribute(tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
         tile_kernel<<<(unsigned)n_tiles, dim3(TILE_C, TILE_R), tsm>>>(
@@ -677,13 +691,14 @@ daxm_status device_prepass(daxm_plan* p) {
         std::vector<int> lu, lf;
         for (size_t q = 0; q < n_tiles; ++q) {
             const TileInfo& ti = ht[q];
-            if (!ti.separated) ++st.nonseparated_tiles;
+            if (ti.separated != MODE_SEPARATED) ++st.nonseparated_tiles;
+            if (ti.separated == MODE_OVERLAP) ++st.overlap_tiles;
             if (ti.k_hi >= ti.k_lo) st.ring_need_max = std::max<int64_t>(st.ring_need_max, ti.ring_need);
             if (ti.k_hi >= ti.k_lo) p->max_nv = std::max(p->max_nv, ti.k_hi - ti.k_lo + 1);
             // TMA boxes start at the tile's first row; a tile that starts above the band
             // (band start not a multiple of TILE_R) would need a negative coordinate -> general kernel
             const int tile_row0 = (p->tr0 + (int)(q / p->n_tc)) * TILE_R;
-            const bool sep = ti.separated != 0 && tile_row0 >= g.row_begin;
+            const bool sep = ti.separated != MODE_GENERAL && tile_row0 >= g.row_begin;
             if (!(sep && ti.ring_need <= NB_U16)) lu.push_back((int)q);
             if (!(sep && ti.ring_need <= NB_F32)) lf.push_back((int)q);
         }
@@ -826,6 +841,7 @@ static DepositArgs make_args(const daxm_plan* p, int dtype) {
     a.tile_list = dtype == DAXM_U16 ? p->d_list_u16 : p->d_list_f32;
     a.n_list = dtype == DAXM_U16 ? p->n_list_u16 : p->n_list_f32;
     a.nb = dtype == DAXM_U16 ? NB_U16 : NB_F32;
+    a.has_overlap = p->stats.overlap_tiles > 0;
     a.max_nv = p->max_nv;
     a.vneed = p->d_vneed;
     a.n_states = p->n_states;
