@@ -139,6 +139,34 @@ daxm_status daxm_reconstruct(daxm_plan *p, const void *d_stack, daxm_dtype dt, f
 daxm_status daxm_reconstruct_host(daxm_plan *p, const void *h_stack, daxm_dtype dt, float *h_out,
                                   void *cuda_stream);
 
+/* daxm_set_cutoff -- intensity cutoff ("d_cutoff", kernel setTwo argument; the
+ * pixel-percentage experiment).  Reading R14: with enable != 0 a
+ * pixel is reconstructed only if its intensity in the FIRST wire-step image, I_0(p),
+ * compared in float32, is >= cutoff; every other pixel's output column is 0 and the
+ * pixel's inputs are not processed (a tile with no such pixel reads no wire-step planes).
+ * enable == 0 (the default) reconstructs every pixel.  Applies to later daxm_reconstruct /
+ * daxm_reconstruct_host calls on this plan.  Errors: INVALID_ARGUMENT (NaN cutoff). */
+daxm_status daxm_set_cutoff(daxm_plan *p, int enable, double cutoff);
+
+/* daxm_select_cutoff -- the cutoff that keeps a fraction of the plan's pixels: *cutoff =
+ * the k-th largest I_0(p) over the plan's rows x C pixels, k = ceil(fraction * n) (>= 1),
+ * so that at least k pixels pass daxm_set_cutoff(p, 1, *cutoff) (more on ties).  NaN
+ * intensities rank lowest.  d_stack: device stack as for daxm_reconstruct (only plane 0 is
+ * read).  Exact (radix select on the value's bits, on the device); synchronises the stream.
+ * Errors: INVALID_ARGUMENT (NULL pointers, dtype, fraction outside (0, 1]), OUT_OF_MEMORY,
+ * CUDA. */
+daxm_status daxm_select_cutoff(daxm_plan *p, const void *d_stack, daxm_dtype dtype, double fraction, double *cutoff,
+                               void *cuda_stream);
+
+/* daxm_depth_profile -- per-depth-bin total intensity of a reconstruction (the paper's
+ * second output, image_set.depth_intensity, P:L208 / image_depth_intensity):
+ * d_profile[m] = sum over the plan's rows and all columns of d_out[m][row][col], in fp64.
+ * d_out: device [M][rows][C] float32 as written by daxm_reconstruct; d_profile: device
+ * double[M], overwritten.  Stream ordered, no allocation.  For a row-sharded multi-GPU run
+ * the per-rank profiles add up (an all-reduce of M doubles).
+ * Errors: INVALID_ARGUMENT (NULL pointers), CUDA. */
+daxm_status daxm_depth_profile(daxm_plan *p, const float *d_out, double *d_profile, void *cuda_stream);
+
 /* Detail text for the last failing call on this plan ("" if none).  Valid until
  * the next call on the plan. */
 const char *daxm_last_error(const daxm_plan *p);

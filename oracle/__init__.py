@@ -11,6 +11,8 @@ Parity status of each exported function:
   oracle_trapezoid_cdf, oracle_deposit_pair    pinned (numeric integration, box overlap, brute force)
   oracle_reconstruct[_pixels]                  pinned (conservation, background, linearity,
                                                reversal identity, forward-model round trip)
+  select_cutoff, active_pixels (python)        pinned (order-statistic definition, tests/test_oracle_cutoff.py)
+  depth_profile (python)                       pinned (conservation: sum of the profile = sum of dI)
 """
 from __future__ import annotations
 
@@ -172,6 +174,36 @@ def reconstruct(g: dict, stack: np.ndarray, rows: tuple | None = None, n_threads
     if st != 0:
         raise ValueError("oracle_reconstruct: invalid argument")
     return out
+
+
+def active_pixels(first_image: np.ndarray, cutoff: float) -> np.ndarray:
+    """Intensity cutoff (d_cutoff; reading R14): a pixel is processed iff its
+    first wire-step intensity I_0, compared in float32, is >= cutoff."""
+    return np.asarray(first_image).astype(np.float32) >= np.float32(cutoff)
+
+
+def select_cutoff(first_image: np.ndarray, fraction: float) -> float:
+    """Pixel percentage (reading R14): the k-th largest I_0, k = ceil(fraction * n)
+    clamped to [1, n]; NaN ranks lowest.  Plain sort."""
+    import math
+    v = np.asarray(first_image, dtype=np.float64).ravel()
+    n = v.size
+    k = min(max(int(math.ceil(fraction * n)), 1), n)
+    v = np.where(np.isnan(v), -np.inf, v)
+    return float(np.sort(v)[::-1][k - 1])
+
+
+def reconstruct_cutoff(g: dict, stack: np.ndarray, cutoff: float, rows: tuple | None = None,
+                       n_threads: int = 0) -> np.ndarray:
+    """reconstruct() with the intensity cutoff: pixels below it are not processed (output 0)."""
+    out = reconstruct(g, stack, rows=rows, n_threads=n_threads)
+    out[:, ~active_pixels(np.asarray(stack)[0], cutoff)] = 0.0
+    return out
+
+
+def depth_profile(out: np.ndarray) -> np.ndarray:
+    """image_set.depth_intensity: per-bin total over all pixels, fp64."""
+    return np.asarray(out, dtype=np.float64).sum(axis=(1, 2))
 
 
 def max_threads() -> int:

@@ -75,6 +75,12 @@ def lib():
         L.daxm_reconstruct.restype = C.c_int
         L.daxm_reconstruct_host.argtypes = [P, P, C.c_int, P, P]
         L.daxm_reconstruct_host.restype = C.c_int
+        L.daxm_set_cutoff.argtypes = [P, C.c_int, C.c_double]
+        L.daxm_set_cutoff.restype = C.c_int
+        L.daxm_select_cutoff.argtypes = [P, P, C.c_int, C.c_double, C.POINTER(C.c_double), P]
+        L.daxm_select_cutoff.restype = C.c_int
+        L.daxm_depth_profile.argtypes = [P, P, P, P]
+        L.daxm_depth_profile.restype = C.c_int
         L.daxm_last_error.argtypes = [P]
         L.daxm_last_error.restype = C.c_char_p
         L.daxm_create_error.restype = C.c_char_p
@@ -133,11 +139,7 @@ class Plan:
     def reconstruct(self, stack, out=None, stream=None):
         """stack: CUDA tensor [S][rows][C] uint16 or float32 -> out [M][rows][C] float32 (CUDA)."""
         import torch
-        if not (stack.is_cuda and stack.is_contiguous()):
-            raise ValueError("stack must be a contiguous CUDA tensor")
-        dt = {torch.uint16: 0, torch.float32: 1}.get(stack.dtype)
-        if dt is None:
-            raise ValueError(f"unsupported stack dtype {stack.dtype}")
+        dt = self._dtype_of(stack)
         if out is None:
             out = torch.empty(self.output_shape(), dtype=torch.float32, device=stack.device)
         if not (out.is_cuda and out.is_contiguous() and out.dtype == torch.float32 and
@@ -148,6 +150,46 @@ class Plan:
         self._check(lib().daxm_reconstruct(self._h, C.c_void_p(stack.data_ptr()), dt, C.c_void_p(out.data_ptr()),
                                            C.c_void_p(stream.cuda_stream)))
         return out
+
+    @staticmethod
+    def _dtype_of(stack):
+        import torch
+        if not (stack.is_cuda and stack.is_contiguous()):
+            raise ValueError("stack must be a contiguous CUDA tensor")
+        dt = {torch.uint16: 0, torch.float32: 1}.get(stack.dtype)
+        if dt is None:
+            raise ValueError(f"unsupported stack dtype {stack.dtype}")
+        return dt
+
+    def set_cutoff(self, cutoff):
+        """Reconstruct only pixels with first-step intensity >= cutoff (None: all pixels)."""
+        self._check(lib().daxm_set_cutoff(self._h, 0 if cutoff is None else 1,
+                                          0.0 if cutoff is None else float(cutoff)))
+
+    def select_cutoff(self, stack, fraction, stream=None):
+        """The cutoff keeping `fraction` of the plan's pixels (k-th largest first-step intensity)."""
+        import torch
+        dt = self._dtype_of(stack)
+        if stream is None:
+            stream = torch.cuda.current_stream(stack.device)
+        val = C.c_double()
+        self._check(lib().daxm_select_cutoff(self._h, C.c_void_p(stack.data_ptr()), dt, float(fraction),
+                                             C.byref(val), C.c_void_p(stream.cuda_stream)))
+        return val.value
+
+    def depth_profile(self, out, profile=None, stream=None):
+        """Per-depth-bin total intensity of `out` ([M][rows][C] float32 CUDA) -> float64 CUDA [M]."""
+        import torch
+        if not (out.is_cuda and out.is_contiguous() and out.dtype == torch.float32 and
+                tuple(out.shape) == self.output_shape()):
+            raise ValueError("out must be the plan's contiguous float32 CUDA output [M][rows][C]")
+        if profile is None:
+            profile = torch.empty(self.n_bins, dtype=torch.float64, device=out.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(out.device)
+        self._check(lib().daxm_depth_profile(self._h, C.c_void_p(out.data_ptr()), C.c_void_p(profile.data_ptr()),
+                                             C.c_void_p(stream.cuda_stream)))
+        return profile
 
     def reconstruct_host(self, stack, out=None, stream=None):
         """Host (numpy or pinned CPU torch) stack -> host output, copies included (daxm_reconstruct_host)."""

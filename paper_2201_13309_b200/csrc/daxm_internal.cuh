@@ -111,9 +111,15 @@ struct DepositArgs {
     const int* vneed;         // [n_tiles][n_states + 1][8 warps] furthest visit index loaded by each state
     int n_states;             // (M + MC - 1) / MC + 1
     float sign;               // s: +1 leading, -1 trailing (reading R2)
+    const void* stack;        // band stack [S][rows][C] (plane 0 read for the intensity cutoff)
+    int use_cutoff;           // 1: only pixels with I_0 >= cutoff are reconstructed (reading R14)
+    float cutoff;
 };
 
-// Launchers (deposit.cu).
+// Launchers (deposit.cu, profile.cu, select.cu).
+cudaError_t select_cutoff(const void* plane0, int dtype, size_t n, unsigned long long k,
+                          unsigned long long* d_hist, cudaStream_t st, double* cutoff);
+cudaError_t launch_depth_profile(const float* out, int M, size_t plane, double* profile, cudaStream_t st);
 size_t fast_smem_bytes(int dtype, int max_nv);
 cudaError_t launch_deposit(const DepositArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
                            const void* stack, int dtype, float* out, bool fast_enabled, cudaStream_t st);

@@ -192,8 +192,11 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
 // pair's first warp writes them with one TMA store; pairs never wait on each
 // other.  Each warp waits for its input once per chunk, up to the furthest
 // wire step its own pixels load in that chunk (pre-pass, a.vneed).
+#ifndef DAXM_MINB
+#define DAXM_MINB 2
+#endif
 template <typename T, int NB, bool POINT, int MODE>
-__global__ void __launch_bounds__(FAST_THREADS, 2)
+__global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
     deposit_fast(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
                  const DepositArgs a) {
     static_assert((NB & (NB - 1)) == 0, "ring size must be a power of two");
@@ -209,7 +212,8 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
     if (!(ti.separated == MODE && row0 >= a.row_begin && ti.ring_need <= NB)) return;
     const int col0 = tc * TILE_C;
     const int row0_local = row0 - a.row_begin;
-    const int nv = ti.k_hi >= ti.k_lo ? ti.k_hi - ti.k_lo + 1 : 0;
+    const int nv_all = ti.k_hi >= ti.k_lo ? ti.k_hi - ti.k_lo + 1 : 0;
+    int nv = nv_all;  // visits streamed: 0 when the intensity cutoff leaves no pixel of the tile
     const int dir = ti.dir;
 
     const uint32_t s_full = sbase + L::OFF_BAR, s_empty = s_full + NB * 8;
@@ -220,7 +224,6 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
     uint64_t* obar = reinterpret_cast<uint64_t*>(smem + L::OFF_OBAR);  // [pair][pfull[OB], pfree[OB]]
     float* tau = reinterpret_cast<float*>(smem + L::OFF_TAU);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool producer = threadIdx.x == 0;
     if (producer) {
         for (int s = 0; s < NB; ++s) {
@@ -235,11 +238,27 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
         }
         fence_mbar_init();
     }
-    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
+    for (int v = threadIdx.x; v < nv_all; v += blockDim.x) {
         const int k = dir > 0 ? ti.k_lo + v : ti.k_hi - v;
         tau[v] = (float)(a.t[k] - ti.t_ref);
     }
-    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pair = warp / WPG, h = warp % WPG;  // 32-row group, column group
+    const int r = pair * 32 + lane;  // tile row
+    const int j = row0 + r;          // global row
+    // intensity cutoff (f1, reading R14): a walk runs only if its pixel's first-step
+    // intensity reaches the cutoff; a tile with no such pixel streams no input at all
+    unsigned act = (1u << CPT) - 1u;
+    if (a.use_cutoff) {
+        act = 0u;
+        if (j < a.row_end) {
+            const T* s0 = static_cast<const T*>(a.stack) + (size_t)(j - a.row_begin) * a.C + col0 + h * CPT;
+#pragma unroll
+            for (int w = 0; w < CPT; ++w)
+                if (col0 + h * CPT + w < a.C && (float)s0[w] >= a.cutoff) act |= 1u << w;
+        }
+    }
+    if (!__syncthreads_or(act != 0u)) nv = 0;
     // producer state (thread 0 only): next visit index to load
     int v_issue = 0;
     auto issue_loads = [&]() {
@@ -264,9 +283,6 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
     };
     if (producer) issue_loads();
 
-    const int pair = warp / WPG, h = warp % WPG;  // 32-row group, column group
-    const int r = pair * 32 + lane;  // tile row
-    const int j = row0 + r;          // global row
     const float sdir2 = 2.f * a.sign * (float)dir;  // c = 2 s dir dI / (sum_{q+1} - sum_q)
     const float INF = __int_as_float(0x7f800000);
     const uint32_t px_off = (uint32_t)(r * TILE_C + h * CPT) * (uint32_t)sizeof(T);
@@ -303,6 +319,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
     const int* vneed_tile = a.vneed + (size_t)tile * (a.n_states + 1) * VN + N_CONSUMER_WARPS;
     bool idle = false;  // all of this warp's walks finished: follow the tile-wide horizon
     auto wait_upto = [&](int vt) {
+        vt = min(vt, nv - 1);
         while (ready < vt) {
             ++ready;
             ready_bar += 8;
@@ -452,7 +469,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
             const int i = col0 + h * CPT + w;
             int2 win = make_int2(0, 0);
             if (j < a.R && i < a.C) win = a.win[(size_t)(j - a.pre_row0) * a.C + i];
-            if (win.y > win.x) {
+            if (win.y > win.x && ((act >> w) & 1u)) {
                 const int v0 = dir > 0 ? win.x - ti.k_lo : ti.k_hi - win.y;
                 vlast[w] = v0 + (win.y - win.x);
                 load_pt(w, v0, llo[w], lhi[w], lI[w]);
@@ -472,7 +489,7 @@ __global__ void __launch_bounds__(FAST_THREADS, 2)
         const int i = col0 + h * CPT + w;
         int2 win = make_int2(0, 0);
         if (j < a.R && i < a.C) win = a.win[(size_t)(j - a.pre_row0) * a.C + i];
-        if (win.y > win.x) {
+        if (win.y > win.x && ((act >> w) & 1u)) {
             const int v0 = dir > 0 ? win.x - ti.k_lo : ti.k_hi - win.y;
             vlast[w] = v0 + (win.y - win.x);
             fetch_raw(w, v0);
@@ -633,7 +650,8 @@ __global__ void __launch_bounds__(256) deposit_general(DepositArgs a, const T* _
             cb[m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + eb) * TILE_R + r];
             cf[m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + ef) * TILE_R + r];
         }
-        const int kb = w.x, ke = w.y, n = ke - kb, dir = ti.dir;
+        const bool act = !a.use_cutoff || (float)stack[(size_t)jl * a.C + i] >= a.cutoff;  // reading R14
+        const int kb = w.x, ke = act ? w.y : w.x, n = ke - kb, dir = ti.dir;
         auto step_of = [&](int q) { return dir > 0 ? kb + q : ke - q; };
         auto point = [&](int q, float& lo, float& hi) {
             const float tau = (float)(a.t[step_of(q)] - ti.t_ref);

@@ -67,6 +67,9 @@ struct daxm_plan {
     size_t out_buf_bytes = 0;
     cudaStream_t st_in = nullptr, st_out = nullptr;  // host-path pipeline streams
     std::vector<cudaEvent_t> ev;
+    int use_cutoff = 0;  // intensity cutoff (f1, reading R14)
+    float cutoff = 0.f;
+    unsigned long long* d_hist = nullptr;  // cutoff selection scratch (256 counters)
     daxm_plan_stats stats{};
     std::string err;
 };
@@ -512,6 +515,7 @@ void free_plan_memory(daxm_plan* p) {
     cudaFree(p->d_list_f32);
     cudaFree(p->d_stack_buf);
     cudaFree(p->d_out_buf);
+    cudaFree(p->d_hist);
     if (p->st_in) cudaStreamDestroy(p->st_in);
     if (p->st_out) cudaStreamDestroy(p->st_out);
     p->st_in = p->st_out = nullptr;
@@ -864,6 +868,9 @@ static DepositArgs make_args(const daxm_plan* p, int dtype) {
     a.m_ref = p->gc.m_ref;
     a.point_mode = p->gc.point_mode;
     a.sign = p->g.edge == DAXM_EDGE_TRAILING ? -1.f : 1.f;
+    a.stack = nullptr;
+    a.use_cutoff = p->use_cutoff;
+    a.cutoff = p->cutoff;
     return a;
 }
 
@@ -931,6 +938,7 @@ static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float*
     DepositArgs a = make_args(p, dt);
     a.tr_begin = tr_begin;
     a.tr_end = tr_end < 0 ? p->n_tr : tr_end;
+    a.stack = d_stack;
     cudaError_t e = launch_deposit(a, &p->in_map, &p->out_map, d_stack, dt, d_out, fast, st);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -1043,6 +1051,53 @@ fail_cuda:
     cudaGetLastError();
     return fail(p, e == cudaErrorMemoryAllocation ? DAXM_ERR_OUT_OF_MEMORY : DAXM_ERR_CUDA, "host path: %s",
                 cudaGetErrorString(e));
+}
+
+daxm_status daxm_set_cutoff(daxm_plan* p, int enable, double cutoff) {
+    if (!p) return DAXM_ERR_INVALID_ARGUMENT;
+    p->err.clear();
+    if (enable && !(cutoff == cutoff)) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "cutoff is NaN");
+    p->use_cutoff = enable ? 1 : 0;
+    p->cutoff = (float)cutoff;
+    return DAXM_OK;
+}
+
+daxm_status daxm_select_cutoff(daxm_plan* p, const void* d_stack, daxm_dtype dt, double fraction, double* cutoff,
+                               void* cuda_stream) {
+    if (!p) return DAXM_ERR_INVALID_ARGUMENT;
+    p->err.clear();
+    if (!d_stack || !cutoff) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "NULL stack or cutoff pointer");
+    if (dt != DAXM_U16 && dt != DAXM_F32) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "unknown dtype %d", (int)dt);
+    if (!(fraction > 0.0 && fraction <= 1.0))
+        return fail(p, DAXM_ERR_INVALID_ARGUMENT, "fraction %g outside (0, 1]", fraction);
+    DeviceGuard guard(p->device);
+    if (!p->d_hist && cudaMalloc(&p->d_hist, 256 * sizeof(unsigned long long)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(p, DAXM_ERR_OUT_OF_MEMORY, "cutoff histogram");
+    }
+    const size_t n = (size_t)p->rows * p->C;
+    unsigned long long k = (unsigned long long)ceil(fraction * (double)n);
+    if (k < 1) k = 1;
+    if (k > n) k = n;
+    cudaError_t e = select_cutoff(d_stack, (int)dt, n, k, p->d_hist, (cudaStream_t)cuda_stream, cutoff);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(p, DAXM_ERR_CUDA, "cutoff selection: %s", cudaGetErrorString(e));
+    }
+    return DAXM_OK;
+}
+
+daxm_status daxm_depth_profile(daxm_plan* p, const float* d_out, double* d_profile, void* cuda_stream) {
+    if (!p) return DAXM_ERR_INVALID_ARGUMENT;
+    p->err.clear();
+    if (!d_out || !d_profile) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "NULL output or profile pointer");
+    DeviceGuard guard(p->device);
+    cudaError_t e = launch_depth_profile(d_out, p->M, (size_t)p->rows * p->C, d_profile, (cudaStream_t)cuda_stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(p, DAXM_ERR_CUDA, "depth profile launch: %s", cudaGetErrorString(e));
+    }
+    return DAXM_OK;
 }
 
 void daxm_destroy(daxm_plan* p) {

@@ -287,3 +287,97 @@ def test_host_path_pipelined_bands(daxm):
             hp = plan.reconstruct_host(torch.from_numpy(band).pin_memory())
             hp2 = plan.reconstruct_host(band)  # pageable host memory works too
             assert torch.equal(dev.cpu(), hp) and torch.equal(hp, hp2)
+
+
+@pytest.mark.parametrize("name,dtype", [("C2", "f32"), ("C3", "u16")])
+def test_depth_profile(daxm, name, dtype):
+    """daxm_depth_profile = the paper's image_set.depth_intensity: per-bin totals of the
+    reconstruction, checked against the oracle's totals."""
+    import torch
+    g = synth.geometry(name)
+    host = synth.stack_numpy(synth.make_maps(name), dtype, noise=True)
+    with daxm.create(g, device=0) as plan:
+        out = plan.reconstruct(torch.from_numpy(host).cuda())
+        prof = plan.depth_profile(out).cpu().numpy()
+        again = out.double().sum(dim=(1, 2)).cpu().numpy()
+    ref = oracle.reconstruct(g, host).sum(axis=(1, 2))
+    scale = parity.abs_dI(host).sum()
+    assert np.allclose(prof, again, rtol=1e-9, atol=1e-6 * scale)
+    assert np.abs(prof - ref).max() <= 1e-5 * scale
+
+
+@pytest.mark.parametrize("name,dtype", [("C2", "f32"), ("C3", "u16")])
+@pytest.mark.parametrize("fraction", [0.003, 0.25, 1.0])
+def test_select_cutoff_matches_oracle(daxm, name, dtype, fraction):
+    """Pixel percentage (reading R14): the device radix select returns exactly the
+    oracle's k-th largest first-step intensity."""
+    import torch
+    g = synth.geometry(name)
+    host = synth.stack_numpy(synth.make_maps(name), dtype, noise=True)
+    if dtype == "f32":
+        host[0, 5, 7] = np.nan
+        host[0, 9, 9] = -np.inf
+    with daxm.create(g, device=0) as plan:
+        c = plan.select_cutoff(torch.from_numpy(host).cuda(), fraction)
+    assert c == oracle.select_cutoff(host[0], fraction)
+
+
+@pytest.mark.parametrize("case", ["C2-f32", "C3-u16", "C3-u16-band", "C2-u16-general", "overlap-u16", "C3-u16-host"])
+def test_cutoff_parity(daxm, case, monkeypatch):
+    """Intensity cutoff (d_cutoff; reading R14): pixels below it are not processed and
+    read as 0, all others are bit-for-bit what the unrestricted run gives (same kernels); tiles
+    with no active pixel skip their input stream entirely."""
+    import torch
+    name, dtype = case.split("-")[:2]
+    rows = None
+    if name == "overlap":
+        g = synth.geometry("C2", n_rows=96, n_cols=64)
+        g["wire_xyz"] = synth.wire_positions(1601, t_range=(40.0, 1040.0))
+        g["depth_res"] = 0.5
+        rng = np.random.default_rng(18)
+        host = (3000 + rng.integers(-400, 400, (1601, 96, 64))).astype(np.uint16)
+    else:
+        g = synth.geometry(name)
+        host = synth.stack_numpy(synth.make_maps(name), dtype, noise=True)
+    if case.endswith("general"):
+        monkeypatch.setenv("DAXM_FORCE_GENERAL", "1")
+    if case.endswith("band"):
+        rows = (128, 901)
+    band = np.ascontiguousarray(host[:, rows[0]:rows[1]] if rows else host)
+    with daxm.create(g, device=0, rows=rows) as plan:
+        dev = torch.from_numpy(band).cuda()
+        full = plan.reconstruct(dev).cpu().numpy()
+        c = plan.select_cutoff(dev, 0.1)
+        plan.set_cutoff(c)
+        part = (plan.reconstruct_host(band) if case.endswith("host") else plan.reconstruct(dev).cpu()).numpy()
+        plan.set_cutoff(None)
+        again = plan.reconstruct(dev).cpu().numpy()
+    act = oracle.active_pixels(band[0], c)
+    assert 0.1 * act.size <= act.sum() < 0.5 * act.size
+    assert np.array_equal(part[:, act], full[:, act])
+    assert not part[:, ~act].any()
+    assert np.array_equal(again, full)
+    if name in ("C2", "overlap"):  # small enough for the whole oracle
+        ref = oracle.reconstruct_cutoff(g, host, c, rows=rows)
+        if rows:
+            ref = ref[:, rows[0]:rows[1]]
+        parity.check(part, ref, band, f"cutoff {case}")
+
+
+def test_cutoff_skips_inactive_tiles(daxm):
+    """A cutoff above every pixel but a few leaves almost every tile without work: the output is
+    exactly zero there and the few active pixels still match the unrestricted run."""
+    import torch
+    g = synth.geometry("C3")
+    host = synth.stack_numpy(synth.make_maps("C3"), "u16", noise=True)
+    host[0, 300:303, 500:502] = 65535
+    with daxm.create(g, device=0) as plan:
+        dev = torch.from_numpy(host).cuda()
+        full = plan.reconstruct(dev)
+        plan.set_cutoff(65535)
+        part = plan.reconstruct(dev)
+        torch.cuda.synchronize()
+    act = host[0] == 65535
+    assert act.sum() == 6
+    assert torch.equal(part[:, torch.from_numpy(act).cuda()], full[:, torch.from_numpy(act).cuda()])
+    assert int(torch.count_nonzero(part[:, torch.from_numpy(~act).cuda()])) == 0
