@@ -195,6 +195,7 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
 #ifndef DAXM_MINB
 #define DAXM_MINB 2
 #endif
+
 template <typename T, int NB, bool POINT, int MODE>
 __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
     deposit_fast(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
@@ -463,6 +464,7 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
     };
 
     wait_upto(vneed[0]);
+    unsigned live = 0u;  // walks with a non-empty window (and above the cutoff)
     if constexpr (MODE == MODE_OVERLAP) {
 #pragma unroll
         for (int w = 0; w < CPT; ++w) {
@@ -477,6 +479,7 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
                 hhi[w] = lhi[w];
                 hI[w] = lI[w];
                 lvn[w] = hvn[w] = v0 + 1;
+                live |= 1u << w;
                 lev[w] = llo[w];  // first rising ramp starts at lo_0
                 hev[w] = hhi[w];  // no falling ramp before hi_0
                 oz0[w] = llo[w];  // F = 0 before the first event
@@ -498,6 +501,7 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
             vn[w] = v0 + 1;
             fetch_raw(w, v0 + 1);  // windows hold >= 2 points
             zlo[w] = nlo[w];       // virtual zone before point 0: F = 0
+            live |= 1u << w;
         }
     }
     int vt_next = vneed[2 * VN], vt_next_tile = vneed_tile[2 * VN];  // prefetched bounds for chunk 0
@@ -523,6 +527,22 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
     const uint32_t sts_off = row_off ^ (((row_off >> 7) & 1u) << 4);
     const int n_chunks = (a.M + MC - 1) / MC;
     float E = (float)(1 - a.m_ref);
+    // a warp none of whose pixels contributes (outside every window, or below the cutoff)
+    // writes zeros into its slice of the staging buffers once and skips all per-plane work
+    const bool wlive = __any_sync(0xffffffffu, live != 0u);
+    if (!wlive) {
+        for (int b = 0; b < OUT_BUFS; ++b)
+#pragma unroll
+            for (int q = 0; q < MC; ++q) {
+                const uint32_t za = out_base + b * PAIR_BUF_BYTES + sts_off + q * (32 * TILE_C * 4);
+                if constexpr (CPT == 4)
+                    st_shared_v4(za, 0.f, 0.f, 0.f, 0.f);
+                else if constexpr (CPT == 2)
+                    asm volatile("st.shared.v2.f32 [%0], {%1, %1};" ::"r"(za), "f"(0.f) : "memory");
+                else
+                    asm volatile("st.shared.f32 [%0], %1;" ::"r"(za), "f"(0.f) : "memory");
+            }
+    }
     for (int ch = 0; ch < n_chunks; ++ch) {
         const int b = ch % OUT_BUFS;
         const int vt = idle ? vt_next_tile : vt_next;
@@ -537,7 +557,7 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
         // planes >= M (last chunk) are padding: their walks may read steps nobody waited for,
         // harmless -- the TMA store clips them and releases are capped at `ready` below
 #pragma unroll 1
-        for (int q = 0; q < MC; ++q, sa += 32 * TILE_C * 4) {
+        for (int q = 0; q < MC && wlive; ++q, sa += 32 * TILE_C * 4) {
 #pragma unroll
             for (int w = 0; w < CPT; ++w) {
                 if constexpr (MODE == MODE_OVERLAP)
