@@ -116,7 +116,8 @@ struct FastSmem {
     static constexpr int OFF_IN = OFF_OUT + N_PAIRS * OUT_BUFS * PAIR_BUF_BYTES;
     static constexpr int OFF_BAR = OFF_IN + NB * IN_SLOT_BYTES;         // full[NB], empty[NB]
     static constexpr int OFF_OBAR = OFF_BAR + 2 * NB * 8;     // [pair][pfull[OUT_BUFS], pfree[OUT_BUFS]]
-    static constexpr int OFF_TAU = OFF_OBAR + 2 * OUT_BUFS * N_PAIRS * 8;
+    static constexpr int OFF_SYNC = OFF_OBAR + 2 * OUT_BUFS * N_PAIRS * 8;  // v_issue, lock, cnt[pair][OB]
+    static constexpr int OFF_TAU = OFF_SYNC + 64;
     static size_t bytes(int max_nv) { return (size_t)OFF_TAU + sizeof(float) * (size_t)(max_nv + 4) + 1024; }
 };
 
@@ -151,7 +152,7 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+[[maybe_unused]] __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
     asm volatile(
         "{\n"
         " .reg .pred p;\n"
@@ -194,6 +195,12 @@ __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
 // wire step its own pixels load in that chunk (pre-pass, a.vneed).
 #ifndef DAXM_MINB
 #define DAXM_MINB 2
+#endif
+#ifndef DAXM_SHPROD
+#define DAXM_SHPROD 1
+#endif
+#ifndef DAXM_LASTSTORE
+#define DAXM_LASTSTORE 1
 #endif
 
 template <typename T, int NB, bool POINT, int MODE>
@@ -239,6 +246,8 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
         }
         fence_mbar_init();
     }
+    int* sync_words = reinterpret_cast<int*>(smem + L::OFF_SYNC);  // [0] v_issue, [1] lock, [2..] cnt
+    if (threadIdx.x < 16) sync_words[threadIdx.x] = 0;
     for (int v = threadIdx.x; v < nv_all; v += blockDim.x) {
         const int k = dir > 0 ? ti.k_lo + v : ti.k_hi - v;
         tau[v] = (float)(a.t[k] - ti.t_ref);
@@ -260,6 +269,33 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
         }
     }
     if (!__syncthreads_or(act != 0u)) nv = 0;
+    // Producer: issue the TMA loads of every visit whose ring slot all warps have released.
+#if DAXM_SHPROD
+    // Shared producer state under a shared-memory lock: thread 0 polls at chunk starts and
+    // lane 0 of ANY warp polls while it waits, so a starving warp fills the ring itself
+    // instead of waiting for warp 0 to reach its next poll.
+    volatile int* v_issue_sh = sync_words;
+    auto issue_loads = [&]() {
+        if (atomicCAS(&sync_words[1], 0, 1) != 0) return;  // another thread is issuing
+        int v = *v_issue_sh;
+        while (v < nv) {
+            const int s = v & (NB - 1);
+            if (v >= NB && !mbar_test(s_empty + s * 8, ((v / NB) - 1) & 1)) break;
+            mbar_arrive_expect_tx(&full[s], L::IN_SLOT_BYTES);
+            const int k = dir > 0 ? ti.k_lo + v : ti.k_hi - v;
+            tma_load_3d(smem + L::OFF_IN + s * L::IN_SLOT_BYTES, &in_map, col0, row0_local, k, &full[s]);
+            ++v;
+        }
+        *v_issue_sh = v;
+        __threadfence_block();
+        atomicExch(&sync_words[1], 0);
+    };
+    auto issued = [&]() { return *v_issue_sh; };
+    auto wait_bar = [&](uint32_t bar, uint32_t parity) {
+        while (!mbar_try(bar, parity))
+            if (lane == 0) issue_loads();
+    };
+#else
     // producer state (thread 0 only): next visit index to load
     int v_issue = 0;
     auto issue_loads = [&]() {
@@ -272,6 +308,7 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
             ++v_issue;
         }
     };
+    auto issued = [&]() { return v_issue; };
     // wait on an mbarrier phase; in warp 0 the producer lane keeps issuing loads meanwhile
     // (warp-uniform split, so the other warps spin on a plain suspend-hinted try_wait)
     auto wait_bar = [&](uint32_t bar, uint32_t parity) {
@@ -282,6 +319,7 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
             mbar_wait_u32(bar, parity);
         }
     };
+#endif
     if (producer) issue_loads();
 
     const float sdir2 = 2.f * a.sign * (float)dir;  // c = 2 s dir dI / (sum_{q+1} - sum_q)
@@ -520,6 +558,7 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
     }
 
     int released = 0;
+    [[maybe_unused]] unsigned pending = 0u;  // output buffers this warp stored and has not handed back (LASTSTORE)
     const uint32_t out_base = sbase + L::OFF_OUT + pair * OUT_BUFS * PAIR_BUF_BYTES;
     // [q][32 rows][8 cols] f32, 32-byte rows, SWIZZLE_32B (16-byte chunk ^= bit 7 of the offset);
     // q * 1024 leaves bit 7 alone, so the swizzled row offset is per-thread constant
@@ -596,6 +635,7 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
         const int wmin = __reduce_min_sync(0xffffffffu, my_min);
         idle = wmin == INT_MAX;
         const int target = min(min(wmin, nv), ready + 1);
+        __syncwarp();  // every lane's staging stores (and proxy fence) precede lane 0's signal
         if (lane == 0) {
             if (released < target) {
                 uint32_t ea = s_empty + (uint32_t)(released & (NB - 1)) * 8;
@@ -604,9 +644,34 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
                     ea = (ea + 8 == s_empty + NB * 8) ? s_empty : ea + 8;
                 }
             }
+#if DAXM_LASTSTORE
+            // The warp that completes chunk ch of its 32-row group last stores it, so no warp
+            // waits for its partner here.  A buffer is handed back (pfree) by whoever stored it,
+            // at that warp's next chunk end, once its bulk stores have been read out.
+            if (pending) {
+                bulk_wait_read<0>();
+#pragma unroll
+                for (int bb = 0; bb < OUT_BUFS; ++bb)
+                    if (pending & (1u << bb)) mbar_arrive(&obar[pair * 2 * OUT_BUFS + OUT_BUFS + bb]);
+                pending = 0u;
+            }
+            int old;
+            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                         : "=r"(old)
+                         : "r"(smem_u32(&sync_words[2 + pair * OUT_BUFS + b]))
+                         : "memory");
+            if (old % WPG == WPG - 1) {
+                tma_store_3d(&out_map, col0, row0_local + pair * 32, ch * MC,
+                             smem + L::OFF_OUT + (pair * OUT_BUFS + b) * PAIR_BUF_BYTES);
+                bulk_commit();
+                pending |= 1u << b;
+            }
+#else
             mbar_arrive(&obar[pair * 2 * OUT_BUFS + b]);  // pfull[b]
+#endif
         }
         released = max(released, target);
+#if !DAXM_LASTSTORE
         if (h == 0 && lane == 0) {  // the pair's storer
             bulk_wait_read<OUT_BUFS - 2>();  // store ch+1-OB has left its buffer ...
             if (ch + 1 >= OUT_BUFS)          // ... which chunk ch+1 reuses
@@ -616,6 +681,7 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
                          smem + L::OFF_OUT + (pair * OUT_BUFS + b) * PAIR_BUF_BYTES);
             bulk_commit();
         }
+#endif
         __syncwarp();
     }
     // release the rest; an arrive for visit v must follow v's fill (else it would count toward
@@ -624,11 +690,16 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
         wait_upto(v);
         if (lane == 0) mbar_arrive(&empty[v & (NB - 1)]);
     }
+#if DAXM_LASTSTORE
+    if (lane == 0) bulk_wait<0>();  // stores this warp issued
+#else
     if (h == 0 && lane == 0) bulk_wait<0>();
+#endif
     if (producer) {
-        while (v_issue < nv) issue_loads();  // others may still need the tail
+        while (issued() < nv) issue_loads();  // others may still need the tail
         // every issued load must land before the CTA may exit
-        for (int v = v_issue > NB ? v_issue - NB : 0; v < v_issue; ++v) mbar_wait(&full[v & (NB - 1)], (v / NB) & 1);
+        const int vi = issued();
+        for (int v = vi > NB ? vi - NB : 0; v < vi; ++v) mbar_wait(&full[v & (NB - 1)], (v / NB) & 1);
     }
 }
 
