@@ -14,8 +14,16 @@ namespace daxm {
 // their pixels in lock step); each thread owns 4 adjacent columns.  Tiles are
 // aligned to GLOBAL detector rows/cols, so a row-band plan reproduces the
 // full-detector plan bit for bit.
-constexpr int TILE_R = 128;
-constexpr int TILE_C = 8;
+#ifndef DAXM_TILE_R
+#define DAXM_TILE_R 128
+#endif
+#ifndef DAXM_TILE_C
+#define DAXM_TILE_C 8
+#endif
+constexpr int TILE_R = DAXM_TILE_R;  // multiple of 32
+constexpr int TILE_C = DAXM_TILE_C;  // 8 or 16: one tile row of output = 32 or 64 bytes
+static_assert(TILE_R % 32 == 0 && (TILE_C == 8 || TILE_C == 16), "tile shape");
+static_assert(TILE_R * TILE_C <= 1024, "pre-pass tile kernel: one thread per pixel");
 constexpr int TILE_E = TILE_C + 1;  // pixel edge columns per tile (finite pixels)
 constexpr int NCOEF = 3;            // depth model per edge point: polynomial of degree NCOEF-1 in wire travel
 // fp64 approximation error allowed for the depth model (bins); the fp32 evaluation adds ~ulp(M/2)

@@ -106,7 +106,7 @@ __device__ __forceinline__ float poly3(const float c[NCOEF], float tau) {
 constexpr int CPT = COLS_PER_THREAD;                          // pixel walks (columns) per thread
 constexpr int WPG = TILE_C / CPT;                             // warps per 32-row group
 constexpr int N_PAIRS = TILE_R / 32;                          // 32-row warp groups (32 rows x 8 cols each)
-constexpr int PAIR_BUF_BYTES = MC * 32 * TILE_C * 4;          // 4 KB: MC planes of a group's 32x8 block
+constexpr int PAIR_BUF_BYTES = MC * 32 * TILE_C * 4;          // MC planes of a group's 32 x TILE_C block
 constexpr int FAST_THREADS = N_CONSUMER_WARPS * 32;
 
 template <typename T, int NB>
@@ -143,6 +143,11 @@ __device__ __forceinline__ float rcp_approx(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+#ifndef DAXM_HINT
+#define DAXM_HINT 2000
+#endif
+#define DAXM_STR2(x) #x
+#define DAXM_STR(x) DAXM_STR2(x)
 __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -157,7 +162,7 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
         "{\n"
         " .reg .pred p;\n"
         "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 2000;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, " DAXM_STR(DAXM_HINT) ";\n"
         " @!p bra WAIT_%=;\n"
         "}\n" ::"r"(bar),
         "r"(parity)
@@ -166,7 +171,7 @@ __device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
 __device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, 2000;\n selp.u32 %0, 1, 0, p;\n}\n"
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, " DAXM_STR(DAXM_HINT) ";\n selp.u32 %0, 1, 0, p;\n}\n"
         : "=r"(ok)
         : "r"(bar), "r"(parity)
         : "memory");
@@ -560,10 +565,11 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
     int released = 0;
     [[maybe_unused]] unsigned pending = 0u;  // output buffers this warp stored and has not handed back (LASTSTORE)
     const uint32_t out_base = sbase + L::OFF_OUT + pair * OUT_BUFS * PAIR_BUF_BYTES;
-    // [q][32 rows][8 cols] f32, 32-byte rows, SWIZZLE_32B (16-byte chunk ^= bit 7 of the offset);
-    // q * 1024 leaves bit 7 alone, so the swizzled row offset is per-thread constant
+    // [q][32 rows][TILE_C cols] f32, 32- or 64-byte rows, SWIZZLE_32B / SWIZZLE_64B (16-byte
+    // chunk index ^= bits 7.. of the offset); a plane (32 rows) is a whole number of swizzle
+    // atoms, so the swizzled row offset is per-thread constant
     const uint32_t row_off = (uint32_t)(lane * (TILE_C * 4) + h * CPT * 4);
-    const uint32_t sts_off = row_off ^ (((row_off >> 7) & 1u) << 4);
+    const uint32_t sts_off = row_off ^ (((row_off >> 7) & (uint32_t)(TILE_C * 4 / 16 - 1)) << 4);
     const int n_chunks = (a.M + MC - 1) / MC;
     float E = (float)(1 - a.m_ref);
     // a warp none of whose pixels contributes (outside every window, or below the cutoff)
@@ -581,8 +587,23 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
                 else
                     asm volatile("st.shared.f32 [%0], %1;" ::"r"(za), "f"(0.f) : "memory");
             }
+        fence_proxy_async_smem();
     }
-    for (int ch = 0; ch < n_chunks; ++ch) {
+    // A 32-row group none of whose warps has work streams its zero planes straight from the
+    // (never rewritten) zero buffer -- no buffer hand-back, stores back to back -- and then
+    // only keeps releasing ring slots for the other groups (final release loop below).
+    int* group_live = sync_words + 2 + N_PAIRS * OUT_BUFS;  // [N_PAIRS], zeroed at start
+    if (lane == 0 && wlive) atomicOr(&group_live[pair], 1);
+    __syncthreads();
+    const bool dead_group = group_live[pair] == 0;
+    if (dead_group && h == 0 && lane == 0) {
+        for (int ch = 0; ch < n_chunks; ++ch) {
+            tma_store_3d(&out_map, col0, row0_local + pair * 32, ch * MC,
+                         smem + L::OFF_OUT + (pair * OUT_BUFS) * PAIR_BUF_BYTES);
+            bulk_commit();
+        }
+    }
+    for (int ch = 0; ch < n_chunks && !dead_group; ++ch) {
         const int b = ch % OUT_BUFS;
         const int vt = idle ? vt_next_tile : vt_next;
         if (ch + 1 < n_chunks) {

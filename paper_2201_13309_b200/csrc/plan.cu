@@ -918,7 +918,8 @@ static daxm_status encode_maps(daxm_plan* p, const void* d_stack, int dt, float*
         cuuint32_t box[3] = {(cuuint32_t)TILE_C, 32u, (cuuint32_t)MC};  // one warp pair's rows
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = enc(&p->out_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_out, dims, strides, box, estr,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, TILE_C == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                         CU_TENSOR_MAP_L2_PROMOTION_NONE,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(p, DAXM_ERR_CUDA, "cuTensorMapEncodeTiled(out) failed: %d", (int)r);
     }
