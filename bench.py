@@ -98,31 +98,50 @@ def workload_config(cfg, noise, world, parallelism_rows):
     }
 
 
-def cpu_oracle_rate(cfg, maps, g, noise, budget_s, max_pixels=1 << 20):
-    """Time the fp64 oracle (as it stands) on a random pixel sample of the workload."""
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_oracle_rate(cfg, maps, g, noise, budget_s, max_pixels=1 << 20, keep=4096):
+    """Time the fp64 oracle (as it stands) on a random pixel sample of the workload.
+
+    Returns the all-thread rate and its sample, the single-thread rate, and the first
+    `keep` sampled pixels with their oracle outputs (for the parity spot check)."""
     import numpy as np
 
     import oracle
     import synth
     rng = np.random.default_rng(12345)
     threads = oracle.max_threads()
+    kept = {}
 
-    def run(n):
+    def run(n, nt=threads):
         js = rng.integers(0, cfg.n, n)
         is_ = rng.integers(0, cfg.n, n)
         ser = synth.pixel_series(maps, js, is_, cfg.dtype, noise=noise)
         t0 = time.perf_counter()
-        oracle.reconstruct_pixels(g, js, is_, ser, n_threads=threads)
-        return time.perf_counter() - t0
+        o = oracle.reconstruct_pixels(g, js, is_, ser, n_threads=nt)
+        dt = time.perf_counter() - t0
+        kept.update(js=js[:keep], is_=is_[:keep], out=o[:keep].copy(), ser=ser[:keep].copy())
+        return dt
 
     n = 256
     t = run(n)
     while t < 0.5 and n < max_pixels:
         n *= 4
         t = run(n)
+    n1 = max(64, int(n * 0.1 * min(budget_s, 20.0) / max(t * threads, 1e-6)))  # ~10 % of the budget
+    t1 = run(n1, 1)
+    single = n1 * cfg.n_steps / t1
     n = int(min(max_pixels, max(n, n * budget_s / max(t, 1e-6))))
     t = run(n)
-    return n * cfg.n_steps / t, n, t, threads
+    return n * cfg.n_steps / t, n, t, threads, single, kept
 
 
 def run_reference(args):
@@ -191,6 +210,8 @@ def main():
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=3.0)
     ap.add_argument("--all-gather", action="store_true", help="also time an NCCL all-gather of the output planes")
+    ap.add_argument("--dtype", choices=["u16", "f32"], default=None,
+                    help="override the config's stack dtype (e.g. C5 in fp32, SURVEY §8(d))")
     ap.add_argument("--fraction", type=float, default=1.0,
                     help="pixel percentage (P:L299-303): reconstruct only this fraction of the pixels, the "
                          "brightest by first-step intensity (daxm_select_cutoff + daxm_set_cutoff)")
@@ -218,6 +239,9 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
 
     cfg = synth.get_config(args.config)
+    if args.dtype:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, dtype=args.dtype)
     noise = (not cfg.sparse) if args.noise is None else args.noise
     g = synth.geometry(cfg)
     R = cfg.n
@@ -263,6 +287,7 @@ def main():
     total_ms = t_start.elapsed_time(t_end)
     kern_ms = [a.elapsed_time(b) for a, b in ev]
     kern_avg = sum(kern_ms) / len(kern_ms)
+    kern_median = sorted(kern_ms)[len(kern_ms) // 2]
     # with a cutoff the input term is scaled by the active-pixel fraction (an estimate: the
     # active pixels' windows are not counted individually)
     alg_bytes = active * (st["contrib_pairs"] + st["contrib_pixels"]) * b_in + st["rows"] * st["cols"] * st["n_bins"] * 4
@@ -296,7 +321,8 @@ def main():
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, K // 4)
     if e2e_steps <= 0:
         return finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_max, achieved_min, value,
-                      units, st, clocks, r0, r1, alg_bytes, allgather_ms, None, (cutoff, active))
+                      units, st, clocks, r0, r1, alg_bytes, allgather_ms, None, (cutoff, active), out,
+                      kern_median)
     h_stack = stack.cpu().pin_memory()
     h_out = torch.empty(plan.output_shape(), dtype=torch.float32).pin_memory()
     del stack
@@ -321,11 +347,32 @@ def main():
     e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
            "ms_per_step": e2e_ms.item(), "path": "daxm_reconstruct_host, pinned host buffers"}
     return finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_max, achieved_min, value,
-                  units, st, clocks, r0, r1, alg_bytes, allgather_ms, e2e, (cutoff, active))
+                  units, st, clocks, r0, r1, alg_bytes, allgather_ms, e2e, (cutoff, active), out,
+                  kern_median)
+
+
+def parity_spot_check(out, kept, r0, cut):
+    """After timing, compare the timed output buffer with the oracle outputs the CPU-baseline
+    leg computed for its pixel sample (north_star tolerance: per bin 1e-4 * sum|dI|)."""
+    import numpy as np
+    import torch
+    if out is None or not kept or cut[0] is not None:
+        return None
+    js = kept["js"] - r0
+    ok = (js >= 0) & (js < out.shape[1])
+    js, is_ = js[ok], kept["is_"][ok]
+    gpu = out[:, torch.from_numpy(js).to(out.device), torch.from_numpy(is_).to(out.device)].double().cpu().numpy().T
+    ref = kept["out"][ok]
+    ser = kept["ser"][ok].astype(np.float64)
+    d = np.abs(np.diff(ser, axis=1)).sum(axis=1)
+    err = np.abs(gpu - ref).max(axis=1) / np.maximum(d, 1e-300)
+    err = np.where(d > 0, err, np.abs(gpu - ref).max(axis=1))
+    return {"pixels": int(len(js)), "max_bin_err_over_sum_abs_dI": float(err.max()), "tol": 1e-4,
+            "pass": bool(err.max() <= 1e-4), "what": "timed output buffer vs fp64 oracle at the CPU-baseline sample"}
 
 
 def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_max, achieved_min, value, units, st,
-           clocks, r0, r1, alg_bytes, allgather_ms, e2e, cut=(None, 1.0)):
+           clocks, r0, r1, alg_bytes, allgather_ms, e2e, cut=(None, 1.0), out=None, kern_median=None):
     import torch.distributed as dist
     if rank == 0:
         peak, peak_src = peak_hbm()
@@ -340,12 +387,15 @@ def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_ma
             except Exception:
                 traffic = None
         cpu = None
+        parity = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                rate, n_pix, t_s, cores = cpu_oracle_rate(cfg, maps, g, noise, args.cpu_budget_s)
+                rate, n_pix, t_s, cores, single, kept = cpu_oracle_rate(cfg, maps, g, noise, args.cpu_budget_s)
                 cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle",
                        "sample": f"{n_pix} random pixels x {cfg.n_steps} steps of {cfg.name} ({t_s:.1f} s, fp64 "
-                                 f"C oracle, OpenMP over pixels)"}
+                                 f"C oracle, OpenMP over pixels)",
+                       "single_thread_value": single, "cpu_model": cpu_model()}
+                parity = parity_spot_check(out, kept, r0, cut)
             except Exception as e:  # reported, not fatal
                 cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "oracle", "sample": f"failed: {e}"}
         line = {
@@ -360,8 +410,10 @@ def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_ma
                          "bytes_rule": "sum_p (S_c(p)+1)*b_in + rows*C*M*4 (SURVEY.md §8(d))"},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": K * world * (1 if st["general_tiles_u16" if cfg.dtype == "u16" else "general_tiles_f32"] == 0
-                                         else 2),
+            # per step: the separated-mode launch, the dual-walk launch if any tile overlaps,
+            # the general kernel if any tile needs it (launch_deposit)
+            "gpu_launches": K * world * (1 + (st["overlap_tiles"] > 0) +
+                                         (st["general_tiles_u16" if cfg.dtype == "u16" else "general_tiles_f32"] > 0)),
             "clocks": clocks.summary(),
             "prepass_ms": st["prepass_ms"],
             "plan": {"contrib_pairs": st["contrib_pairs"], "window_pairs": st["window_pairs"],
@@ -370,6 +422,10 @@ def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_ma
                      "staged_steps": st["staged_steps"], "fit_max_err_bins": st["fit_max_err_bins"],
                      "fit_model_err_bins": st["fit_model_err_bins"]},
         }
+        if parity is not None:
+            line["parity_sample"] = parity
+        if kern_median is not None:
+            line["roofline"]["kernel_ms_median"] = kern_median
         if cut[0] is not None:
             line["config"]["pixel_fraction"] = args.fraction
             line["config"]["cutoff_first_step_intensity"] = cut[0]

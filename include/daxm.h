@@ -44,8 +44,7 @@ typedef enum {
     DAXM_OK = 0,
     DAXM_ERR_INVALID_ARGUMENT = 1, /* bad sizes/enums/NaN/null pointers (see daxm_create)          */
     DAXM_ERR_NONMONOTONE_SCAN = 2, /* wire travel or a pixel's depth-vs-step not monotone           */
-    DAXM_ERR_GEOMETRY = 3,         /* non-collinear wire path, NaN depth inside a window, depth
-                                      model (cubic) error above tolerance, or no valid pixel          */
+    DAXM_ERR_GEOMETRY = 3,         /* NaN tangent depth inside a pixel's contributing window        */
     DAXM_ERR_OUT_OF_MEMORY = 4,
     DAXM_ERR_CUDA = 5              /* any CUDA runtime error; detail in daxm_last_error()            */
 } daxm_status;
@@ -70,8 +69,10 @@ typedef struct {
     double wire_axis[3];            /* wire axis a-hat (normalised by the library)                       */
     double wire_radius;             /* r > 0                                                             */
     int32_t n_steps;                /* S >= 2 wire steps                                                 */
-    const double *wire_xyz;         /* host pointer, S x 3 wire-centre positions (copied at create);    */
-                                    /* must be collinear (perpendicular to a-hat) and monotone           */
+    const double *wire_xyz;         /* host pointer, S x 3 wire-centre positions (copied at create).    */
+                                    /* Any path along which every pixel edge's depth is monotone; a     */
+                                    /* straight scan runs the fast kernels, any other path (jitter, a   */
+                                    /* curved stage) an exact per-step depth table          */
     double depth_start, depth_end;  /* centres of the first / last depth bin                             */
     double depth_res;               /* bin width dz > 0; M = round((end-start)/dz) + 1 bins,            */
                                     /* bin m covers [start + (m-1/2) dz, start + (m+1/2) dz)             */
@@ -99,6 +100,9 @@ typedef struct {
     double fit_model_err_bins; /* the same for the fp64 cubic: approximation error (<= 1e-6 enforced)     */
     double prepass_ms;         /* GPU time of the geometry pre-pass                                       */
     int64_t device_bytes;      /* device memory owned by the plan                                         */
+    int64_t depth_table_bytes; /* > 0: depths come from an exact per-step fp32 table (bins) over every    */
+                               /* tile's step range and all tiles run the general kernel: the wire path */
+                               /* is not straight, or the polynomial model missed its tolerance          */
 } daxm_plan_stats;
 
 /* daxm_create -- validate `g`, run the fp64 geometry pre-pass on `cuda_device`,
@@ -108,11 +112,15 @@ typedef struct {
  *     not an integer within 1e-6; zero-length or non-finite beam/axis vectors;
  *     any non-finite input; beam parallel to the axis; unknown enum value;
  *     wire_xyz NULL.
- *   NONMONOTONE_SCAN: projected wire travel decreases anywhere, all positions
- *     equal, or a pixel edge's depth is not monotone in the step index.
- *   GEOMETRY: wire centres off a straight line by > 1e-6 um (+1e-9 relative);
- *     NaN tangent depth inside a pixel's contributing window; cubic depth
- *     model error > 1e-6 bins (fp64) or > 1e-3 bins (as stored in fp32).
+ *   NONMONOTONE_SCAN: first and last positions coincide (perpendicular to a-hat),
+ *     the travel of a straight scan decreases, or a pixel edge's depth is not
+ *     monotone in the step index inside its window.
+ *   GEOMETRY: NaN tangent depth inside a pixel's contributing window.
+ * Depth source: for a straight scan (centres within 1e-6 um + 1e-9 relative of
+ * the line through the first and last) a quadratic per edge point in wire
+ * travel, kept if its fp64 error is <= 2e-5 bins and its fp32 error <= 1e-3 bins;
+ * otherwise (or with DAXM_FORCE_TABLE set in the environment) the exact per-step
+ * table, see daxm_plan_stats.depth_table_bytes.
  *   OUT_OF_MEMORY / CUDA: allocation or runtime failure.
  * The calling thread's current device is restored before returning. */
 daxm_status daxm_create(const daxm_geometry *g, int cuda_device, daxm_plan **out);

@@ -51,6 +51,7 @@ class PlanStats(C.Structure):
         ("nonseparated_tiles", C.c_int64), ("overlap_tiles", C.c_int64), ("ring_need_max", C.c_int64),
         ("tile_rows", C.c_int32), ("tile_cols", C.c_int32),
         ("fit_max_err_bins", C.c_double), ("fit_model_err_bins", C.c_double), ("prepass_ms", C.c_double), ("device_bytes", C.c_int64),
+        ("depth_table_bytes", C.c_int64),
     ]
 
 

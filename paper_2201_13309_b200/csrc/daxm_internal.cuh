@@ -120,6 +120,8 @@ struct DepositArgs {
     int n_states;             // (M + MC - 1) / MC + 1
     float sign;               // s: +1 leading, -1 trailing (reading R2)
     const void* stack;        // band stack [S][rows][C] (plane 0 read for the intensity cutoff)
+    const float* table;       // exact depth table (general kernel) or nullptr: per tile at toff[tile],
+    const long long* toff;    //   [k - k_lo][TILE_E][TILE_R] fp32 bins relative to m_ref
     int use_cutoff;           // 1: only pixels with I_0 >= cutoff are reconstructed (reading R14)
     float cutoff;
 };

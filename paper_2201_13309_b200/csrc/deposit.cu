@@ -766,8 +766,16 @@ __global__ void __launch_bounds__(256) deposit_general(DepositArgs a, const T* _
         const int kb = w.x, ke = act ? w.y : w.x, n = ke - kb, dir = ti.dir;
         auto step_of = [&](int q) { return dir > 0 ? kb + q : ke - q; };
         auto point = [&](int q, float& lo, float& hi) {
-            const float tau = (float)(a.t[step_of(q)] - ti.t_ref);
-            const float x0 = poly3(cb, tau), x1 = poly3(cf, tau);
+            float x0, x1;
+            if (a.table) {  // exact per-step depths (general wire paths)
+                const float* tb = a.table + a.toff[tile] + (size_t)(step_of(q) - ti.k_lo) * (TILE_E * TILE_R) + r;
+                x0 = tb[eb * TILE_R];
+                x1 = tb[ef * TILE_R];
+            } else {
+                const float tau = (float)(a.t[step_of(q)] - ti.t_ref);
+                x0 = poly3(cb, tau);
+                x1 = poly3(cf, tau);
+            }
             lo = fminf(x0, x1);
             hi = fmaxf(x0, x1);
         };

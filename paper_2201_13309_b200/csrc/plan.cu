@@ -50,6 +50,9 @@ struct daxm_plan {
     signed char* d_pdir = nullptr;
     signed char* d_psep = nullptr;
     int* d_vneed = nullptr;     // [n_tiles][n_states + 1] furthest visit index needed (fast kernel)
+    bool straight = true;       // wire centres on a line: travel-polynomial depth model possible
+    float* d_table = nullptr;   // exact per-step depth table (general wire paths / model miss)
+    long long* d_toff = nullptr;
     int n_states = 0;
     int* d_list_u16 = nullptr;  // general-kernel tile lists per dtype
     int* d_list_f32 = nullptr;
@@ -516,6 +519,8 @@ void free_plan_memory(daxm_plan* p) {
     cudaFree(p->d_stack_buf);
     cudaFree(p->d_out_buf);
     cudaFree(p->d_hist);
+    cudaFree(p->d_table);
+    cudaFree(p->d_toff);
     if (p->st_in) cudaStreamDestroy(p->st_in);
     if (p->st_out) cudaStreamDestroy(p->st_out);
     p->st_in = p->st_out = nullptr;
@@ -572,17 +577,16 @@ daxm_status host_prepare(daxm_plan* p) {
         return fail(nullptr, DAXM_ERR_NONMONOTONE_SCAN, "first and last wire positions coincide (perpendicular to the axis)");
     for (int c = 0; c < 3; ++c) gc.d[c] = v[3 * (S - 1) + c] / dl;
     p->t.assign(S, 0.0);
+    p->straight = true;
     for (int k = 0; k < S; ++k) {
         double tk = v[3 * k] * gc.d[0] + v[3 * k + 1] * gc.d[1] + v[3 * k + 2] * gc.d[2];
         double res[3] = {v[3 * k] - tk * gc.d[0], v[3 * k + 1] - tk * gc.d[1], v[3 * k + 2] - tk * gc.d[2]};
-        if (norm3(res) > 1e-6 + 1e-9 * fabs(tk))
-            return fail(nullptr, DAXM_ERR_GEOMETRY,
-                        "wire centre %d is %.3g um off the scan line (only straight scans are supported)", k,
-                        norm3(res));
+        if (norm3(res) > 1e-6 + 1e-9 * fabs(tk)) p->straight = false;  // general path: exact depth table
         p->t[k] = tk;
-        if (k > 0 && tk < p->t[k - 1])
-            return fail(nullptr, DAXM_ERR_NONMONOTONE_SCAN, "wire travel decreases between steps %d and %d", k - 1, k);
     }
+    for (int k = 1; k < S && p->straight; ++k)
+        if (p->t[k] < p->t[k - 1])
+            return fail(nullptr, DAXM_ERR_NONMONOTONE_SCAN, "wire travel decreases between steps %d and %d", k - 1, k);
     gc.r = g.wire_radius;
     gc.dz = g.depth_res;
     gc.lo0 = g.depth_start - 0.5 * g.depth_res;
@@ -594,6 +598,29 @@ daxm_status host_prepare(daxm_plan* p) {
     gc.point_mode = g.pixel_model == DAXM_PIXEL_POINT;
     gc.m_ref = p->M / 2;
     return DAXM_OK;
+}
+
+// Exact per-step depth table (general wire paths, or where the polynomial model
+// misses its tolerance): for every tile, edge point and step of the tile's step
+// range, u = (D - lo0)/dz - m_ref in fp32.  One CTA per tile, TILE_R x 8 threads.
+__global__ void __launch_bounds__(1024) table_kernel(GeomConst g, const double* __restrict__ wire, int tr0, int n_tc,
+                             const TileInfo* __restrict__ tiles, const long long* __restrict__ toff,
+                             float* __restrict__ table) {
+    const int tile = blockIdx.x;
+    const TileInfo ti = tiles[tile];
+    if (ti.k_hi < ti.k_lo) return;
+    const int tr = tile / n_tc, tc = tile % n_tc;
+    const int r = threadIdx.x;
+    const int j = (tr0 + tr) * TILE_R + r;
+    const int nv = ti.k_hi - ti.k_lo + 1;
+    float* tb = table + toff[tile];
+    for (int e = threadIdx.y; e < TILE_E; e += blockDim.y) {
+        double Q[3];
+        edge_point(g, j, tc * TILE_C + e, Q);
+        const double sg = edge_sigma(g, Q);
+        for (int v = 0; v < nv; ++v)
+            tb[((size_t)v * TILE_E + e) * TILE_R + r] = (float)tangent_u(g, Q, sg, wire + 3 * (ti.k_lo + v));
+    }
 }
 
 daxm_status device_prepass(daxm_plan* p) {
@@ -689,9 +716,34 @@ daxm_status device_prepass(daxm_plan* p) {
                                 (sizeof(int2) + 1) * (size_t)p->pre_rows * g.n_cols +
                                 sizeof(float) * n_tiles * NCOEF * TILE_E * TILE_R);
 
+    if (flags & (FLAG_NONMONOTONE | FLAG_MIXED_DIR))
+        return fail(nullptr, DAXM_ERR_NONMONOTONE_SCAN,
+                    "a pixel edge's tangent depth is not monotone in the wire step inside its window (flags 0x%x)", flags);
+    if (flags & FLAG_NAN_IN_WINDOW)
+        return fail(nullptr, DAXM_ERR_GEOMETRY, "NaN tangent depth inside a pixel's contributing window");
+    // depth source: the travel polynomial where it holds its tolerance, else the exact table
+    const bool use_table = !p->straight || (flags & FLAG_FIT_NAN) || !(model_err <= MODEL_ERR_MAX) ||
+                           !(max_err <= 1e-3) || getenv("DAXM_FORCE_TABLE") != nullptr;
     {
         std::vector<TileInfo> ht(n_tiles);
         CK(cudaMemcpy(ht.data(), p->d_tiles, sizeof(TileInfo) * n_tiles, cudaMemcpyDeviceToHost));
+        if (use_table) {
+            std::vector<long long> off(n_tiles);
+            long long tot = 0;
+            for (size_t q = 0; q < n_tiles; ++q) {
+                off[q] = tot;
+                if (ht[q].k_hi >= ht[q].k_lo) tot += (long long)(ht[q].k_hi - ht[q].k_lo + 1) * TILE_E * TILE_R;
+            }
+            CK(cudaMalloc(&p->d_toff, sizeof(long long) * n_tiles));
+            CK(cudaMemcpy(p->d_toff, off.data(), sizeof(long long) * n_tiles, cudaMemcpyHostToDevice));
+            CK(cudaMalloc(&p->d_table, sizeof(float) * (size_t)(tot > 0 ? tot : 1)));
+            table_kernel<<<(unsigned)n_tiles, dim3(TILE_R, 8)>>>(gc, p->d_wire, p->tr0, p->n_tc, p->d_tiles,
+                                                                p->d_toff, p->d_table);
+            CK(cudaGetLastError());
+            CK(cudaDeviceSynchronize());
+            st.depth_table_bytes = (int64_t)(sizeof(float) * (size_t)tot);
+            st.device_bytes += st.depth_table_bytes + (int64_t)(sizeof(long long) * n_tiles);
+        }
         std::vector<int> lu, lf;
         for (size_t q = 0; q < n_tiles; ++q) {
             const TileInfo& ti = ht[q];
@@ -702,7 +754,7 @@ daxm_status device_prepass(daxm_plan* p) {
             // TMA boxes start at the tile's first row; a tile that starts above the band
             // (band start not a multiple of TILE_R) would need a negative coordinate -> general kernel
             const int tile_row0 = (p->tr0 + (int)(q / p->n_tc)) * TILE_R;
-            const bool sep = ti.separated != MODE_GENERAL && tile_row0 >= g.row_begin;
+            const bool sep = ti.separated != MODE_GENERAL && tile_row0 >= g.row_begin && !use_table;
             if (!(sep && ti.ring_need <= NB_U16)) lu.push_back((int)q);
             if (!(sep && ti.ring_need <= NB_F32)) lf.push_back((int)q);
         }
@@ -719,17 +771,6 @@ daxm_status device_prepass(daxm_plan* p) {
         st.general_tiles_u16 = p->n_list_u16;
         st.general_tiles_f32 = p->n_list_f32;
     }
-    if (flags & (FLAG_NONMONOTONE | FLAG_MIXED_DIR))
-        return fail(nullptr, DAXM_ERR_NONMONOTONE_SCAN,
-                    "a pixel edge's tangent depth is not monotone in the wire step inside its window (flags 0x%x)", flags);
-    if (flags & FLAG_NAN_IN_WINDOW)
-        return fail(nullptr, DAXM_ERR_GEOMETRY, "NaN tangent depth inside a pixel's contributing window");
-    if (flags & FLAG_FIT_NAN) return fail(nullptr, DAXM_ERR_GEOMETRY, "NaN tangent depth at a depth-model node");
-    if (!(model_err <= MODEL_ERR_MAX))
-        return fail(nullptr, DAXM_ERR_GEOMETRY, "depth model (degree %d) error %.3g bins exceeds %.3g", NCOEF - 1,
-                    model_err, MODEL_ERR_MAX);
-    if (!(max_err <= 1e-3))
-        return fail(nullptr, DAXM_ERR_GEOMETRY, "fp32 depth model error %.3g bins exceeds 1e-3", max_err);
     return DAXM_OK;
 }
 
@@ -869,6 +910,8 @@ static DepositArgs make_args(const daxm_plan* p, int dtype) {
     a.point_mode = p->gc.point_mode;
     a.sign = p->g.edge == DAXM_EDGE_TRAILING ? -1.f : 1.f;
     a.stack = nullptr;
+    a.table = p->d_table;
+    a.toff = p->d_toff;
     a.use_cutoff = p->use_cutoff;
     a.cutoff = p->cutoff;
     return a;
@@ -892,7 +935,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // The fast kernel needs TMA-describable buffers: row pitch a multiple of 16 bytes.
 static bool fast_possible(const daxm_plan* p, int dt) {
     const int es = dt == DAXM_U16 ? 2 : 4;
-    return (p->C * es) % 16 == 0 && (p->C * 4) % 16 == 0 && p->max_nv <= MAX_FAST_NV && p->d_vneed != nullptr &&
+    return p->d_table == nullptr && (p->C * es) % 16 == 0 && (p->C * 4) % 16 == 0 && p->max_nv <= MAX_FAST_NV &&
+           p->d_vneed != nullptr &&
            getenv("DAXM_FORCE_GENERAL") == nullptr && tensor_map_encoder() != nullptr;
 }
 

@@ -122,6 +122,19 @@ def wire_positions(n_steps: int, t: np.ndarray | None = None, t_range: tuple = (
     return w0[None, :] + t[:, None] * d[None, :]
 
 
+def jittered_wire_positions(n_steps: int, t_range: tuple = (T_FIRST_UM, T_LAST_UM), amp_um: float = 0.3,
+                            seed: int = 2201) -> np.ndarray:
+    """A non-straight scan: the straight positions plus seeded jitter of up
+    to +-amp_um perpendicular to both the scan line and the wire axis, and along the axis."""
+    w = wire_positions(n_steps, t_range=t_range)
+    rng = np.random.default_rng(seed)
+    s2 = math.sqrt(2.0)
+    perp = np.array([0.0, 1.0 / s2, -1.0 / s2])
+    w = w + rng.uniform(-amp_um, amp_um, n_steps)[:, None] * perp[None, :]
+    w[:, 0] += rng.uniform(-amp_um, amp_um, n_steps)
+    return w
+
+
 def geometry(cfg: Config | str, edge: str = "leading", pixel_model: str = "finite",
              n_rows: int | None = None, n_cols: int | None = None) -> dict:
     """Plain-number geometry dict consumed by both sides (each fills its own struct)."""

@@ -89,7 +89,6 @@ def _create_status(daxm, g, rows=None, device=0):
     (lambda g: g.update(pixel_model=9), 1),
     (lambda g: g.update(wire_xyz=g["wire_xyz"][::-1][np.r_[0:5, 7, 6, 8:21]].copy()), 2),  # travel reverses
     (lambda g: g.update(wire_xyz=np.repeat(g["wire_xyz"][:1], 21, 0)), 2),  # no motion
-    (lambda g: g["wire_xyz"].__setitem__((10, 2), g["wire_xyz"][10, 2] + 5.0), 3),  # off the line
 ])
 def test_create_validation(daxm, mut, status):
     g = synth.geometry("C1")

@@ -381,3 +381,50 @@ def test_cutoff_skips_inactive_tiles(daxm):
     assert act.sum() == 6
     assert torch.equal(part[:, torch.from_numpy(act).cuda()], full[:, torch.from_numpy(act).cuda()])
     assert int(torch.count_nonzero(part[:, torch.from_numpy(~act).cuda()])) == 0
+
+
+@pytest.mark.parametrize("name,dtype,edge", [("C1", "f32", "leading"), ("C2", "u16", "leading"),
+                                             ("C2", "f32", "trailing")])
+def test_general_wire_path(daxm, name, dtype, edge):
+    """a jittered (non-straight) scan has no travel polynomial; the plan builds the
+    exact per-step depth table and the general kernel reproduces the oracle (which uses the
+    actual W_k)."""
+    cfg = synth.get_config(name)
+    g = synth.geometry(name, edge=edge)
+    g["wire_xyz"] = synth.jittered_wire_positions(cfg.n_steps, t_range=cfg.t_range, amp_um=0.3)
+    host = synth.stack_numpy(synth.make_maps(name), dtype, noise=True)
+    gpu, st = run_gpu(daxm, g, host)
+    assert st["depth_table_bytes"] > 0 and st[f"general_tiles_{dtype}"] == st["n_tiles"], st
+    parity.check(gpu, oracle.reconstruct(g, host), host, f"{name} jittered {edge}")
+
+
+def test_forced_table_equals_model_path(daxm, monkeypatch):
+    """The exact-table path on a straight scan (DAXM_FORCE_TABLE) against the oracle and against
+    the polynomial-model fast path."""
+    g = synth.geometry("C2")
+    host = synth.stack_numpy(synth.make_maps("C2"), "u16", noise=True)
+    fast, st0 = run_gpu(daxm, g, host)
+    monkeypatch.setenv("DAXM_FORCE_TABLE", "1")
+    tab, st1 = run_gpu(daxm, g, host)
+    assert st0["depth_table_bytes"] == 0 and st1["depth_table_bytes"] > 0
+    parity.check(tab, oracle.reconstruct(g, host), host, "C2 forced table")
+    d = parity.abs_dI(host)
+    assert (np.abs(tab - fast) <= 2e-4 * d[None]).all()
+
+
+def test_general_wire_path_full_size_sampled(daxm):
+    """C3-size jittered scan through the table path; sampled pixels against the oracle."""
+    import torch
+    cfg = synth.get_config("C3")
+    g = synth.geometry("C3")
+    g["wire_xyz"] = synth.jittered_wire_positions(cfg.n_steps, t_range=cfg.t_range, amp_um=0.2, seed=7)
+    maps = synth.make_maps("C3")
+    rng = np.random.default_rng(5)
+    js, is_ = _sample_pixels(cfg, maps, 300, rng)
+    with daxm.create(g, device=0) as plan:
+        assert plan.stats()["depth_table_bytes"] > 0
+        out = plan.reconstruct(synth.stack_torch(maps, "u16", "cuda:0", noise=True))
+        gpu = out[:, torch.from_numpy(js).cuda(), torch.from_numpy(is_).cuda()].cpu().numpy()  # [M, n]
+    ser = synth.pixel_series(maps, js, is_, "u16", noise=True)
+    ref = oracle.reconstruct_pixels(g, js, is_, ser).T
+    parity.check(gpu, ref, ser.T, "C3 jittered sampled")
