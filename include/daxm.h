@@ -103,6 +103,10 @@ typedef struct {
     int64_t depth_table_bytes; /* > 0: depths come from an exact per-step fp32 table (bins) over every    */
                                /* tile's step range and all tiles run the general kernel: the wire path */
                                /* is not straight, or the polynomial model missed its tolerance          */
+    int64_t lock_tiles_small;  /* tiles the step-locked kernel handles with a 16-plane output ring        */
+    int64_t lock_tiles_large;  /* ... with a 32-plane output ring                                         */
+    int64_t lock_ring_violations; /* step-locked ring-capacity violations so far (read synchronously;    */
+                               /* always 0: the pre-pass admits only tiles whose ring provably suffices) */
 } daxm_plan_stats;
 
 /* daxm_create -- validate `g`, run the fp64 geometry pre-pass on `cuda_device`,

@@ -83,7 +83,7 @@ struct TileInfo {
     int dir;        // +1: depth increases with the step index, -1: decreases
     int separated;  // deposit mode: MODE_SEPARATED / MODE_OVERLAP (fast kernel) or MODE_GENERAL
     int ring_need;  // input ring slots the fast kernel needs for this tile (deadlock-free bound)
-    int pad;
+    int lock;       // step-locked kernel: output ring class (LOCK_RB_SMALL / LOCK_RB_LARGE) or 0 (not eligible)
 };
 
 // Per-tile deposit mode (pre-pass, fp64): every pixel's consecutive edge spans are
@@ -124,7 +124,37 @@ struct DepositArgs {
     const long long* toff;    //   [k - k_lo][TILE_E][TILE_R] fp32 bins relative to m_ref
     int use_cutoff;           // 1: only pixels with I_0 >= cutoff are reconstructed (reading R14)
     float cutoff;
+    int lock_enabled;         // step-locked kernel handles tiles with tiles[].lock != 0
+    int lock_small, lock_large, lock_rest;  // tile counts: lock classes, fast tiles left to deposit_fast
+    unsigned* lock_err;       // device word: ring-capacity violations (must stay 0)
 };
+
+// Step-locked deposit kernel (deposit_lock.cu): one warp = 16 detector rows x 8 columns,
+// lanes = 8 columns x 4 row groups, 4 pixel walks (rows) per thread.  Every walk advances
+// one wire step per iteration (aligned at its own window start); the edges of the zone the
+// step closes are evaluated in a warp-uniform loop.  Output planes go through a per-warp
+// ring of LOCK_RB planes indexed by bin edge.
+constexpr int LOCK_ROWS = 16;       // detector rows per warp
+constexpr int LOCK_WARPS = 4;       // warps per CTA (independent pipelines)
+constexpr int LOCK_SUBS = TILE_R / (LOCK_ROWS * LOCK_WARPS);  // CTAs per deposit tile
+constexpr int LOCK_NB = 16;         // input ring slots (wire steps) per warp
+constexpr int LOCK_CLASS_MASK = 0xff;  // TileInfo.lock: ring class in the low byte
+constexpr int LOCK_FRONT_LO = 0x100;   //   flag: the front pixel edge is the shallower over the whole tile
+constexpr int LOCK_RB_SMALL = 16;   // output ring planes per warp
+constexpr int LOCK_RB_LARGE = 32;
+// largest "need" (edges from the slowest walk's frontier to the furthest edge written in one
+// iteration, inclusive) a ring of rb planes holds: planes below the frontier are copied out
+// before the next iteration, so writes stay below frontier - 1 + rb
+constexpr int lock_need_max(int rb) { return rb; }
+// window-start spread (steps) a warp's input ring holds: loads are issued in groups of 4, so
+// up to 3 slots may be pending besides the spread, the prefetched step and one spare
+constexpr int LOCK_SPREAD_MAX = LOCK_NB - 6;
+
+// Corner depth of one pixel edge at fp32 wire travel tau (bins relative to m_ref): the
+// pre-pass ring check and the step-locked kernel evaluate exactly this expression.
+__device__ __forceinline__ float lock_poly(float c0, float c1, float c2, float t) {
+    return fmaf(fmaf(c2, t, c1), t, c0);
+}
 
 // Launchers (deposit.cu, profile.cu, select.cu).
 cudaError_t select_cutoff(const void* plane0, int dtype, size_t n, unsigned long long k,
@@ -132,6 +162,11 @@ cudaError_t select_cutoff(const void* plane0, int dtype, size_t n, unsigned long
 cudaError_t launch_depth_profile(const float* out, int M, size_t plane, double* profile, cudaStream_t st);
 size_t fast_smem_bytes(int dtype, int max_nv);
 cudaError_t launch_deposit(const DepositArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
-                           const void* stack, int dtype, float* out, bool fast_enabled, cudaStream_t st);
+                           const void* stack, int dtype, float* out, bool fast_enabled, cudaStream_t st,
+                           const CUtensorMap* lock_in_map);
+size_t lock_smem_bytes(int dtype, int rb, int max_nv);
+cudaError_t launch_lock(const DepositArgs& a, const CUtensorMap* in_map, float* out, int dtype, int n_tiles,
+                        cudaStream_t st);
+cudaError_t launch_lock_prepass(const DepositArgs& a, int n_tiles, int* d_stats, cudaStream_t st);
 
 }  // namespace daxm

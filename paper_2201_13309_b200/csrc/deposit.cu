@@ -35,66 +35,11 @@
 #include <stdint.h>
 
 #include "daxm_internal.cuh"
+#include "ptx.cuh"
 
 namespace daxm {
 namespace {
-
-// ------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        " .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-        "[%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, int c0, int c1, int c2, const void* src) {
-    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                     reinterpret_cast<uint64_t>(map)),
-                 "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void bulk_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-template <int N>
-__device__ __forceinline__ void bulk_wait() {
-    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-[[maybe_unused]] __device__ __forceinline__ void st_shared_v4(uint32_t addr, float a, float b, float c, float d) {
-    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d) : "memory");
-}
+using namespace ptx;
 
 __device__ __forceinline__ float poly3(const float c[NCOEF], float tau) {
     float p = c[NCOEF - 1];
@@ -120,63 +65,6 @@ struct FastSmem {
     static constexpr int OFF_TAU = OFF_SYNC + 64;
     static size_t bytes(int max_nv) { return (size_t)OFF_TAU + sizeof(float) * (size_t)(max_nv + 4) + 1024; }
 };
-
-__device__ __forceinline__ float lds_f32(uint32_t addr) {
-    float v;
-    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-    return v;
-}
-template <typename T>
-__device__ __forceinline__ float lds_px(uint32_t addr);
-template <>
-__device__ __forceinline__ float lds_px<uint16_t>(uint32_t addr) {
-    unsigned short v;
-    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
-    return (float)v;
-}
-template <>
-__device__ __forceinline__ float lds_px<float>(uint32_t addr) {
-    return lds_f32(addr);
-}
-__device__ __forceinline__ float rcp_approx(float x) {
-    float y;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-#ifndef DAXM_HINT
-#define DAXM_HINT 2000
-#endif
-#define DAXM_STR2(x) #x
-#define DAXM_STR(x) DAXM_STR2(x)
-__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-[[maybe_unused]] __device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        " .reg .pred p;\n"
-        "WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, " DAXM_STR(DAXM_HINT) ";\n"
-        " @!p bra WAIT_%=;\n"
-        "}\n" ::"r"(bar),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint32_t bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, " DAXM_STR(DAXM_HINT) ";\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
 
 // ------------------------------------------------------------------ fast kernel
 // Eight warps: warp w covers tile rows 32*(w/2) .. +31 (lanes) and columns
@@ -223,6 +111,7 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
     const int row0 = (a.tr0 + tr) * TILE_R;  // global row of tile row 0
     // the general kernel owns this tile (same predicate as the plan's tile lists)
     if (!(ti.separated == MODE && row0 >= a.row_begin && ti.ring_need <= NB)) return;
+    if (a.lock_enabled && ti.lock) return;  // the step-locked kernel owns this tile
     const int col0 = tc * TILE_C;
     const int row0_local = row0 - a.row_begin;
     const int nv_all = ti.k_hi >= ti.k_lo ? ti.k_hi - ti.k_lo + 1 : 0;
@@ -861,13 +750,19 @@ size_t fast_smem_bytes(int dtype, int max_nv) {
 }
 
 cudaError_t launch_deposit(const DepositArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
-                           const void* stack, int dtype, float* out, bool fast_enabled, cudaStream_t st) {
+                           const void* stack, int dtype, float* out, bool fast_enabled, cudaStream_t st,
+                           const CUtensorMap* lock_in_map) {
     const int n_tiles = (a.tr_end - a.tr_begin) * a.n_tc;
     if (n_tiles <= 0) return cudaSuccess;
     cudaError_t e = cudaSuccess;
     if (fast_enabled) {
-        e = dtype == DAXM_U16 ? launch_fast_modes<uint16_t, NB_U16>(in_map, out_map, a, n_tiles, st)
-                              : launch_fast_modes<float, NB_F32>(in_map, out_map, a, n_tiles, st);
+        if (a.lock_enabled) {
+            e = launch_lock(a, lock_in_map, out, dtype, n_tiles, st);
+            if (e != cudaSuccess) return e;
+        }
+        if (a.lock_rest > 0)
+            e = dtype == DAXM_U16 ? launch_fast_modes<uint16_t, NB_U16>(in_map, out_map, a, n_tiles, st)
+                                  : launch_fast_modes<float, NB_F32>(in_map, out_map, a, n_tiles, st);
         if (e != cudaSuccess) return e;
         if (a.n_list == 0) return cudaSuccess;
     }

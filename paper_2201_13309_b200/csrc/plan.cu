@@ -60,6 +60,9 @@ struct daxm_plan {
     int max_nv = 0;
     // TMA descriptors, re-encoded when the caller's buffers change
     CUtensorMap in_map{}, out_map{};
+    CUtensorMap lock_in_map{};  // step-locked kernel: one warp's [16 rows][8 cols] block per wire step
+    int lock_small = 0, lock_large = 0, lock_rest = 0;                // tile counts (lock pre-pass)
+    unsigned* d_lock_err = nullptr;                                   // ring-capacity violations
     const void* map_stack = nullptr;
     const float* map_out = nullptr;
     int map_dtype = -1;
@@ -78,6 +81,7 @@ struct daxm_plan {
 };
 
 static thread_local std::string g_create_err;
+static DepositArgs make_args(const daxm_plan* p, int dtype);
 
 namespace {
 
@@ -361,7 +365,7 @@ __global__ void __launch_bounds__(1024) tile_kernel(GeomConst g, const double* _
     __syncthreads();
     if (tid == 0) {
         TileInfo ti;
-        ti.pad = 0;
+        ti.lock = 0;
         if (s_kb == INT_MAX) {
             ti.t_ref = 0.0;
             ti.k_lo = 0;
@@ -521,6 +525,8 @@ void free_plan_memory(daxm_plan* p) {
     cudaFree(p->d_hist);
     cudaFree(p->d_table);
     cudaFree(p->d_toff);
+    cudaFree(p->d_lock_err);
+    p->d_lock_err = nullptr;
     if (p->st_in) cudaStreamDestroy(p->st_in);
     if (p->st_out) cudaStreamDestroy(p->st_out);
     p->st_in = p->st_out = nullptr;
@@ -771,6 +777,22 @@ daxm_status device_prepass(daxm_plan* p) {
         st.general_tiles_u16 = p->n_list_u16;
         st.general_tiles_f32 = p->n_list_f32;
     }
+    // ---- step-locked kernel: per tile, replay the walks' edge frontiers in fp32 and admit the
+    // tile if its per-warp output ring provably holds them (deposit_lock.cu)
+    CK(cudaMalloc(&p->d_lock_err, 16));
+    CK(cudaMemset(p->d_lock_err, 0, 16));
+    if (!use_table) {
+        int* d_ls = reinterpret_cast<int*>(p->d_lock_err) + 1;
+        DepositArgs a = make_args(p, DAXM_U16);
+        CK(launch_lock_prepass(a, (int)n_tiles, d_ls, 0));
+        int hs[3];
+        CK(cudaMemcpy(hs, d_ls, sizeof hs, cudaMemcpyDeviceToHost));
+        p->lock_small = hs[0];
+        p->lock_large = hs[1];
+        p->lock_rest = hs[2];
+        st.lock_tiles_small = hs[0];
+        st.lock_tiles_large = hs[1];
+    }
     return DAXM_OK;
 }
 
@@ -878,8 +900,19 @@ daxm_status daxm_plan_info(const daxm_plan* p, int64_t* n_bins, int64_t* rows, i
 daxm_status daxm_plan_stats_get(const daxm_plan* p, daxm_plan_stats* st) {
     if (!p || !st) return DAXM_ERR_INVALID_ARGUMENT;
     *st = p->stats;
+    if (p->d_lock_err) {  // synchronous read of the step-locked kernel's violation counter
+        DeviceGuard guard(p->device);
+        unsigned v = 0;
+        if (cudaMemcpy(&v, p->d_lock_err, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cudaGetLastError();
+            return DAXM_ERR_CUDA;
+        }
+        st->lock_ring_violations = v;
+    }
     return DAXM_OK;
 }
+
+}  // extern "C"
 
 static DepositArgs make_args(const daxm_plan* p, int dtype) {
     DepositArgs a;
@@ -914,8 +947,15 @@ static DepositArgs make_args(const daxm_plan* p, int dtype) {
     a.toff = p->d_toff;
     a.use_cutoff = p->use_cutoff;
     a.cutoff = p->cutoff;
+    a.lock_enabled = (p->lock_small + p->lock_large) > 0 && getenv("DAXM_NO_LOCK") == nullptr;
+    a.lock_small = p->lock_small;
+    a.lock_large = p->lock_large;
+    a.lock_rest = a.lock_enabled ? p->lock_rest : 1;
+    a.lock_err = p->d_lock_err;
     return a;
 }
+
+extern "C" {
 
 static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -967,6 +1007,17 @@ static daxm_status encode_maps(daxm_plan* p, const void* d_stack, int dt, float*
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(p, DAXM_ERR_CUDA, "cuTensorMapEncodeTiled(out) failed: %d", (int)r);
     }
+    {   // step-locked kernel: one warp's [16 rows][8 cols] block per wire step
+        cuuint64_t dims[3] = {C, R, (cuuint64_t)p->S};
+        cuuint64_t strides[2] = {C * es, C * R * es};
+        cuuint32_t box[3] = {(cuuint32_t)TILE_C, (cuuint32_t)LOCK_ROWS, 1};
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = enc(&p->lock_in_map, dt == DAXM_U16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                         3, const_cast<void*>(d_stack), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(p, DAXM_ERR_CUDA, "cuTensorMapEncodeTiled(lock stack) failed: %d", (int)r);
+    }
     p->map_stack = d_stack;
     p->map_out = d_out;
     p->map_dtype = dt;
@@ -984,7 +1035,7 @@ static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float*
     a.tr_begin = tr_begin;
     a.tr_end = tr_end < 0 ? p->n_tr : tr_end;
     a.stack = d_stack;
-    cudaError_t e = launch_deposit(a, &p->in_map, &p->out_map, d_stack, dt, d_out, fast, st);
+    cudaError_t e = launch_deposit(a, &p->in_map, &p->out_map, d_stack, dt, d_out, fast, st, &p->lock_in_map);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(p, DAXM_ERR_CUDA, "deposit launch: %s", cudaGetErrorString(e));

@@ -23,7 +23,7 @@ def check(gpu, ref, series, what=""):
     assert np.isfinite(gpu).all(), f"{what}: non-finite GPU output"
     d = abs_dI(series)
     err = np.abs(gpu - ref)
-    lim = BIN_TOL * d[None]
+    lim = np.broadcast_to(BIN_TOL * d[None], err.shape)
     bad = err > lim
     if bad.any():
         idx = np.argwhere(bad)[0]

@@ -428,3 +428,79 @@ def test_general_wire_path_full_size_sampled(daxm):
     ser = synth.pixel_series(maps, js, is_, "u16", noise=True)
     ref = oracle.reconstruct_pixels(g, js, is_, ser).T
     parity.check(gpu, ref, ser.T, "C3 jittered sampled")
+
+
+# ------------------------------------------------------------------ step-locked kernel
+
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
+def test_lock_kernel_owns_separated_tiles(daxm, name):
+    """The pre-pass admits (nearly) every separated tile of the benchmark configs to the
+    step-locked kernel, and its ring-capacity counter stays 0 after a reconstruction."""
+    import torch
+    cfg = synth.get_config(name)
+    g = synth.geometry(cfg)
+    with daxm.create(g, device=0) as plan:
+        st = plan.stats()
+        n_lock = st["lock_tiles_small"] + st["lock_tiles_large"]
+        n_sep = st["n_tiles"] - st["nonseparated_tiles"]
+        assert n_lock >= 0.9 * n_sep, st
+        if name in ("C2", "C3"):
+            stack = torch.from_numpy(synth.stack_numpy(synth.make_maps(cfg), cfg.dtype, noise=True)).cuda()
+        else:
+            stack = synth.stack_torch(synth.make_maps(cfg), cfg.dtype, "cuda:0", noise=True)
+        plan.reconstruct(stack)
+        torch.cuda.synchronize()
+        assert plan.stats()["lock_ring_violations"] == 0
+
+
+@pytest.mark.parametrize("case", ["C1-f32", "C1-u16-point", "C2-f32-trailing", "C3-u16"])
+def test_fast_kernel_without_lock(daxm, case, monkeypatch):
+    """DAXM_NO_LOCK routes the separated tiles back to the bin-major fast kernel: both
+    schedules of the same deposit algebra match the oracle."""
+    monkeypatch.setenv("DAXM_NO_LOCK", "1")
+    parts = case.split("-")
+    name, dtype = parts[0], parts[1]
+    edge = "trailing" if "trailing" in parts else "leading"
+    pm = "point" if "point" in parts else "finite"
+    g = synth.geometry(name, edge=edge, pixel_model=pm)
+    host = synth.stack_numpy(synth.make_maps(name), dtype, noise=True)
+    gpu, _ = run_gpu(daxm, g, host)
+    parity.check(gpu, oracle.reconstruct(g, host), host, f"{case} fast (no lock)")
+
+
+def test_lock_kernel_sparse_and_cutoff(daxm):
+    """Sparse stack (most pixels have dI = 0 everywhere) with an intensity cutoff: inactive
+    walks and zero planes through the step-locked kernel."""
+    import torch
+    g = synth.geometry("C3")
+    maps = synth.make_maps("C3")
+    host = synth.stack_numpy(maps, "u16", noise=False)
+    with daxm.create(g, device=0) as plan:
+        st = torch.from_numpy(host).cuda()
+        cut = plan.select_cutoff(st, 0.05)
+        plan.set_cutoff(cut)
+        out = plan.reconstruct(st)
+        torch.cuda.synchronize()
+        gpu = out.cpu().numpy()
+        assert plan.stats()["lock_ring_violations"] == 0
+    ref = oracle.reconstruct_cutoff(g, host, cut)
+    parity.check(gpu, ref, host, "C3 sparse cutoff (lock)")
+
+
+def test_lock_ring_check_build(tmp_path):
+    """A DAXM_LOCK_CHECK=1 build of the library counts every write past the recycled part of
+    a warp's output ring; the pre-pass admission must make that count 0 on every config."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from paper_2201_13309_b200 import _build
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = _build.build_library(out=str(tmp_path / "libdaxm_lockcheck.so"), defines=["DAXM_LOCK_CHECK=1"])
+    env = dict(os.environ, DAXM_LIBRARY=lib)
+    out = subprocess.run([sys.executable, os.path.join(root, "scripts", "lock_check.py")], env=env,
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res and all(v["lock_ring_violations"] == 0 for v in res.values()), res
+    assert all(v["lock_tiles_small"] + v["lock_tiles_large"] > 0 for v in res.values()), res
