@@ -351,6 +351,19 @@ def main():
                   kern_median)
 
 
+def launches_per_step(st, dtype):
+    """Kernels one daxm_reconstruct launches (csrc/deposit.cu launch_deposit): the step-locked
+    kernel once per output-ring class in use, deposit_fast (separated + dual-walk launches) if
+    any non-general tile is left to it, the general kernel if any tile needs it."""
+    general = st["general_tiles_u16" if dtype == "u16" else "general_tiles_f32"]
+    small, large = st.get("lock_tiles_small", 0), st.get("lock_tiles_large", 0)
+    rest = st["n_tiles"] - general - small - large
+    n = (small > 0) + (large > 0) + (general > 0)
+    if rest > 0:
+        n += 1 + (st["overlap_tiles"] > 0)
+    return int(n)
+
+
 def parity_spot_check(out, kept, r0, cut):
     """After timing, compare the timed output buffer with the oracle outputs the CPU-baseline
     leg computed for its pixel sample (north_star tolerance: per bin 1e-4 * sum|dI|)."""
@@ -410,15 +423,13 @@ def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_ma
                          "bytes_rule": "sum_p (S_c(p)+1)*b_in + rows*C*M*4 (SURVEY.md §8(d))"},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            # per step: the separated-mode launch, the dual-walk launch if any tile overlaps,
-            # the general kernel if any tile needs it (launch_deposit)
-            "gpu_launches": K * world * (1 + (st["overlap_tiles"] > 0) +
-                                         (st["general_tiles_u16" if cfg.dtype == "u16" else "general_tiles_f32"] > 0)),
+            "gpu_launches": K * world * launches_per_step(st, cfg.dtype),
             "clocks": clocks.summary(),
             "prepass_ms": st["prepass_ms"],
             "plan": {"contrib_pairs": st["contrib_pairs"], "window_pairs": st["window_pairs"],
                      "general_tiles": st["general_tiles_u16" if cfg.dtype == "u16" else "general_tiles_f32"],
-                     "n_tiles": st["n_tiles"],
+                     "n_tiles": st["n_tiles"], "lock_tiles_small": st.get("lock_tiles_small"),
+                     "lock_tiles_large": st.get("lock_tiles_large"), "overlap_tiles": st["overlap_tiles"],
                      "staged_steps": st["staged_steps"], "fit_max_err_bins": st["fit_max_err_bins"],
                      "fit_model_err_bins": st["fit_model_err_bins"]},
         }
