@@ -138,6 +138,8 @@ constexpr int LOCK_ROWS = 16;       // detector rows per warp
 constexpr int LOCK_WARPS = 4;       // warps per CTA (independent pipelines)
 constexpr int LOCK_SUBS = TILE_R / (LOCK_ROWS * LOCK_WARPS);  // CTAs per deposit tile
 constexpr int LOCK_NB = 16;         // input ring slots (wire steps) per warp
+constexpr int LOCK_G = 4;           // wire steps per TMA box and mbarrier (one group)
+constexpr int LOCK_NG = LOCK_NB / LOCK_G;  // groups in the input ring
 constexpr int LOCK_CLASS_MASK = 0xff;  // TileInfo.lock: ring class in the low byte
 constexpr int LOCK_FRONT_LO = 0x100;   //   flag: the front pixel edge is the shallower over the whole tile
 constexpr int LOCK_RB_SMALL = 16;   // output ring planes per warp
@@ -146,9 +148,10 @@ constexpr int LOCK_RB_LARGE = 32;
 // iteration, inclusive) a ring of rb planes holds: planes below the frontier are copied out
 // before the next iteration, so writes stay below frontier - 1 + rb
 constexpr int lock_need_max(int rb) { return rb; }
-// window-start spread (steps) a warp's input ring holds: loads are issued in groups of 4, so
-// up to 3 slots may be pending besides the spread, the prefetched step and one spare
-constexpr int LOCK_SPREAD_MAX = LOCK_NB - 6;
+// window-start spread (steps) a warp's input ring holds: at iteration jj the groups up to
+// (jj + NB - G) / G are issued, and the fastest walk needs visit vmin0 + spread + jj + 1
+constexpr int LOCK_SPREAD_MAX = LOCK_NB - LOCK_G - 1;
+static_assert(LOCK_NB % LOCK_G == 0 && (LOCK_NB / LOCK_G & (LOCK_NB / LOCK_G - 1)) == 0, "lock input ring shape");
 
 // Corner depth of one pixel edge at fp32 wire travel tau (bins relative to m_ref): the
 // pre-pass ring check and the step-locked kernel evaluate exactly this expression.

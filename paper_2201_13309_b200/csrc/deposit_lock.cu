@@ -22,8 +22,8 @@
 // setup): lane = (row group rg = lane / 8, column = lane % 8), walk w (0..3) = row
 // 4 w + rg, so one walk's 32 lanes cover 4 consecutive rows x 8 columns = 128
 // contiguous bytes of a staged plane (conflict-free scalar stores).
-//   input : TMA loads of the warp's [16 rows][8 cols] block of each wire step into a
-//           16-slot mbarrier ring (lane 0 produces, one step per iteration);
+//   input : TMA loads of the warp's [LOCK_G steps][16 rows][8 cols] block into a 16-slot
+//           ring, one mbarrier per group of LOCK_G steps (lane 0 produces);
 //   output: a ring of RB staged planes indexed by bin edge e (plane e - 1); planes below
 //           the slowest walk's frontier are TMA-stored in batches of SB, their slots
 //           zeroed once the store has read them.  The pre-pass (lock_prepass_kernel)
@@ -48,10 +48,16 @@ static_assert(TILE_C == 8 && TILE_R % (LOCK_ROWS * LOCK_WARPS) == 0, "lock kerne
 #define DAXM_LOCK_MINB 4  // CTAs per SM the register allocation targets (128 regs at 4)
 #endif
 #ifndef DAXM_LOCK_UNROLL
-#define DAXM_LOCK_UNROLL 1
+#define DAXM_LOCK_UNROLL 2  // iterations per loop body (2: no loop-carried register rotation)
 #endif
 #define DAXM_PRAGMA(x) _Pragma(#x)
 #define DAXM_UNROLL(n) DAXM_PRAGMA(unroll n)
+#ifndef DAXM_LOCK_KUNROLL
+#define DAXM_LOCK_KUNROLL 1  // edge-loop trips per loop body
+#endif
+#ifndef DAXM_LOCK_DRAIN2
+#define DAXM_LOCK_DRAIN2 1  // 1: copy-out loads two planes before storing either
+#endif
 #ifndef DAXM_LOCK_CHECK
 #define DAXM_LOCK_CHECK 0  // 1: count ring-capacity violations (the pre-pass makes them impossible)
 #endif
@@ -63,6 +69,7 @@ template <typename T, int RB>
 struct LockSmem {
     static constexpr int OUT_BYTES = RB * LK_PLANE;                       // per warp
     static constexpr int IN_SLOT = LOCK_ROWS * TILE_C * (int)sizeof(T);    // per warp and step
+    static constexpr int IN_GROUP = LOCK_G * IN_SLOT;                     // one TMA box
     static constexpr int IN_BYTES = LOCK_NB * IN_SLOT;                    // per warp
     static constexpr int OFF_OUT = 0;
     static constexpr int OFF_IN = OFF_OUT + LOCK_WARPS * OUT_BYTES;
@@ -135,8 +142,9 @@ __device__ __forceinline__ float4 lds128(uint32_t addr) {
                  : "memory");
     return v;
 }
-__device__ __forceinline__ void stg128_cs(float* p, float4 v) {  // streaming store: the output is written once
-    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+__device__ __forceinline__ void stg128_cs_if(bool ok, float* p, float4 v) {  // streaming (written once), predicated
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n @q st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};\n}\n" ::"l"(p),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"((unsigned)ok)
                  : "memory");
 }
 
@@ -173,7 +181,7 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
         tau[v] = (float)(a.t[k] - ti.t_ref);
     }
     if (lane == 0) {
-        for (int s = 0; s < LOCK_NB; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < LOCK_NG; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
     // zero the output ring: RB planes x 512 B, 16 B per lane per plane
@@ -241,12 +249,21 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
             sts_zero4(s_copy + (uint32_t)(RB - 1) * LK_PLANE);
             done_p = 0;
         }
+        auto slot = [&](int p) { return s_copy + (uint32_t)(p & (RB - 1)) * LK_PLANE; };
+#pragma unroll 1
+        for (; DAXM_LOCK_DRAIN2 && done_p + 1 < upto; done_p += 2) {  // two planes per trip: both loads in flight
+            const float4 va = lds128(slot(done_p)), vb = lds128(slot(done_p + 1));
+            sts_zero4(slot(done_p));
+            sts_zero4(slot(done_p + 1));
+            stg128_cs_if(c_ok, gp, va);
+            stg128_cs_if(c_ok, gp + plane_stride, vb);
+            gp += 2 * plane_stride;
+        }
 #pragma unroll 1
         for (; done_p < upto; ++done_p) {
-            const uint32_t sa = s_copy + (uint32_t)(done_p & (RB - 1)) * LK_PLANE;
-            const float4 v = lds128(sa);
-            if (c_ok) stg128_cs(gp, v);
-            sts_zero4(sa);
+            const float4 v = lds128(slot(done_p));
+            sts_zero4(slot(done_p));
+            stg128_cs_if(c_ok, gp, v);
             gp += plane_stride;
         }
         __syncwarp();
@@ -255,38 +272,45 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
     if (niter > 0) {
         // ---- input ring: visit v (relative r = v - vmin0) in slot r % NB, parity (r / NB) & 1.
         // Loads are issued in groups of >= 4 and waited for in groups (warp-uniform bookkeeping).
-        int v_issue = vmin0, waited = vmin0;  // next visit to load / to wait for
-        auto issue = [&](int limit) {
-            const int lim = min(limit, vend + 1);
-            if (!(lim - v_issue >= 4 || (lim == vend + 1 && lim > v_issue))) return;
+        // Visits vmin0 + 4g .. + 3 form group g: one TMA box of LOCK_G consecutive wire steps
+        // (ascending k, so for dir < 0 a group's visits land in reverse slot order: slot =
+        // ((v - vmin0) ^ xr) mod NB) completing mbarrier g mod NG.  Group g reuses the slots of
+        // group g - NG, free once every walk has read past it: at iteration jj the slowest walk
+        // has consumed the visits below vmin0 + jj, so groups up to (jj + NB - G) / G may be in
+        // flight; the fastest walk needs visit vmax0 + jj + 1, at most LOCK_SPREAD_MAX + jj + 1.
+        const int xr = dir > 0 ? 0 : LOCK_G - 1;
+        const int ngroups = (vend - vmin0) / LOCK_G + 1;
+        const int kbase = dir > 0 ? ti.k_lo + vmin0 : ti.k_hi - vmin0 - (LOCK_G - 1);
+        int g_issue = 0, g_wait = 0;  // next group to load / to wait for
+        auto issue = [&](int jj) {    // groups the ring can hold at iteration jj
+            const int lim = min((jj + LOCK_NB - LOCK_G) / LOCK_G, ngroups - 1);
+            if (g_issue > lim) return;
             if (lane == 0) {
-                for (int v = v_issue; v < lim; ++v) {
-                    const int s = (v - vmin0) & (LOCK_NB - 1);
-                    mbar_arrive_expect_tx(&bars[s], L::IN_SLOT);
-                    const int k = dir > 0 ? ti.k_lo + v : ti.k_hi - v;
-                    tma_load_3d(smem + (s_in - sbase) + s * L::IN_SLOT, &in_map, col0, row_local, k, &bars[s]);
+                for (int g = g_issue; g <= lim; ++g) {
+                    const int b = g & (LOCK_NG - 1);
+                    mbar_arrive_expect_tx(&bars[b], L::IN_GROUP);
+                    tma_load_3d(smem + (s_in - sbase) + b * L::IN_GROUP, &in_map, col0, row_local,
+                                dir > 0 ? kbase + g * LOCK_G : kbase - g * LOCK_G, &bars[b]);
                 }
             }
-            v_issue = lim;
+            g_issue = lim + 1;
         };
-        auto wait_upto = [&](int v) {
-            v = min(v, vend);
-            if (waited > v) return;
-            const int tgt = min(v + 3, v_issue - 1);
-            for (; waited <= tgt; ++waited) {  // compiler-visible retry loop: the warp reconverges after it
-                const int rr = waited - vmin0;
-                while (!mbar_try(s_bar + (uint32_t)(rr & (LOCK_NB - 1)) * 8u, (uint32_t)(rr / LOCK_NB) & 1u)) {
+        auto wait_upto = [&](int v) {  // every group up to visit v's (clamped to the last) has landed
+            const int g_need = (min(v, vend) - vmin0) / LOCK_G;
+            if (g_wait > g_need) return;
+            for (; g_wait <= g_need; ++g_wait) {  // compiler-visible retry loop: the warp reconverges after it
+                while (!mbar_try(s_bar + (uint32_t)(g_wait & (LOCK_NG - 1)) * 8u, (uint32_t)(g_wait / LOCK_NG) & 1u)) {
                 }
             }
             __syncwarp();
         };
-        issue(vmin0 + LOCK_NB);
+        issue(0);
 
         // per-lane addresses
         const uint32_t in_lane = s_in + (uint32_t)(rg * TILE_C + col) * (uint32_t)sizeof(T);  // + w * 4 rows
         const uint32_t out_lane = s_out + (uint32_t)(rg * TILE_C + col) * 4u;                 // + w * 128
         auto in_addr = [&](int w, int v) -> uint32_t {
-            return in_lane + (uint32_t)((v - vmin0) & (LOCK_NB - 1)) * (uint32_t)L::IN_SLOT +
+            return in_lane + (uint32_t)(((v - vmin0) ^ xr) & (LOCK_NB - 1)) * (uint32_t)L::IN_SLOT +
                    (uint32_t)(w * 4 * TILE_C * (int)sizeof(T));
         };
 
@@ -349,7 +373,7 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
         DAXM_UNROLL(DAXM_LOCK_UNROLL)
         for (int jj = 1; jj < niter; ++jj) {
             // point jj (prefetched); refill the ring below the slowest walk; prefetch point jj + 1
-            issue(vmin0 + jj + LOCK_NB - 1);
+            issue(jj);
             wait_upto(vmax0 + jj + 1);
             float2 zlo[2], zw[2], zc[2], zd[2], zg[2], zF0[2], Eb[2];
             float2 tn[2], In[2];
@@ -404,7 +428,7 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
             }
             const int K = __reduce_max_sync(0xffffffffu, (int)kmax);
             float kf = 0.f;
-#pragma unroll 1
+            DAXM_UNROLL(DAXM_LOCK_KUNROLL)
             for (int k = 0; k < K; ++k, kf += 1.f) {
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {

@@ -60,7 +60,7 @@ struct daxm_plan {
     int max_nv = 0;
     // TMA descriptors, re-encoded when the caller's buffers change
     CUtensorMap in_map{}, out_map{};
-    CUtensorMap lock_in_map{};  // step-locked kernel: one warp's [16 rows][8 cols] block per wire step
+    CUtensorMap lock_in_map{};  // step-locked kernel: one warp's [16 rows][8 cols] block of LOCK_G wire steps
     int lock_small = 0, lock_large = 0, lock_rest = 0;                // tile counts (lock pre-pass)
     unsigned* d_lock_err = nullptr;                                   // ring-capacity violations
     const void* map_stack = nullptr;
@@ -1007,10 +1007,10 @@ static daxm_status encode_maps(daxm_plan* p, const void* d_stack, int dt, float*
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(p, DAXM_ERR_CUDA, "cuTensorMapEncodeTiled(out) failed: %d", (int)r);
     }
-    {   // step-locked kernel: one warp's [16 rows][8 cols] block per wire step
+    {   // step-locked kernel: one warp's [16 rows][8 cols] block of LOCK_G consecutive wire steps
         cuuint64_t dims[3] = {C, R, (cuuint64_t)p->S};
         cuuint64_t strides[2] = {C * es, C * R * es};
-        cuuint32_t box[3] = {(cuuint32_t)TILE_C, (cuuint32_t)LOCK_ROWS, 1};
+        cuuint32_t box[3] = {(cuuint32_t)TILE_C, (cuuint32_t)LOCK_ROWS, (cuuint32_t)LOCK_G};
         cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = enc(&p->lock_in_map, dt == DAXM_U16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                          3, const_cast<void*>(d_stack), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
