@@ -130,9 +130,9 @@ struct DepositArgs {
 };
 
 // Step-locked deposit kernel (deposit_lock.cu): one warp = 16 detector rows x 8 columns,
-// lanes = 8 columns x 4 row groups, 4 pixel walks (rows) per thread.  Every walk advances
-// one wire step per iteration (aligned at its own window start); the edges of the zone the
-// step closes are evaluated in a warp-uniform loop.  Output planes go through a per-warp
+// lanes = 8 columns x 4 row groups, 4 pixel walks (rows) per thread.  Every walk of a warp
+// visits the same wire step at the same iteration (warp-locked, from the warp's first window
+// start); the edges of the zone the step closes are evaluated in a warp-uniform loop.  Output planes go through a per-warp
 // ring of LOCK_RB planes indexed by bin edge.
 constexpr int LOCK_ROWS = 16;       // detector rows per warp
 constexpr int LOCK_WARPS = 4;       // warps per CTA (independent pipelines)
@@ -148,9 +148,6 @@ constexpr int LOCK_RB_LARGE = 32;
 // iteration, inclusive) a ring of rb planes holds: planes below the frontier are copied out
 // before the next iteration, so writes stay below frontier - 1 + rb
 constexpr int lock_need_max(int rb) { return rb; }
-// window-start spread (steps) a warp's input ring holds: at iteration jj the groups up to
-// (jj + NB - G) / G are issued, and the fastest walk needs visit vmin0 + spread + jj + 1
-constexpr int LOCK_SPREAD_MAX = LOCK_NB - LOCK_G - 1;
 static_assert(LOCK_NB % LOCK_G == 0 && (LOCK_NB / LOCK_G & (LOCK_NB / LOCK_G - 1)) == 0, "lock input ring shape");
 
 // Corner depth of one pixel edge at fp32 wire travel tau (bins relative to m_ref): the

@@ -12,11 +12,14 @@
 // pairs, one owner per (bin, pixel), no atomics.
 //
 // How it is scheduled differs: instead of walking bin edges and branching into a zone
-// transition whenever a pixel crosses a knot (divergent, serialised per walk), every
-// walk advances exactly ONE wire step per iteration -- walk p processes point
-// v0(p) + j at iteration j, v0 its own window start -- and then evaluates the bin edges
-// of the zone that step closed in a warp-uniform, predicated loop.  All control flow is
-// warp-uniform; walk pairs run in packed fp32x2 (FFMA2/FADD2/FMUL2).
+// transition whenever a pixel crosses a knot (divergent, serialised per walk), every walk of
+// a warp advances exactly ONE wire step per iteration -- all walks process visit vmin0 + j at
+// iteration j, vmin0 the warp's first window start (from the geometry windows, so the cutoff
+// cannot change an active walk's arithmetic) -- and then evaluates the bin edges of the zone
+// that step closed in a warp-uniform, predicated loop.  Before its own window a walk's zones
+// lie below the bins (they only offset F, which the bin differences cancel); after it they lie
+// above (no edge left: pre-pass).  The wire travel and the input slot are warp-uniform, all
+// control flow is warp-uniform, and walk pairs run in packed fp32x2 (FFMA2/FADD2/FMUL2).
 //
 // Warp = 16 detector rows x 8 columns, an independent pipeline (no CTA-level sync after
 // setup): lane = (row group rg = lane / 8, column = lane % 8), walk w (0..3) = row
@@ -193,38 +196,35 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
     // ---- walks: rows wrow + 4w + rg, column col
     const int i = col0 + col;
     float cbs[4][3], cfs[4][3];
-    int v0[4], npts[4];
-    int vmin0 = INT_MAX, vmax0 = INT_MIN, vend = INT_MIN, niter = 0;
+    bool act[4];
+    int vmin0 = INT_MAX, vend = INT_MIN;
 #pragma unroll
     for (int w = 0; w < 4; ++w) {
         const int r = wrow + 4 * w + rg;
         const int j = row0 + r;
-        bool act = true;
+        bool on = true;
         if (a.use_cutoff && j < a.row_end && i < a.C) {  // intensity cutoff (f1, reading R14)
             const T* s0 = static_cast<const T*>(a.stack) + (size_t)(j - a.row_begin) * a.C + i;
-            act = (float)s0[0] >= a.cutoff;
+            on = (float)s0[0] >= a.cutoff;
         }
-        const LockWalk lw = lock_walk(a, ti, j, i, act);
-        v0[w] = lw.v0;
-        npts[w] = lw.npts;
+        // the warp's visit range comes from the geometry windows alone, so an active walk's
+        // arithmetic (hence its output, bit for bit) does not depend on which others are active
+        const LockWalk lw = lock_walk(a, ti, j, i, true);
+        act[w] = on && lw.npts > 0;
         if (ti.lock & LOCK_FRONT_LO)  // the front edge is the shallower one over the whole tile (pre-pass)
             lock_coef(a, tile, r, col, POINT, cfs[w], cbs[w]);
         else
             lock_coef(a, tile, r, col, POINT, cbs[w], cfs[w]);
         if (lw.npts > 0) {
             vmin0 = min(vmin0, lw.v0);
-            vmax0 = max(vmax0, lw.v0);
             vend = max(vend, lw.v0 + lw.npts - 1);
-            niter = max(niter, lw.npts);
         }
     }
     vmin0 = __reduce_min_sync(0xffffffffu, vmin0);
-    vmax0 = __reduce_max_sync(0xffffffffu, vmax0);
     vend = __reduce_max_sync(0xffffffffu, vend);
-    niter = __reduce_max_sync(0xffffffffu, niter);
-#pragma unroll
-    for (int w = 0; w < 4; ++w)
-        if (npts[w] == 0) v0[w] = vmin0;  // inactive walks read (and ignore) the slowest walk's data
+    // warp-locked walks: every walk visits vmin0 + jj at iteration jj (0 <= jj < niter)
+    const bool any_act = __any_sync(0xffffffffu, act[0] || act[1] || act[2] || act[3]);
+    const int niter = any_act && vend >= vmin0 ? vend - vmin0 + 1 : 0;
 
     const int rows_band = a.row_end - a.row_begin;
     const int row_local = row0 - a.row_begin + wrow;  // input / output row of the warp's first row
@@ -275,9 +275,9 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
         // Visits vmin0 + 4g .. + 3 form group g: one TMA box of LOCK_G consecutive wire steps
         // (ascending k, so for dir < 0 a group's visits land in reverse slot order: slot =
         // ((v - vmin0) ^ xr) mod NB) completing mbarrier g mod NG.  Group g reuses the slots of
-        // group g - NG, free once every walk has read past it: at iteration jj the slowest walk
-        // has consumed the visits below vmin0 + jj, so groups up to (jj + NB - G) / G may be in
-        // flight; the fastest walk needs visit vmax0 + jj + 1, at most LOCK_SPREAD_MAX + jj + 1.
+        // group g - NG, free once every walk has read past it: at iteration jj the walks have
+        // consumed the visits below vmin0 + jj, so groups up to (jj + NB - G) / G may be in
+        // flight; the prefetch needs visit vmin0 + jj + 1.
         const int xr = dir > 0 ? 0 : LOCK_G - 1;
         const int ngroups = (vend - vmin0) / LOCK_G + 1;
         const int kbase = dir > 0 ? ti.k_lo + vmin0 : ti.k_hi - vmin0 - (LOCK_G - 1);
@@ -309,10 +309,6 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
         // per-lane addresses
         const uint32_t in_lane = s_in + (uint32_t)(rg * TILE_C + col) * (uint32_t)sizeof(T);  // + w * 4 rows
         const uint32_t out_lane = s_out + (uint32_t)(rg * TILE_C + col) * 4u;                 // + w * 128
-        auto in_addr = [&](int w, int v) -> uint32_t {
-            return in_lane + (uint32_t)(((v - vmin0) ^ xr) & (LOCK_NB - 1)) * (uint32_t)L::IN_SLOT +
-                   (uint32_t)(w * 4 * TILE_C * (int)sizeof(T));
-        };
 
         // ---- walk state, packed by walk pairs (0,1), (2,3)
         float2 cb[2][3], cf[2][3];
@@ -323,35 +319,34 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
                 cb[p][m] = make_float2(cbs[2 * p][m], cbs[2 * p + 1][m]);
                 cf[p][m] = make_float2(cfs[2 * p][m], cfs[2 * p + 1][m]);
             }
-        int vlast[4];
-#pragma unroll
-        for (int w = 0; w < 4; ++w) vlast[w] = npts[w] > 0 ? v0[w] + npts[w] - 1 : vmin0;
-        auto fetch = [&](int w, int v, float& t, float& I) {
-            const int vv = min(v, vlast[w]);
-            t = lds_f32(s_tau + 4u * (uint32_t)vv);
-            I = lds_px<T>(in_addr(w, vv));
+        // wire travel (warp-uniform) and the 4 walks' intensities at visit vmin0 + jj; past the
+        // last visit every walk re-reads it (its points lie above EM: pre-pass)
+        auto fetch = [&](int jj, float& t, float2 I[2]) {
+            const int vv = min(jj, niter - 1);
+            t = lds_f32(s_tau + 4u * (uint32_t)(vmin0 + vv));
+            const uint32_t sl = in_lane + (uint32_t)((vv ^ xr) & (LOCK_NB - 1)) * (uint32_t)L::IN_SLOT;
+            constexpr uint32_t WB = 4 * TILE_C * sizeof(T);  // walk w: rows + 4 w
+            I[0] = make_float2(lds_px<T>(sl), lds_px<T>(sl + WB));
+            I[1] = make_float2(lds_px<T>(sl + 2 * WB), lds_px<T>(sl + 3 * WB));
         };
 
-        wait_upto(vmax0 + 1);
-        float2 plo[2], phi[2], ps[2], pI[2], cq[2], zF[2], Fp[2], En[2], tq[2], Iq[2];
+        wait_upto(vmin0 + 1);
+        float2 plo[2], phi[2], ps[2], pI[2], cq[2], zF[2], Fp[2], En[2], Iq[2];
+        float tq;
+        {
+            float t0;
+            fetch(0, t0, pI);
 #pragma unroll
-        for (int p = 0; p < 2; ++p) {
-            float t0, t1, I0, I1;
-            fetch(2 * p, v0[2 * p], t0, I0);
-            fetch(2 * p + 1, v0[2 * p + 1], t1, I1);
-            const float2 t = make_float2(t0, t1);
-            plo[p] = poly2(cb[p], t);  // lo edge / hi edge: fixed order over the window (pre-pass)
-            phi[p] = POINT ? plo[p] : poly2(cf[p], t);
-            ps[p] = add2(plo[p], phi[p]);
-            pI[p] = make_float2(I0, I1);
-            cq[p] = zF[p] = Fp[p] = f2(0.f);
-            // first edge: the first above point 0's lo (F = 0 below it); inactive walks never evaluate
-            En[p].x = npts[2 * p] > 0 ? fmaxf(E0, floorf(plo[p].x) + 1.f) : EM + 1.f;
-            En[p].y = npts[2 * p + 1] > 0 ? fmaxf(E0, floorf(plo[p].y) + 1.f) : EM + 1.f;
-            fetch(2 * p, v0[2 * p] + 1, t0, I0);
-            fetch(2 * p + 1, v0[2 * p + 1] + 1, t1, I1);
-            tq[p] = make_float2(t0, t1);
-            Iq[p] = make_float2(I0, I1);
+            for (int p = 0; p < 2; ++p) {
+                plo[p] = poly2(cb[p], f2(t0));  // lo edge / hi edge: fixed order over the tile (pre-pass)
+                phi[p] = POINT ? plo[p] : poly2(cf[p], f2(t0));
+                ps[p] = add2(plo[p], phi[p]);
+                cq[p] = zF[p] = Fp[p] = f2(0.f);
+                // first edge: the first above point 0's lo (F = 0 below it); inactive walks never evaluate
+                En[p].x = act[2 * p] ? fmaxf(E0, floorf(plo[p].x) + 1.f) : EM + 1.f;
+                En[p].y = act[2 * p + 1] ? fmaxf(E0, floorf(plo[p].y) + 1.f) : EM + 1.f;
+            }
+            fetch(1, tq, Iq);
         }
         const float2 sdir2 = f2(2.f * a.sign * (float)dir);  // c = 2 s dir dI / (sum_{q+1} - sum_q)
         const int m_ref = a.m_ref;
@@ -368,28 +363,22 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
         unsigned viol = 0u;
 #endif
 
-        // iteration jj closes zone jj - 1 of every walk with jj < npts; a window's last zone lies
-        // above the bins (pre-pass), so iteration niter would close nothing
+        // iteration jj closes zone jj - 1 of every walk; before its own window a walk's zones lie
+        // below the bins (F offset only), after it above them (no edge left: pre-pass)
         DAXM_UNROLL(DAXM_LOCK_UNROLL)
         for (int jj = 1; jj < niter; ++jj) {
             // point jj (prefetched); refill the ring below the slowest walk; prefetch point jj + 1
             issue(jj);
-            wait_upto(vmax0 + jj + 1);
+            wait_upto(vmin0 + jj + 1);
             float2 zlo[2], zw[2], zc[2], zd[2], zg[2], zF0[2], Eb[2];
-            float2 tn[2], In[2];
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                float t0, t1, I0, I1;
-                fetch(2 * p, v0[2 * p] + jj + 1, t0, I0);
-                fetch(2 * p + 1, v0[2 * p + 1] + jj + 1, t1, I1);
-                tn[p] = make_float2(t0, t1);
-                In[p] = make_float2(I0, I1);
-            }
+            float tn;
+            float2 In[2];
+            fetch(jj + 1, tn, In);
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
                 // past its window a walk re-reads its last point (lo >= EM, pre-pass): no edges
                 // remain below EM for it, whatever its zone arithmetic produces
-                const float2 lo = poly2(cb[p], tq[p]), hi = POINT ? lo : poly2(cf[p], tq[p]);
+                const float2 lo = poly2(cb[p], f2(tq)), hi = POINT ? lo : poly2(cf[p], f2(tq));
                 const float2 s = add2(lo, hi);
                 const float2 c = mul2(mul2(sdir2, sub2(pI[p], Iq[p])), rcp2(sub2(s, ps[p])));
                 const float2 w = sub2(phi[p], plo[p]);
@@ -409,9 +398,9 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
                 ps[p] = s;
                 pI[p] = Iq[p];
                 cq[p] = c;
-                tq[p] = tn[p];
                 Iq[p] = In[p];
             }
+            tq = tn;
             // ---- edges of zone jj - 1: En .. floor(min(lo_jj, EM)), a warp-uniform trip count
             uint32_t es[4];
             float2 x[2], cm[2], fl[2];
@@ -453,8 +442,8 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
                 const float lim = (float)(done_p + RB - m_ref + 1);  // edge bound: e - 1 < done_p + RB
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    if (jj <= npts[2 * p] && En[p].x - 1.f >= lim) viol = 1u;
-                    if (jj <= npts[2 * p + 1] && En[p].y - 1.f >= lim) viol = 1u;
+                    if (cm[p].x >= 0.f && En[p].x - 1.f >= lim) viol = 1u;  // highest edge stored this iteration
+                    if (cm[p].y >= 0.f && En[p].y - 1.f >= lim) viol = 1u;
                 }
             }
 #endif
@@ -469,13 +458,14 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
 }
 
 // ------------------------------------------------------------------ pre-pass
-// Replays, per tile and lock warp, the walks' per-iteration edge bounds with the kernel's
-// own fp32 arithmetic (lock_poly, fminf, floorf) and classifies the tile:
-//   * the same pixel edge (back or front) is the shallower one at every point of every window
-//     of the tile (the kernel then skips the per-point min/max; flag LOCK_FRONT_LO);
+// Replays, per tile and lock warp, the kernel's warp-locked walks with its own fp32 arithmetic
+// (lock_poly, fminf, floorf) and classifies the tile:
+//   * the same pixel edge (back or front) is the shallower one at every point any walk of the
+//     tile evaluates (the kernel then skips the per-point min/max; flag LOCK_FRONT_LO);
+//   * consecutive points of a walk have distinct edge sums (finite zone densities, also before
+//     and after the walk's own window);
 //   * every window's last point lies at or above the top bin edge EM, so a walk past its
 //     window has no edge left (the kernel needs no end-of-window case);
-//   * the warp's input-ring spread of window starts is at most LOCK_SPREAD_MAX;
 //   * the output-ring need, max over iterations j of
 //       (furthest edge written at j) - (slowest walk's next edge after j - 1) + 1,
 //     fits LOCK_RB_SMALL or LOCK_RB_LARGE planes -> lock = that class (0: not eligible).
@@ -490,9 +480,9 @@ __global__ void __launch_bounds__(256) lock_prepass_kernel(DepositArgs a, TileIn
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;  // 8 warps = TILE_R / 16 lock warps
     const int col = lane & 7, rg = lane >> 3;
     const int wrow = warp * LOCK_ROWS;
-    __shared__ int s_need, s_spread, s_bad, s_back_lo, s_front_lo;
+    __shared__ int s_need, s_bad, s_back_lo, s_front_lo;
     if (threadIdx.x == 0) {
-        s_need = s_spread = s_bad = 0;
+        s_need = s_bad = 0;
         s_back_lo = s_front_lo = 1;
     }
     __syncthreads();
@@ -501,9 +491,9 @@ __global__ void __launch_bounds__(256) lock_prepass_kernel(DepositArgs a, TileIn
     if (eligible) {
         const int i = tc * TILE_C + col;
         const float E0 = (float)(-a.m_ref), EM = (float)(a.M - a.m_ref);
-        float cb[4][3] = {}, cf[4][3] = {}, En[4];
-        int v0[4], npts[4];
-        int vmin0 = INT_MAX, vmax0 = INT_MIN, niter = 0;
+        float cb[4][3] = {}, cf[4][3] = {}, En[4], ps[4] = {};
+        bool on[4];
+        int vmin0 = INT_MAX, vend = INT_MIN;
         bool back_lo = true, front_lo = true, bad = false;
         auto point = [&](int w, int v, float& x0, float& x1) {
             const int k = ti.dir > 0 ? ti.k_lo + v : ti.k_hi - v;
@@ -516,34 +506,40 @@ __global__ void __launch_bounds__(256) lock_prepass_kernel(DepositArgs a, TileIn
         for (int w = 0; w < 4; ++w) {
             const int r = wrow + 4 * w + rg;
             const LockWalk lw = lock_walk(a, ti, row0 + r, i, true);
-            v0[w] = lw.v0;
-            npts[w] = lw.npts;
+            on[w] = lw.npts > 0;
             lock_coef(a, tile, r, col, a.point_mode != 0, cb[w], cf[w]);
-            En[w] = EM + 1.f;
-            if (lw.npts > 0) {
+            if (on[w]) {
                 vmin0 = min(vmin0, lw.v0);
-                vmax0 = max(vmax0, lw.v0);
-                niter = max(niter, lw.npts);
+                vend = max(vend, lw.v0 + lw.npts - 1);
                 float x0, x1;
-                point(w, lw.v0, x0, x1);
-                En[w] = fmaxf(E0, floorf(fminf(x0, x1)) + 1.f);
                 point(w, lw.v0 + lw.npts - 1, x0, x1);
                 bad |= !(fminf(x0, x1) >= EM);  // last point at or above the top bin edge
             }
         }
         vmin0 = __reduce_min_sync(0xffffffffu, vmin0);
-        vmax0 = __reduce_max_sync(0xffffffffu, vmax0);
-        niter = __reduce_max_sync(0xffffffffu, niter);
+        vend = __reduce_max_sync(0xffffffffu, vend);
+        const int niter = vend >= vmin0 ? vend - vmin0 + 1 : 0;
         int need = 0;
         if (niter > 0) {
+            for (int w = 0; w < 4; ++w) {
+                En[w] = EM + 1.f;
+                if (!on[w]) continue;
+                float x0, x1;
+                point(w, vmin0, x0, x1);
+                En[w] = fmaxf(E0, floorf(fminf(x0, x1)) + 1.f);
+                ps[w] = x0 + x1;
+            }
             float fr = fminf(fminf(En[0], En[1]), fminf(En[2], En[3]));
             int fr_e = __reduce_min_sync(0xffffffffu, (int)fr + a.m_ref);
             for (int jj = 1; jj < niter; ++jj) {  // iterations >= niter close no edge (last points >= EM)
                 float mx = -3.0e38f;
                 for (int w = 0; w < 4; ++w) {
-                    if (jj >= npts[w]) continue;
+                    if (!on[w]) continue;
                     float x0, x1;
-                    point(w, v0[w] + jj, x0, x1);
+                    point(w, vmin0 + jj, x0, x1);
+                    const float sum = x0 + x1;
+                    bad |= !(sum != ps[w]);  // the zone density needs a finite 1 / (sum - previous sum)
+                    ps[w] = sum;
                     const float Eb = fminf(fminf(x0, x1), EM);
                     if (En[w] <= Eb) mx = fmaxf(mx, Eb);
                     En[w] = fmaxf(En[w], floorf(Eb) + 1.f);
@@ -554,10 +550,7 @@ __global__ void __launch_bounds__(256) lock_prepass_kernel(DepositArgs a, TileIn
                 fr_e = __reduce_min_sync(0xffffffffu, (int)fr + a.m_ref);
             }
         }
-        if (lane == 0) {
-            atomicMax(&s_need, need);
-            if (niter > 0) atomicMax(&s_spread, vmax0 - vmin0);
-        }
+        if (lane == 0) atomicMax(&s_need, need);
         if (bad) atomicOr(&s_bad, 1);
         if (!back_lo) atomicAnd(&s_back_lo, 0);
         if (!front_lo) atomicAnd(&s_front_lo, 0);
@@ -565,7 +558,7 @@ __global__ void __launch_bounds__(256) lock_prepass_kernel(DepositArgs a, TileIn
     __syncthreads();
     if (threadIdx.x == 0) {
         int lock = 0;
-        if (eligible && s_spread <= LOCK_SPREAD_MAX && !s_bad && (s_back_lo || s_front_lo)) {
+        if (eligible && !s_bad && (s_back_lo || s_front_lo)) {
             if (s_need <= lock_need_max(LOCK_RB_SMALL))
                 lock = LOCK_RB_SMALL;
             else if (s_need <= lock_need_max(LOCK_RB_LARGE))
