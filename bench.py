@@ -357,8 +357,9 @@ def launches_per_step(st, dtype):
     any non-general tile is left to it, the general kernel if any tile needs it."""
     general = st["general_tiles_u16" if dtype == "u16" else "general_tiles_f32"]
     small, large = st.get("lock_tiles_small", 0), st.get("lock_tiles_large", 0)
-    rest = st["n_tiles"] - general - small - large
-    n = (small > 0) + (large > 0) + (general > 0)
+    ov = st.get("lock_tiles_overlap", 0)  # one launch per ring class in use (counted together: an upper bound)
+    rest = st["n_tiles"] - general - small - large - ov
+    n = (small > 0) + (large > 0) + (general > 0) + (ov > 0)
     if rest > 0:
         n += 1 + (st["overlap_tiles"] > 0)
     return int(n)
@@ -429,7 +430,8 @@ def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_ma
             "plan": {"contrib_pairs": st["contrib_pairs"], "window_pairs": st["window_pairs"],
                      "general_tiles": st["general_tiles_u16" if cfg.dtype == "u16" else "general_tiles_f32"],
                      "n_tiles": st["n_tiles"], "lock_tiles_small": st.get("lock_tiles_small"),
-                     "lock_tiles_large": st.get("lock_tiles_large"), "overlap_tiles": st["overlap_tiles"],
+                     "lock_tiles_large": st.get("lock_tiles_large"), "lock_tiles_overlap": st.get("lock_tiles_overlap"),
+                     "overlap_tiles": st["overlap_tiles"],
                      "staged_steps": st["staged_steps"], "fit_max_err_bins": st["fit_max_err_bins"],
                      "fit_model_err_bins": st["fit_model_err_bins"]},
         }

@@ -107,6 +107,7 @@ typedef struct {
     int64_t lock_tiles_large;  /* ... with a 32-plane output ring                                         */
     int64_t lock_ring_violations; /* step-locked ring-capacity violations so far (read synchronously;    */
                                /* always 0: the pre-pass admits only tiles whose ring provably suffices) */
+    int64_t lock_tiles_overlap; /* overlapping-span tiles the step-locked ramp-superposition kernel handles */
 } daxm_plan_stats;
 
 /* daxm_create -- validate `g`, run the fp64 geometry pre-pass on `cuda_device`,

@@ -53,6 +53,7 @@ class PlanStats(C.Structure):
         ("fit_max_err_bins", C.c_double), ("fit_model_err_bins", C.c_double), ("prepass_ms", C.c_double), ("device_bytes", C.c_int64),
         ("depth_table_bytes", C.c_int64),
         ("lock_tiles_small", C.c_int64), ("lock_tiles_large", C.c_int64), ("lock_ring_violations", C.c_int64),
+        ("lock_tiles_overlap", C.c_int64),
     ]
 
 

@@ -126,6 +126,8 @@ struct DepositArgs {
     float cutoff;
     int lock_enabled;         // step-locked kernel handles tiles with tiles[].lock != 0
     int lock_small, lock_large, lock_rest;  // tile counts: lock classes, fast tiles left to deposit_fast
+    int lock_ov_small, lock_ov_large;       // ... overlapping tiles in deposit_lock_ov
+    int lock_ov_enabled;                    // pre-pass: admit overlapping tiles (unset by DAXM_NO_LOCK_OV)
     unsigned* lock_err;       // device word: ring-capacity violations (must stay 0)
 };
 
@@ -142,6 +144,8 @@ constexpr int LOCK_G = 4;           // wire steps per TMA box and mbarrier (one 
 constexpr int LOCK_NG = LOCK_NB / LOCK_G;  // groups in the input ring
 constexpr int LOCK_CLASS_MASK = 0xff;  // TileInfo.lock: ring class in the low byte
 constexpr int LOCK_FRONT_LO = 0x100;   //   flag: the front pixel edge is the shallower over the whole tile
+constexpr int LOCK_OVB = 0x40;         //   class bit: overlapping edge spans (deposit_lock_ov, ramp superposition)
+constexpr int LOCK_P = 4;              // ramps deposit_lock_ov keeps quadratic: hi_q <= lo_{q+LOCK_P} (pre-pass)
 constexpr int LOCK_RB_SMALL = 16;   // output ring planes per warp
 constexpr int LOCK_RB_LARGE = 32;
 // largest "need" (edges from the slowest walk's frontier to the furthest edge written in one

@@ -62,6 +62,7 @@ struct daxm_plan {
     CUtensorMap in_map{}, out_map{};
     CUtensorMap lock_in_map{};  // step-locked kernel: one warp's [16 rows][8 cols] block of LOCK_G wire steps
     int lock_small = 0, lock_large = 0, lock_rest = 0;                // tile counts (lock pre-pass)
+    int lock_ov_small = 0, lock_ov_large = 0;                         // ... overlapping tiles
     unsigned* d_lock_err = nullptr;                                   // ring-capacity violations
     const void* map_stack = nullptr;
     const float* map_out = nullptr;
@@ -779,19 +780,22 @@ daxm_status device_prepass(daxm_plan* p) {
     }
     // ---- step-locked kernel: per tile, replay the walks' edge frontiers in fp32 and admit the
     // tile if its per-warp output ring provably holds them (deposit_lock.cu)
-    CK(cudaMalloc(&p->d_lock_err, 16));
-    CK(cudaMemset(p->d_lock_err, 0, 16));
+    CK(cudaMalloc(&p->d_lock_err, 32));
+    CK(cudaMemset(p->d_lock_err, 0, 32));
     if (!use_table) {
         int* d_ls = reinterpret_cast<int*>(p->d_lock_err) + 1;
         DepositArgs a = make_args(p, DAXM_U16);
         CK(launch_lock_prepass(a, (int)n_tiles, d_ls, 0));
-        int hs[3];
+        int hs[5];
         CK(cudaMemcpy(hs, d_ls, sizeof hs, cudaMemcpyDeviceToHost));
         p->lock_small = hs[0];
         p->lock_large = hs[1];
         p->lock_rest = hs[2];
+        p->lock_ov_small = p->gc.point_mode ? 0 : hs[3];
+        p->lock_ov_large = p->gc.point_mode ? 0 : hs[4];
         st.lock_tiles_small = hs[0];
         st.lock_tiles_large = hs[1];
+        st.lock_tiles_overlap = p->lock_ov_small + p->lock_ov_large;
     }
     return DAXM_OK;
 }
@@ -947,9 +951,13 @@ static DepositArgs make_args(const daxm_plan* p, int dtype) {
     a.toff = p->d_toff;
     a.use_cutoff = p->use_cutoff;
     a.cutoff = p->cutoff;
-    a.lock_enabled = (p->lock_small + p->lock_large) > 0 && getenv("DAXM_NO_LOCK") == nullptr;
+    a.lock_enabled = (p->lock_small + p->lock_large + p->lock_ov_small + p->lock_ov_large) > 0 &&
+                     getenv("DAXM_NO_LOCK") == nullptr;
     a.lock_small = p->lock_small;
     a.lock_large = p->lock_large;
+    a.lock_ov_small = p->lock_ov_small;
+    a.lock_ov_large = p->lock_ov_large;
+    a.lock_ov_enabled = getenv("DAXM_NO_LOCK_OV") == nullptr;
     a.lock_rest = a.lock_enabled ? p->lock_rest : 1;
     a.lock_err = p->d_lock_err;
     return a;

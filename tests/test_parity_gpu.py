@@ -247,22 +247,38 @@ def test_benchmark_configs_take_the_fast_path(daxm, name):
     assert st[key] == 0, {k: st[k] for k in ("nonseparated_tiles", "ring_need_max", key)}
 
 
-def test_c5_overlapping_tiles_use_the_dual_walk(daxm):
+def test_c5_overlapping_tiles_use_the_ramp_superposition_kernel(daxm):
     """C5's finest bins make the pixel-edge span exceed the per-step sweep on the detector's
-    shallow side: those tiles run the fast kernel's overlap (dual ramp walk) mode; only tiles
-    mixing both regimes fall back to the general kernel."""
+    shallow side: those tiles run the step-locked ramp-superposition kernel (deposit_lock_ov);
+    only tiles mixing both regimes fall back to the general kernel."""
     cfg = synth.get_config("C5")
     with daxm.create(synth.geometry(cfg), device=0) as plan:
         st = plan.stats()
     assert st["overlap_tiles"] > 0
+    assert st["lock_tiles_overlap"] == st["overlap_tiles"], st
     assert st["general_tiles_u16"] == st["nonseparated_tiles"] - st["overlap_tiles"]
     assert st["general_tiles_u16"] < st["n_tiles"] // 20
 
 
 @pytest.mark.parametrize("dtype", ["u16", "f32"])
+def test_overlap_regime_dual_walk_fallback(daxm, dtype, monkeypatch):
+    """DAXM_NO_LOCK_OV keeps the overlapping tiles on the fast kernel's dual ramp walk: both
+    algebras of the overlap regime match the oracle."""
+    monkeypatch.setenv("DAXM_NO_LOCK_OV", "1")
+    g = synth.geometry("C2", n_rows=96, n_cols=64)
+    g["wire_xyz"] = synth.wire_positions(1601, t_range=(40.0, 1040.0))
+    g["depth_res"] = 0.5
+    rng = np.random.default_rng(18)
+    host = (3000 + rng.integers(-400, 400, (1601, 96, 64))).astype(np.uint16 if dtype == "u16" else np.float32)
+    gpu, st = run_gpu(daxm, g, host)
+    assert st["overlap_tiles"] == st["n_tiles"] and st["lock_tiles_overlap"] == 0, st
+    parity.check(gpu, oracle.reconstruct(g, host), host, f"overlap dual walk {dtype}")
+
+
+@pytest.mark.parametrize("dtype", ["u16", "f32"])
 def test_overlap_regime_parity(daxm, dtype):
     """Many fine wire steps on a coarse-pitch detector: every pixel's edge span (0.68 um) exceeds
-    the per-step sweep (0.24-0.6 um) -> all tiles in the overlap mode of the fast kernel."""
+    the per-step sweep (0.24-0.6 um) -> all tiles overlapping, all in deposit_lock_ov."""
     g = synth.geometry("C2", n_rows=96, n_cols=64)
     g["wire_xyz"] = synth.wire_positions(1601, t_range=(40.0, 1040.0))
     g["depth_res"] = 0.5
@@ -270,6 +286,7 @@ def test_overlap_regime_parity(daxm, dtype):
     host = (3000 + rng.integers(-400, 400, (1601, 96, 64))).astype(np.uint16 if dtype == "u16" else np.float32)
     gpu, st = run_gpu(daxm, g, host)
     assert st["overlap_tiles"] == st["n_tiles"], st
+    assert st["lock_tiles_overlap"] == st["n_tiles"], st  # the ramp-superposition kernel
     parity.check(gpu, oracle.reconstruct(g, host), host, f"overlap {dtype}")
 
 
