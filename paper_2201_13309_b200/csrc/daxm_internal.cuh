@@ -167,10 +167,10 @@ cudaError_t launch_depth_profile(const float* out, int M, size_t plane, double* 
 size_t fast_smem_bytes(int dtype, int max_nv);
 cudaError_t launch_deposit(const DepositArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
                            const void* stack, int dtype, float* out, bool fast_enabled, cudaStream_t st,
-                           const CUtensorMap* lock_in_map);
+                           const CUtensorMap* lock_in_map, const cudaStream_t* lock_sts, int n_lock_sts);
 size_t lock_smem_bytes(int dtype, int rb, int max_nv);
 cudaError_t launch_lock(const DepositArgs& a, const CUtensorMap* in_map, float* out, int dtype, int n_tiles,
-                        cudaStream_t st);
+                        const cudaStream_t* sts, int nst);
 cudaError_t launch_lock_prepass(const DepositArgs& a, int n_tiles, int* d_stats, cudaStream_t st);
 
 }  // namespace daxm

@@ -751,13 +751,13 @@ size_t fast_smem_bytes(int dtype, int max_nv) {
 
 cudaError_t launch_deposit(const DepositArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
                            const void* stack, int dtype, float* out, bool fast_enabled, cudaStream_t st,
-                           const CUtensorMap* lock_in_map) {
+                           const CUtensorMap* lock_in_map, const cudaStream_t* lock_sts, int n_lock_sts) {
     const int n_tiles = (a.tr_end - a.tr_begin) * a.n_tc;
     if (n_tiles <= 0) return cudaSuccess;
     cudaError_t e = cudaSuccess;
     if (fast_enabled) {
         if (a.lock_enabled) {
-            e = launch_lock(a, lock_in_map, out, dtype, n_tiles, st);
+            e = launch_lock(a, lock_in_map, out, dtype, n_tiles, lock_sts, n_lock_sts);
             if (e != cudaSuccess) return e;
         }
         if (a.lock_rest > 0)

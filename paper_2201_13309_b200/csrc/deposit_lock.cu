@@ -933,20 +933,26 @@ cudaError_t launch_lock_rb(const CUtensorMap* in_map, float* out, const DepositA
 }
 
 template <typename T>
-cudaError_t launch_lock_t(const DepositArgs& a, const CUtensorMap* in_map, float* out, int n_tiles, cudaStream_t st) {
+cudaError_t launch_lock_t(const DepositArgs& a, const CUtensorMap* in_map, float* out, int n_tiles,
+                          const cudaStream_t* sts, int nst) {
+    // one launch per tile class; class i goes to stream i mod nst (the classes own disjoint
+    // tiles, so with nst > 1 they run concurrently and share each other's tails)
     cudaError_t e = cudaSuccess;
+    int i = 0;
     if (a.lock_small > 0)
-        e = a.point_mode ? launch_lock_rb<T, true, LOCK_RB_SMALL, false>(in_map, out, a, n_tiles, st)
-                         : launch_lock_rb<T, false, LOCK_RB_SMALL, false>(in_map, out, a, n_tiles, st);
+        e = a.point_mode ? launch_lock_rb<T, true, LOCK_RB_SMALL, false>(in_map, out, a, n_tiles, sts[i++ % nst])
+                         : launch_lock_rb<T, false, LOCK_RB_SMALL, false>(in_map, out, a, n_tiles, sts[i++ % nst]);
     if (e != cudaSuccess) return e;
     if (a.lock_large > 0)
-        e = a.point_mode ? launch_lock_rb<T, true, LOCK_RB_LARGE, false>(in_map, out, a, n_tiles, st)
-                         : launch_lock_rb<T, false, LOCK_RB_LARGE, false>(in_map, out, a, n_tiles, st);
+        e = a.point_mode ? launch_lock_rb<T, true, LOCK_RB_LARGE, false>(in_map, out, a, n_tiles, sts[i++ % nst])
+                         : launch_lock_rb<T, false, LOCK_RB_LARGE, false>(in_map, out, a, n_tiles, sts[i++ % nst]);
     if (e != cudaSuccess) return e;
     // overlapping tiles (never POINT pixels: a point has no edge span)
-    if (a.lock_ov_small > 0 && !a.point_mode) e = launch_lock_rb<T, false, LOCK_RB_SMALL, true>(in_map, out, a, n_tiles, st);
+    if (a.lock_ov_small > 0 && !a.point_mode)
+        e = launch_lock_rb<T, false, LOCK_RB_SMALL, true>(in_map, out, a, n_tiles, sts[i++ % nst]);
     if (e != cudaSuccess) return e;
-    if (a.lock_ov_large > 0 && !a.point_mode) e = launch_lock_rb<T, false, LOCK_RB_LARGE, true>(in_map, out, a, n_tiles, st);
+    if (a.lock_ov_large > 0 && !a.point_mode)
+        e = launch_lock_rb<T, false, LOCK_RB_LARGE, true>(in_map, out, a, n_tiles, sts[i++ % nst]);
     return e;
 }
 
@@ -961,10 +967,10 @@ size_t lock_smem_bytes(int dtype, int rb, int max_nv) {
 }
 
 cudaError_t launch_lock(const DepositArgs& a, const CUtensorMap* in_map, float* out, int dtype, int n_tiles,
-                        cudaStream_t st) {
+                        const cudaStream_t* sts, int nst) {
     if (n_tiles <= 0) return cudaSuccess;
-    return dtype == DAXM_U16 ? launch_lock_t<uint16_t>(a, in_map, out, n_tiles, st)
-                             : launch_lock_t<float>(a, in_map, out, n_tiles, st);
+    return dtype == DAXM_U16 ? launch_lock_t<uint16_t>(a, in_map, out, n_tiles, sts, nst)
+                             : launch_lock_t<float>(a, in_map, out, n_tiles, sts, nst);
 }
 
 cudaError_t launch_lock_prepass(const DepositArgs& a, int n_tiles, int* d_stats, cudaStream_t st) {

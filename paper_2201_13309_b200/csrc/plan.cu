@@ -73,6 +73,8 @@ struct daxm_plan {
     float* d_out_buf = nullptr;
     size_t out_buf_bytes = 0;
     cudaStream_t st_in = nullptr, st_out = nullptr;  // host-path pipeline streams
+    cudaStream_t st_cls[2] = {nullptr, nullptr};     // concurrent step-locked class launches (fork/join)
+    cudaEvent_t ev_cls[3] = {nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> ev;
     int use_cutoff = 0;  // intensity cutoff (f1, reading R14)
     float cutoff = 0.f;
@@ -528,6 +530,10 @@ void free_plan_memory(daxm_plan* p) {
     cudaFree(p->d_toff);
     cudaFree(p->d_lock_err);
     p->d_lock_err = nullptr;
+    for (int i = 0; i < 2; ++i)
+        if (p->st_cls[i]) cudaStreamDestroy(p->st_cls[i]);
+    for (int i = 0; i < 3; ++i)
+        if (p->ev_cls[i]) cudaEventDestroy(p->ev_cls[i]);
     if (p->st_in) cudaStreamDestroy(p->st_in);
     if (p->st_out) cudaStreamDestroy(p->st_out);
     p->st_in = p->st_out = nullptr;
@@ -796,6 +802,12 @@ daxm_status device_prepass(daxm_plan* p) {
         st.lock_tiles_small = hs[0];
         st.lock_tiles_large = hs[1];
         st.lock_tiles_overlap = p->lock_ov_small + p->lock_ov_large;
+        // several tile classes: their launches run concurrently on forked streams
+        const int ncls = (p->lock_small > 0) + (p->lock_large > 0) + (p->lock_ov_small > 0) + (p->lock_ov_large > 0);
+        if (ncls >= 2) {
+            for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&p->st_cls[i], cudaStreamNonBlocking));
+            for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&p->ev_cls[i], cudaEventDisableTiming));
+        }
     }
     return DAXM_OK;
 }
@@ -1043,7 +1055,24 @@ static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float*
     a.tr_begin = tr_begin;
     a.tr_end = tr_end < 0 ? p->n_tr : tr_end;
     a.stack = d_stack;
-    cudaError_t e = launch_deposit(a, &p->in_map, &p->out_map, d_stack, dt, d_out, fast, st, &p->lock_in_map);
+    // fork: class launches on {st, st_cls[0], st_cls[1]}, joined back into st (graph-capturable)
+    const bool fork = fast && a.lock_enabled && p->st_cls[0] != nullptr && getenv("DAXM_NO_FORK") == nullptr;
+    cudaStream_t sts[3] = {st, p->st_cls[0], p->st_cls[1]};
+    cudaError_t e = cudaSuccess;
+    if (fork) {
+        e = cudaEventRecord(p->ev_cls[0], st);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(p->st_cls[i], p->ev_cls[0], 0);
+    }
+    if (e == cudaSuccess)
+        e = launch_deposit(a, &p->in_map, &p->out_map, d_stack, dt, d_out, fast, st, &p->lock_in_map, sts,
+                           fork ? 3 : 1);
+    if (fork) {  // join even after a failed launch, so a capture or the caller's stream stays consistent
+        for (int i = 0; i < 2; ++i) {
+            cudaError_t j = cudaEventRecord(p->ev_cls[1 + i], p->st_cls[i]);
+            if (j == cudaSuccess) j = cudaStreamWaitEvent(st, p->ev_cls[1 + i], 0);
+            if (e == cudaSuccess) e = j;
+        }
+    }
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(p, DAXM_ERR_CUDA, "deposit launch: %s", cudaGetErrorString(e));

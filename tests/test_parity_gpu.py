@@ -521,3 +521,27 @@ def test_lock_ring_check_build(tmp_path):
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res and all(v["lock_ring_violations"] == 0 for v in res.values()), res
     assert all(v["lock_tiles_small"] + v["lock_tiles_large"] > 0 for v in res.values()), res
+
+
+def test_reconstruct_is_graph_capturable(daxm):
+    """daxm_reconstruct is stream-ordered and allocation-free: captured into a CUDA graph (C5:
+    three tile classes whose launches fork onto the plan's streams and join back) and replayed,
+    it reproduces the eager result bit for bit."""
+    import torch
+    cfg = synth.get_config("C5")
+    with daxm.create(synth.geometry(cfg), device=0) as plan:
+        st = plan.stats()
+        assert (st["lock_tiles_small"] > 0) + (st["lock_tiles_large"] > 0) + (st["lock_tiles_overlap"] > 0) >= 2, st
+        stack = synth.stack_torch(synth.make_maps(cfg), cfg.dtype, "cuda:0", noise=False)
+        eager = torch.empty(plan.output_shape(), dtype=torch.float32, device="cuda:0")
+        plan.reconstruct(stack, eager)
+        graphed = torch.full_like(eager, float("nan"))
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                plan.reconstruct(stack, graphed, s)
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(eager, graphed)
