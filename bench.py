@@ -351,10 +351,11 @@ def main():
                   kern_median)
 
 
-def launches_per_step(st, dtype):
+def launches_per_step(st, dtype, cutoff=False):
     """Kernels one daxm_reconstruct launches (csrc/deposit.cu launch_deposit): the step-locked
     kernel once per output-ring class in use, deposit_fast (separated + dual-walk launches) if
-    any non-general tile is left to it, the general kernel if any tile needs it."""
+    any non-general tile is left to it, the general kernel if any tile needs it; with a cutoff
+    also tile_live and zero_dead_tiles (csrc/select.cu)."""
     general = st["general_tiles_u16" if dtype == "u16" else "general_tiles_f32"]
     small, large = st.get("lock_tiles_small", 0), st.get("lock_tiles_large", 0)
     ov = st.get("lock_tiles_overlap", 0)  # one launch per ring class in use (counted together: an upper bound)
@@ -362,7 +363,7 @@ def launches_per_step(st, dtype):
     n = (small > 0) + (large > 0) + (general > 0) + (ov > 0)
     if rest > 0:
         n += 1 + (st["overlap_tiles"] > 0)
-    return int(n)
+    return int(n) + (2 if cutoff else 0)
 
 
 def parity_spot_check(out, kept, r0, cut):
@@ -424,7 +425,7 @@ def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_ma
                          "bytes_rule": "sum_p (S_c(p)+1)*b_in + rows*C*M*4 (SURVEY.md §8(d))"},
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": K * world * launches_per_step(st, cfg.dtype),
+            "gpu_launches": K * world * launches_per_step(st, cfg.dtype, cut[0] is not None),
             "clocks": clocks.summary(),
             "prepass_ms": st["prepass_ms"],
             "plan": {"contrib_pairs": st["contrib_pairs"], "window_pairs": st["window_pairs"],

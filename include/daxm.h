@@ -156,7 +156,8 @@ daxm_status daxm_reconstruct_host(daxm_plan *p, const void *h_stack, daxm_dtype 
  * pixel-percentage experiment).  Reading R14: with enable != 0 a
  * pixel is reconstructed only if its intensity in the FIRST wire-step image, I_0(p),
  * compared in float32, is >= cutoff; every other pixel's output column is 0 and the
- * pixel's inputs are not processed (a tile with no such pixel reads no wire-step planes).
+ * pixel's inputs are not processed (a deposit tile with no such pixel reads no wire-step
+ * planes; its output block is written as zeros by a row-wise fill).
  * enable == 0 (the default) reconstructs every pixel.  Applies to later daxm_reconstruct /
  * daxm_reconstruct_host calls on this plan.  Errors: INVALID_ARGUMENT (NaN cutoff). */
 daxm_status daxm_set_cutoff(daxm_plan *p, int enable, double cutoff);

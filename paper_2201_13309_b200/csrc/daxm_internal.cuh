@@ -124,6 +124,9 @@ struct DepositArgs {
     const long long* toff;    //   [k - k_lo][TILE_E][TILE_R] fp32 bins relative to m_ref
     int use_cutoff;           // 1: only pixels with I_0 >= cutoff are reconstructed (reading R14)
     float cutoff;
+    const unsigned char* tile_live;  // [n_tr][n_tc] cutoff on: 0 = no pixel of the tile passes (CTAs exit;
+                                     //   zero_dead_tiles writes its planes), else nullptr
+    const unsigned char* grp_live;   // [n_tr][n_tc][NG16] the same per 16-row group (one locked warp)
     int lock_enabled;         // step-locked kernel handles tiles with tiles[].lock != 0
     int lock_small, lock_large, lock_rest;  // tile counts: lock classes, fast tiles left to deposit_fast
     int lock_ov_small, lock_ov_large;       // ... overlapping tiles in deposit_lock_ov
@@ -137,6 +140,7 @@ struct DepositArgs {
 // start); the edges of the zone the step closes are evaluated in a warp-uniform loop.  Output planes go through a per-warp
 // ring of LOCK_RB planes indexed by bin edge.
 constexpr int LOCK_ROWS = 16;       // detector rows per warp
+constexpr int NG16 = TILE_R / LOCK_ROWS;  // 16-row groups per tile (cutoff liveness flags)
 constexpr int LOCK_WARPS = 4;       // warps per CTA (independent pipelines)
 constexpr int LOCK_SUBS = TILE_R / (LOCK_ROWS * LOCK_WARPS);  // CTAs per deposit tile
 constexpr int LOCK_NB = 16;         // input ring slots (wire steps) per warp
@@ -163,6 +167,8 @@ __device__ __forceinline__ float lock_poly(float c0, float c1, float c2, float t
 // Launchers (deposit.cu, profile.cu, select.cu).
 cudaError_t select_cutoff(const void* plane0, int dtype, size_t n, unsigned long long k,
                           unsigned long long* d_hist, cudaStream_t st, double* cutoff);
+cudaError_t launch_cutoff_tiles(const DepositArgs& a, const void* plane0, int dtype, float* out, unsigned char* live,
+                                int phase, cudaStream_t st);  // phase 0: tile flags; 1: zero fill of dead tiles
 cudaError_t launch_depth_profile(const float* out, int M, size_t plane, double* profile, cudaStream_t st);
 size_t fast_smem_bytes(int dtype, int max_nv);
 cudaError_t launch_deposit(const DepositArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,

@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(FAST_THREADS, DAXM_MINB)
     // the general kernel owns this tile (same predicate as the plan's tile lists)
     if (!(ti.separated == MODE && row0 >= a.row_begin && ti.ring_need <= NB)) return;
     if (a.lock_enabled && ti.lock) return;  // the step-locked kernel owns this tile
+    if (a.tile_live && !a.tile_live[tile]) return;  // cutoff: zero_dead_tiles writes this tile
     const int col0 = tc * TILE_C;
     const int row0_local = row0 - a.row_begin;
     const int nv_all = ti.k_hi >= ti.k_lo ? ti.k_hi - ti.k_lo + 1 : 0;
@@ -636,6 +637,7 @@ __global__ void __launch_bounds__(256) deposit_general(DepositArgs a, const T* _
     const TileInfo ti = a.tiles[tile];
     const int tr = tile / a.n_tc, tc = tile % a.n_tc;
     if (tr < a.tr_begin || tr >= a.tr_end) return;  // row-band launch: not this band
+    if (a.tile_live && !a.tile_live[tile]) return;  // cutoff: zero_dead_tiles writes this tile
     const int rows = a.row_end - a.row_begin;
     const size_t plane = (size_t)rows * a.C;
     for (int pix = threadIdx.x; pix < TILE_R * TILE_C; pix += blockDim.x) {

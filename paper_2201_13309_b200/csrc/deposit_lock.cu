@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
     const int sub = (int)blockIdx.x % LOCK_SUBS;
     const TileInfo ti = a.tiles[tile];
     if ((ti.lock & LOCK_CLASS_MASK) != RB) return;
+    if (a.tile_live && !a.tile_live[tile]) return;  // cutoff: zero_dead_tiles writes this tile
     const int tr = tile / a.n_tc, tc = tile % a.n_tc;
     const int row0 = (a.tr0 + tr) * TILE_R;  // global row of tile row 0 (>= row_begin: pre-pass)
     const int col0 = tc * TILE_C;
@@ -453,7 +454,8 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
         if (viol && a.lock_err) atomicAdd(a.lock_err, 1u);
 #endif
     }
-    drain(M);
+    // a group without a pixel above the cutoff is written by zero_dead_tiles (its walks stored nothing)
+    if (!(a.grp_live && !a.grp_live[(size_t)tile * NG16 + wrow / LOCK_ROWS])) drain(M);
     // every issued input load has been waited for (wait_upto reached vend), so the CTA may exit
 }
 
@@ -469,6 +471,7 @@ __global__ void __launch_bounds__(LK_THREADS, 2)
     const int sub = (int)blockIdx.x % LOCK_SUBS;
     const TileInfo ti = a.tiles[tile];
     if ((ti.lock & LOCK_CLASS_MASK) != (RB | LOCK_OVB)) return;
+    if (a.tile_live && !a.tile_live[tile]) return;  // cutoff: zero_dead_tiles writes this tile
     const int tr = tile / a.n_tc, tc = tile % a.n_tc;
     const int row0 = (a.tr0 + tr) * TILE_R;  // global row of tile row 0 (>= row_begin: pre-pass)
     const int col0 = tc * TILE_C;
@@ -784,7 +787,8 @@ __global__ void __launch_bounds__(LK_THREADS, 2)
         if (viol && a.lock_err) atomicAdd(a.lock_err, 1u);
 #endif
     }
-    drain(M);
+    // a group without a pixel above the cutoff is written by zero_dead_tiles (its walks stored nothing)
+    if (!(a.grp_live && !a.grp_live[(size_t)tile * NG16 + wrow / LOCK_ROWS])) drain(M);
     // every issued input load has been waited for (wait_upto reached vend), so the CTA may exit
 }
 

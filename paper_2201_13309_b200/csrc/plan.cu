@@ -79,6 +79,7 @@ struct daxm_plan {
     int use_cutoff = 0;  // intensity cutoff (f1, reading R14)
     float cutoff = 0.f;
     unsigned long long* d_hist = nullptr;  // cutoff selection scratch (256 counters)
+    unsigned char* d_live = nullptr;       // [n_tr][n_tc] cutoff: tile has a pixel above it
     daxm_plan_stats stats{};
     std::string err;
 };
@@ -526,6 +527,7 @@ void free_plan_memory(daxm_plan* p) {
     cudaFree(p->d_stack_buf);
     cudaFree(p->d_out_buf);
     cudaFree(p->d_hist);
+    cudaFree(p->d_live);
     cudaFree(p->d_table);
     cudaFree(p->d_toff);
     cudaFree(p->d_lock_err);
@@ -788,6 +790,7 @@ daxm_status device_prepass(daxm_plan* p) {
     // tile if its per-warp output ring provably holds them (deposit_lock.cu)
     CK(cudaMalloc(&p->d_lock_err, 32));
     CK(cudaMemset(p->d_lock_err, 0, 32));
+    CK(cudaMalloc(&p->d_live, n_tiles * (1 + NG16)));  // tile flags, then 16-row group flags
     if (!use_table) {
         int* d_ls = reinterpret_cast<int*>(p->d_lock_err) + 1;
         DepositArgs a = make_args(p, DAXM_U16);
@@ -963,6 +966,8 @@ static DepositArgs make_args(const daxm_plan* p, int dtype) {
     a.toff = p->d_toff;
     a.use_cutoff = p->use_cutoff;
     a.cutoff = p->cutoff;
+    a.tile_live = nullptr;
+    a.grp_live = nullptr;
     a.lock_enabled = (p->lock_small + p->lock_large + p->lock_ov_small + p->lock_ov_large) > 0 &&
                      getenv("DAXM_NO_LOCK") == nullptr;
     a.lock_small = p->lock_small;
@@ -1055,14 +1060,25 @@ static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float*
     a.tr_begin = tr_begin;
     a.tr_end = tr_end < 0 ? p->n_tr : tr_end;
     a.stack = d_stack;
+    cudaError_t e = cudaSuccess;
+    const bool live = a.use_cutoff && getenv("DAXM_NO_TILE_LIVE") == nullptr;
+    if (live) {  // dead tiles: flags here; their zero fill after the fork, beside the class launches
+        e = launch_cutoff_tiles(a, d_stack, dt, d_out, p->d_live, 0, st);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(p, DAXM_ERR_CUDA, "cutoff tile launch: %s", cudaGetErrorString(e));
+        }
+        a.tile_live = p->d_live;
+        if (getenv("DAXM_NO_GRP_LIVE") == nullptr) a.grp_live = p->d_live + (size_t)p->n_tr * p->n_tc;
+    }
     // fork: class launches on {st, st_cls[0], st_cls[1]}, joined back into st (graph-capturable)
     const bool fork = fast && a.lock_enabled && p->st_cls[0] != nullptr && getenv("DAXM_NO_FORK") == nullptr;
     cudaStream_t sts[3] = {st, p->st_cls[0], p->st_cls[1]};
-    cudaError_t e = cudaSuccess;
     if (fork) {
         e = cudaEventRecord(p->ev_cls[0], st);
         for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(p->st_cls[i], p->ev_cls[0], 0);
     }
+    if (live && e == cudaSuccess) e = launch_cutoff_tiles(a, d_stack, dt, d_out, p->d_live, 1, st);
     if (e == cudaSuccess)
         e = launch_deposit(a, &p->in_map, &p->out_map, d_stack, dt, d_out, fast, st, &p->lock_in_map, sts,
                            fork ? 3 : 1);

@@ -400,6 +400,39 @@ def test_cutoff_skips_inactive_tiles(daxm):
     assert int(torch.count_nonzero(part[:, torch.from_numpy(~act).cuda()])) == 0
 
 
+@pytest.mark.parametrize("rows,host_path", [(None, False), ((100, 1000), False), ((100, 1000), True)])
+def test_cutoff_dead_tiles_written(daxm, rows, host_path):
+    """Tiles with no pixel above the cutoff are skipped by every deposit kernel and their planes
+    are written as zeros by the row-wise zero fill: an output buffer pre-filled with NaN must come
+    back exactly zero there (band starting inside a tile, device and host paths), and live tiles
+    bit for bit as the unrestricted run."""
+    import torch
+    g = synth.geometry("C3")
+    host = synth.stack_numpy(synth.make_maps("C3"), "u16", noise=True)
+    host[0] = 100
+    host[0, 130:140, 17:19] = 5000    # live tiles in the first (partial) tile row of the band
+    host[0, 600:900:37, 400:1000:53] = 5000  # scattered live pixels
+    band = np.ascontiguousarray(host[:, rows[0]:rows[1]] if rows else host)
+    with daxm.create(g, device=0, rows=rows) as plan:
+        dev = torch.from_numpy(band).cuda()
+        full = plan.reconstruct(dev).cpu()
+        plan.set_cutoff(5000)
+        if host_path:
+            out = torch.full(plan.output_shape(), float("nan"), dtype=torch.float32).pin_memory()
+            plan.reconstruct_host(torch.from_numpy(band).pin_memory(), out=out)
+            part = out
+        else:
+            out = torch.full(plan.output_shape(), float("nan"), dtype=torch.float32, device="cuda")
+            plan.reconstruct(dev, out=out)
+            part = out.cpu()
+        torch.cuda.synchronize()
+    act = torch.from_numpy(band[0] == 5000)
+    assert int(act.sum()) > 0
+    assert torch.equal(part[:, act], full[:, act])
+    assert not torch.isnan(part).any()
+    assert int(torch.count_nonzero(part[:, ~act])) == 0
+
+
 @pytest.mark.parametrize("name,dtype,edge", [("C1", "f32", "leading"), ("C2", "u16", "leading"),
                                              ("C2", "f32", "trailing")])
 def test_general_wire_path(daxm, name, dtype, edge):
