@@ -193,6 +193,8 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
 #pragma unroll
     for (int s = 0; s < RB; ++s) sts_zero4(s_copy + s * LK_PLANE);
     __syncthreads();
+    // a group without a pixel above the cutoff is written by zero_dead_tiles: its warp is done
+    if (a.grp_live && !a.grp_live[tile * NG16 + wrow / LOCK_ROWS]) return;
 
     // ---- walks: rows wrow + 4w + rg, column col
     const int i = col0 + col;
@@ -454,8 +456,7 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
         if (viol && a.lock_err) atomicAdd(a.lock_err, 1u);
 #endif
     }
-    // a group without a pixel above the cutoff is written by zero_dead_tiles (its walks stored nothing)
-    if (!(a.grp_live && !a.grp_live[(size_t)tile * NG16 + wrow / LOCK_ROWS])) drain(M);
+    drain(M);
     // every issued input load has been waited for (wait_upto reached vend), so the CTA may exit
 }
 
@@ -501,6 +502,8 @@ __global__ void __launch_bounds__(LK_THREADS, 2)
 #pragma unroll
     for (int s = 0; s < RB; ++s) sts_zero4(s_copy + s * LK_PLANE);
     __syncthreads();
+    // a group without a pixel above the cutoff is written by zero_dead_tiles: its warp is done
+    if (a.grp_live && !a.grp_live[tile * NG16 + wrow / LOCK_ROWS]) return;
 
     // ---- walks: rows wrow + 4w + rg, column col
     const int i = col0 + col;
@@ -787,8 +790,7 @@ __global__ void __launch_bounds__(LK_THREADS, 2)
         if (viol && a.lock_err) atomicAdd(a.lock_err, 1u);
 #endif
     }
-    // a group without a pixel above the cutoff is written by zero_dead_tiles (its walks stored nothing)
-    if (!(a.grp_live && !a.grp_live[(size_t)tile * NG16 + wrow / LOCK_ROWS])) drain(M);
+    drain(M);
     // every issued input load has been waited for (wait_upto reached vend), so the CTA may exit
 }
 
