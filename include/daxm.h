@@ -44,7 +44,7 @@ typedef enum {
     DAXM_OK = 0,
     DAXM_ERR_INVALID_ARGUMENT = 1, /* bad sizes/enums/NaN/null pointers (see daxm_create)          */
     DAXM_ERR_NONMONOTONE_SCAN = 2, /* wire travel or a pixel's depth-vs-step not monotone           */
-    DAXM_ERR_GEOMETRY = 3,         /* NaN tangent depth inside a pixel's contributing window        */
+    DAXM_ERR_GEOMETRY = 3,         /* every pixel invalid (NaN tangent depth at every wire step)    */
     DAXM_ERR_OUT_OF_MEMORY = 4,
     DAXM_ERR_CUDA = 5              /* any CUDA runtime error; detail in daxm_last_error()            */
 } daxm_status;
@@ -108,6 +108,12 @@ typedef struct {
     int64_t lock_ring_violations; /* step-locked ring-capacity violations so far (read synchronously;    */
                                /* always 0: the pre-pass admits only tiles whose ring provably suffices) */
     int64_t lock_tiles_overlap; /* overlapping-span tiles the step-locked ramp-superposition kernel handles */
+    int64_t row_tiles_small;   /* row tiles (2 rows x 64 columns) the row-segment kernel handles with a   */
+    int64_t row_tiles_large;   /* 16- / 32-plane output ring; the rest run the general kernel             */
+    int64_t row_tiles_general;
+    int64_t row_ring_need_max; /* largest output-ring need (planes) the admission replay found          */
+    int64_t row_reject_bits;   /* OR of the reasons row tiles were not admitted (RW_WHY_* bits,         */
+    int64_t row_reject[8];     /* DESIGN.md §5.3) and the number of row tiles per reason bit            */
 } daxm_plan_stats;
 
 /* daxm_create -- validate `g`, run the fp64 geometry pre-pass on `cuda_device`,
@@ -120,7 +126,10 @@ typedef struct {
  *   NONMONOTONE_SCAN: first and last positions coincide (perpendicular to a-hat),
  *     the travel of a straight scan decreases, or a pixel edge's depth is not
  *     monotone in the step index inside its window.
- *   GEOMETRY: NaN tangent depth inside a pixel's contributing window.
+ *   GEOMETRY: every pixel invalid: each pixel edge lies inside the wire cylinder, or its tangent
+ *     plane is parallel to the beam, at every wire step.  Per-pixel degeneracies are not errors:
+ *     a step pair with a NaN corner depth is skipped, as in the oracle (reading R8; such plans run
+ *     the exact-depth-table general kernel).
  * Depth source: for a straight scan (centres within 1e-6 um + 1e-9 relative of
  * the line through the first and last) a quadratic per edge point in wire
  * travel, kept if its fp64 error is <= 2e-5 bins and its fp32 error <= 1e-3 bins;

@@ -54,6 +54,8 @@ class PlanStats(C.Structure):
         ("depth_table_bytes", C.c_int64),
         ("lock_tiles_small", C.c_int64), ("lock_tiles_large", C.c_int64), ("lock_ring_violations", C.c_int64),
         ("lock_tiles_overlap", C.c_int64),
+        ("row_tiles_small", C.c_int64), ("row_tiles_large", C.c_int64), ("row_tiles_general", C.c_int64),
+        ("row_ring_need_max", C.c_int64), ("row_reject_bits", C.c_int64), ("row_reject", C.c_int64 * 8),
     ]
 
 
@@ -134,7 +136,8 @@ class Plan:
     def stats(self) -> dict:
         s = PlanStats()
         self._check(lib().daxm_plan_stats_get(self._h, C.byref(s)))
-        return {f: getattr(s, f) for f, _ in PlanStats._fields_}
+        return {f: (list(getattr(s, f)) if isinstance(getattr(s, f), C.Array) else getattr(s, f))
+                for f, _ in PlanStats._fields_}
 
     def output_shape(self):
         return (self.n_bins, self.rows, self.cols)

@@ -158,6 +158,83 @@ constexpr int LOCK_RB_LARGE = 32;
 constexpr int lock_need_max(int rb) { return rb; }
 static_assert(LOCK_NB % LOCK_G == 0 && (LOCK_NB / LOCK_G & (LOCK_NB / LOCK_G - 1)) == 0, "lock input ring shape");
 
+// ---- Row-segment deposit kernel (deposit_row.cu), the production path.
+// One warp = one "row tile" of RW_ROWS detector rows x RW_COLS columns, aligned to global rows
+// and columns; lane l owns columns col0 + l + 32 h (h < RW_COLS / 32) of all RW_ROWS rows: four
+// pixel walks, packed in two pairs (two rows of one column).  Output planes leave as TMA stores of
+// [RW_PB planes][RW_ROWS][RW_COLS] boxes (256-byte rows), the stack arrives as TMA loads of
+// [RW_G steps][RW_ROWS][RW_COLS] boxes (128-byte rows for u16): the store geometry that reaches
+// the copy ceiling (profiles/r02b_membench.md), where the round-1 16 x 8 warp block could not.
+#ifndef DAXM_RW_ROWS
+#define DAXM_RW_ROWS 2
+#endif
+#ifndef DAXM_RW_NB
+#define DAXM_RW_NB 32
+#endif
+#ifndef DAXM_RW_KT
+#define DAXM_RW_KT 5
+#endif
+constexpr int RW_ROWS = DAXM_RW_ROWS;  // 2 (tile 2 x 64) or 4 (tile 4 x 32)
+constexpr int RW_COLS = 128 / RW_ROWS;
+constexpr int RW_H = RW_COLS / 32;  // column halves per lane: pair p = half p (RW_H = 2) or rows 2p, 2p+1
+constexpr int RW_NB = DAXM_RW_NB;   // input ring slots (wire steps) per warp
+constexpr int RW_G = 4;             // wire steps per TMA load box
+#ifndef DAXM_RW_PB
+#define DAXM_RW_PB 4
+#endif
+constexpr int RW_PB = DAXM_RW_PB;   // output planes per TMA store box
+constexpr int RW_EXT = 16;          // steps a row tile's range extends below its windows (lock-step starts)
+constexpr int RW_KT = DAXM_RW_KT;   // max bin edges one walk evaluates per iteration (unrolled trips)
+constexpr int RW_RB_SMALL = 16, RW_RB_LARGE = 32;  // output ring planes (+ RW_KT - 1 overflow planes)
+constexpr int RW_CLS_RB = 0xff;         // RowTile.cls: ring planes (0: not admitted -> general kernel)
+constexpr int RW_CLS_FRONT_LO = 0x100;  //   the front pixel edge is the shallower one over the tile
+static_assert(RW_ROWS * RW_COLS == 128 && RW_COLS % 32 == 0 && (RW_ROWS == 2 || RW_ROWS == 4),
+              "row tile: 4 walks per lane, two per pair");
+// pair p of a lane: column half and first row
+__host__ __device__ constexpr int rw_half(int p) { return RW_H == 2 ? p : 0; }
+__host__ __device__ constexpr int rw_row(int p) { return RW_H == 2 ? 0 : 2 * p; }
+static_assert(RW_KT - 1 <= RW_RB_SMALL && RW_RB_SMALL % RW_PB == 0 && RW_NB % RW_G == 0, "row ring shapes");
+
+struct RowTile {
+    double t_ref;  // wire-travel reference the tile's depth polynomials are expanded about
+    int k_lo, k_hi;  // union of the tile's pixel windows (points); k_hi < k_lo: empty
+    int dir;         // +1: depth increases with the step index
+    int sep;         // MODE_SEPARATED / MODE_OVERLAP / MODE_GENERAL over the tile's band pixels
+    int cls;         // admission class (RW_CLS_*), 0 = general kernel
+    int niter;       // iterations of the admitted schedule (pre-pass replay)
+    int why;         // not admitted: RW_WHY_* bits
+};
+enum : unsigned {
+    RW_WHY_MODE = 1u,      // not every pixel in the separated-span regime
+    RW_WHY_KT = 2u,        // a zone holds more than RW_KT bin edges
+    RW_WHY_INPUT = 4u,     // the pairs' visits spread wider than the input ring
+    RW_WHY_DENSITY = 8u,   // equal consecutive edge sums or a vanishing edge span (fp32)
+    RW_WHY_TOP = 16u,      // a window's last point below the top bin edge
+    RW_WHY_RING = 32u,     // output-ring need above RW_RB_LARGE
+    RW_WHY_ORDER = 64u,    // neither pixel edge is the shallower one throughout
+    RW_WHY_ITER = 128u,
+};
+
+struct RowArgs {
+    const double* t;       // [S] wire travel
+    const RowTile* rt;     // [n_rt]
+    const int2* win;       // [pre_rows][C] pixel windows (global pixel indexing, rows from pre_row0)
+    const float* coef;     // [n_rt][NCOEF][RW_COLS + 1][RW_ROWS] depth polynomials (bins rel. m_ref)
+    const int* list;       // row tiles of this launch (one class), ascending
+    int n_list;
+    int R, C, S, M, m_ref;
+    int row_begin, row_end, pre_row0;
+    int row_org;           // global row of row-tile row 0 (= row_begin: row tiles start at the band)
+    int n_rc;              // row-tile columns
+    int max_nv;            // largest tile step range (tau table size)
+    int point_mode;
+    float sign;            // s: +1 leading, -1 trailing (reading R2)
+    const void* stack;     // band stack (plane 0 read for the intensity cutoff)
+    int use_cutoff;
+    float cutoff;
+    unsigned* err;         // DAXM_ROW_CHECK builds: schedule violations (must stay 0)
+};
+
 // Corner depth of one pixel edge at fp32 wire travel tau (bins relative to m_ref): the
 // pre-pass ring check and the step-locked kernel evaluate exactly this expression.
 __device__ __forceinline__ float lock_poly(float c0, float c1, float c2, float t) {
@@ -178,5 +255,13 @@ size_t lock_smem_bytes(int dtype, int rb, int max_nv);
 cudaError_t launch_lock(const DepositArgs& a, const CUtensorMap* in_map, float* out, int dtype, int n_tiles,
                         const cudaStream_t* sts, int nst);
 cudaError_t launch_lock_prepass(const DepositArgs& a, int n_tiles, int* d_stats, cudaStream_t st);
+// row-segment kernel (deposit_row.cu): pre-pass replay (admission) and the class launches
+cudaError_t launch_row_admit(const RowArgs& a, RowTile* rt, int n_rt, int* d_stats, cudaStream_t st);
+size_t row_smem_bytes(int dtype, int rb, int max_nv);
+cudaError_t row_set_attributes(int max_nv);  // per device: dynamic shared memory of every instance
+cudaError_t launch_row(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int dtype, int rb,
+                       cudaStream_t st);
+cudaError_t launch_general_rows(const DepositArgs& a, const int* rt_list, int n, int n_rc, int row_org,
+                                const void* stack, int dtype, float* out, cudaStream_t st);
 
 }  // namespace daxm

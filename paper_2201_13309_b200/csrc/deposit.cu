@@ -630,89 +630,115 @@ __device__ __forceinline__ float trapezoid_fraction(float lo0, float hi0, float 
     return H / A;
 }
 
+// One pixel (global row j, column i; position r, c in deposit tile `tile`), any geometry: bin edge
+// by bin edge, F(E) = (dI of the pairs whose trapezoid lies below E) + sum over the open pairs of
+// dI_q H_q(E) / A_q.  A pair with a NaN corner depth (the pixel edge inside the wire cylinder, or
+// a tangent plane parallel to the beam) is skipped, as in the oracle (reading R8).
+template <typename T>
+__device__ void general_pixel(const DepositArgs& a, int tile, int r, int c, int j, int i, const T* __restrict__ stack,
+                              float* __restrict__ out) {
+    const TileInfo ti = a.tiles[tile];
+    const int rows = a.row_end - a.row_begin;
+    const size_t plane = (size_t)rows * a.C;
+    const int jl = j - a.row_begin;
+    const int2 w = a.win[(size_t)(j - a.pre_row0) * a.C + i];
+    float cb[NCOEF], cf[NCOEF];
+    const int eb = c, ef = a.point_mode ? c : c + 1;
+#pragma unroll
+    for (int m = 0; m < NCOEF; ++m) {
+        cb[m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + eb) * TILE_R + r];
+        cf[m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + ef) * TILE_R + r];
+    }
+    const bool act = !a.use_cutoff || (float)stack[(size_t)jl * a.C + i] >= a.cutoff;  // reading R14
+    const int kb = w.x, ke = act ? w.y : w.x, n = ke - kb, dir = ti.dir;
+    auto step_of = [&](int q) { return dir > 0 ? kb + q : ke - q; };
+    // corner depths of point q (lo <= hi), false if either is NaN
+    auto point = [&](int q, float& lo, float& hi) {
+        float x0, x1;
+        if (a.table) {  // exact per-step depths (general wire paths)
+            const float* tb = a.table + a.toff[tile] + (size_t)(step_of(q) - ti.k_lo) * (TILE_E * TILE_R) + r;
+            x0 = tb[eb * TILE_R];
+            x1 = tb[ef * TILE_R];
+        } else {
+            const float tau = (float)(a.t[step_of(q)] - ti.t_ref);
+            x0 = poly3(cb, tau);
+            x1 = poly3(cf, tau);
+        }
+        lo = fminf(x0, x1);
+        hi = fmaxf(x0, x1);
+        return !(isnan(x0) || isnan(x1));
+    };
+    const T* px = stack + (size_t)jl * a.C + i;
+    const float sgn = a.sign * (float)dir;
+    auto dI = [&](int q) -> float {
+        return sgn * ((float)px[(size_t)step_of(q) * plane] - (float)px[(size_t)step_of(q + 1) * plane]);
+    };
+    int qc = 0, qo = 0;
+    float P = 0.f, F_prev = 0.f;
+    float* o = out + (size_t)jl * a.C + i;
+    for (int e = 0; e <= a.M; ++e) {
+        const float E = (float)(e - a.m_ref);
+        while (qc < n) {  // close pairs whose trapezoid lies entirely below E (NaN pairs: at once, empty)
+            float lo1, hi1, lo2, hi2;
+            const bool ok = point(qc, lo1, hi1) & point(qc + 1, lo2, hi2);
+            if (!ok) {
+                ++qc;
+            } else if (fmaxf(hi1, hi2) < E) {
+                P += dI(qc);
+                ++qc;
+            } else {
+                break;
+            }
+        }
+        if (qo < qc) qo = qc;
+        while (qo < n) {  // open pairs whose trapezoid starts below E
+            float lo1, hi1, lo2, hi2;
+            const bool ok = point(qo, lo1, hi1) & point(qo + 1, lo2, hi2);
+            if (!ok || fminf(lo1, lo2) < E)
+                ++qo;
+            else
+                break;
+        }
+        float F = P;
+        for (int q = qc; q < qo; ++q) {
+            float lo1, hi1, lo2, hi2;
+            if (!(point(q, lo1, hi1) & point(q + 1, lo2, hi2))) continue;
+            const float d = dI(q);
+            if (d != 0.f) F += d * trapezoid_fraction(lo1, hi1, lo2, hi2, E);
+        }
+        if (e > 0) o[(size_t)(e - 1) * plane] = F - F_prev;
+        F_prev = F;
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) deposit_general(DepositArgs a, const T* __restrict__ stack,
                                                        float* __restrict__ out) {
     const int tile = a.tile_list ? a.tile_list[blockIdx.x] : a.tr_begin * a.n_tc + (int)blockIdx.x;
-    const TileInfo ti = a.tiles[tile];
     const int tr = tile / a.n_tc, tc = tile % a.n_tc;
     if (tr < a.tr_begin || tr >= a.tr_end) return;  // row-band launch: not this band
     if (a.tile_live && !a.tile_live[tile]) return;  // cutoff: zero_dead_tiles writes this tile
-    const int rows = a.row_end - a.row_begin;
-    const size_t plane = (size_t)rows * a.C;
     for (int pix = threadIdx.x; pix < TILE_R * TILE_C; pix += blockDim.x) {
         const int r = pix / TILE_C, c = pix % TILE_C;
         const int j = (a.tr0 + tr) * TILE_R + r, i = tc * TILE_C + c;
         if (j < a.row_begin || j >= a.row_end || i >= a.C) continue;
-        const int jl = j - a.row_begin;
-        const int2 w = a.win[(size_t)(j - a.pre_row0) * a.C + i];
-        float cb[NCOEF], cf[NCOEF];
-        const int eb = c, ef = a.point_mode ? c : c + 1;
-#pragma unroll
-        for (int m = 0; m < NCOEF; ++m) {
-            cb[m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + eb) * TILE_R + r];
-            cf[m] = a.coef[(((size_t)tile * NCOEF + m) * TILE_E + ef) * TILE_R + r];
-        }
-        const bool act = !a.use_cutoff || (float)stack[(size_t)jl * a.C + i] >= a.cutoff;  // reading R14
-        const int kb = w.x, ke = act ? w.y : w.x, n = ke - kb, dir = ti.dir;
-        auto step_of = [&](int q) { return dir > 0 ? kb + q : ke - q; };
-        auto point = [&](int q, float& lo, float& hi) {
-            float x0, x1;
-            if (a.table) {  // exact per-step depths (general wire paths)
-                const float* tb = a.table + a.toff[tile] + (size_t)(step_of(q) - ti.k_lo) * (TILE_E * TILE_R) + r;
-                x0 = tb[eb * TILE_R];
-                x1 = tb[ef * TILE_R];
-            } else {
-                const float tau = (float)(a.t[step_of(q)] - ti.t_ref);
-                x0 = poly3(cb, tau);
-                x1 = poly3(cf, tau);
-            }
-            lo = fminf(x0, x1);
-            hi = fmaxf(x0, x1);
-        };
-        const T* px = stack + (size_t)jl * a.C + i;
-        const float sgn = a.sign * (float)dir;
-        auto dI = [&](int q) -> float {
-            return sgn * ((float)px[(size_t)step_of(q) * plane] - (float)px[(size_t)step_of(q + 1) * plane]);
-        };
-        int qc = 0, qo = 0;
-        float P = 0.f, F_prev = 0.f;
-        float* o = out + (size_t)jl * a.C + i;
-        for (int e = 0; e <= a.M; ++e) {
-            const float E = (float)(e - a.m_ref);
-            while (qc < n) {  // close pairs whose trapezoid lies entirely below E
-                float lo1, hi1, lo2, hi2;
-                point(qc, lo1, hi1);
-                point(qc + 1, lo2, hi2);
-                if (fmaxf(hi1, hi2) < E) {
-                    P += dI(qc);
-                    ++qc;
-                } else {
-                    break;
-                }
-            }
-            if (qo < qc) qo = qc;
-            while (qo < n) {  // open pairs whose trapezoid starts below E
-                float lo1, hi1, lo2, hi2;
-                point(qo, lo1, hi1);
-                point(qo + 1, lo2, hi2);
-                if (fminf(lo1, lo2) < E)
-                    ++qo;
-                else
-                    break;
-            }
-            float F = P;
-            for (int q = qc; q < qo; ++q) {
-                float lo1, hi1, lo2, hi2;
-                point(q, lo1, hi1);
-                point(q + 1, lo2, hi2);
-                const float d = dI(q);
-                if (d != 0.f) F += d * trapezoid_fraction(lo1, hi1, lo2, hi2, E);
-            }
-            if (e > 0) o[(size_t)(e - 1) * plane] = F - F_prev;
-            F_prev = F;
-        }
+        general_pixel<T>(a, tile, r, c, j, i, stack, out);
     }
+}
+
+// The general kernel over row tiles the row-segment kernel did not admit (one CTA per row tile,
+// one thread per pixel); each pixel's depth polynomials come from its deposit tile.
+template <typename T>
+__global__ void __launch_bounds__(RW_ROWS * RW_COLS) deposit_general_rows(DepositArgs a, const int* __restrict__ list,
+                                                                          int n_rc, int row_org,
+                                                                          const T* __restrict__ stack,
+                                                                          float* __restrict__ out) {
+    const int rt = list[blockIdx.x];
+    const int rr = rt / n_rc, rc = rt % n_rc;
+    const int j = row_org + rr * RW_ROWS + (int)threadIdx.x / RW_COLS, i = rc * RW_COLS + (int)threadIdx.x % RW_COLS;
+    if (j < a.row_begin || j >= a.row_end || i >= a.C) return;
+    const int tile = (j / TILE_R - a.tr0) * a.n_tc + i / TILE_C;
+    general_pixel<T>(a, tile, j % TILE_R, i % TILE_C, j, i, stack, out);
 }
 
 template <typename T, int NB, bool POINT, int MODE>
@@ -777,6 +803,18 @@ cudaError_t launch_deposit(const DepositArgs& a, const CUtensorMap* in_map, cons
         deposit_general<uint16_t><<<ga.n_list, 256, 0, st>>>(ga, static_cast<const uint16_t*>(stack), out);
     else
         deposit_general<float><<<ga.n_list, 256, 0, st>>>(ga, static_cast<const float*>(stack), out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_general_rows(const DepositArgs& a, const int* rt_list, int n, int n_rc, int row_org,
+                                const void* stack, int dtype, float* out, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    if (dtype == DAXM_U16)
+        deposit_general_rows<uint16_t><<<n, RW_ROWS * RW_COLS, 0, st>>>(a, rt_list, n_rc, row_org,
+                                                                        static_cast<const uint16_t*>(stack), out);
+    else
+        deposit_general_rows<float><<<n, RW_ROWS * RW_COLS, 0, st>>>(a, rt_list, n_rc, row_org,
+                                                                     static_cast<const float*>(stack), out);
     return cudaGetLastError();
 }
 

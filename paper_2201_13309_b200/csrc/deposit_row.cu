@@ -1,0 +1,779 @@
+// deposit_row.cu -- the production gather deposit for pixels in
+// the separated-span regime, and the pre-pass replay that admits a row tile to it.
+//
+// What is computed: per pixel, with the step pairs visited in the order their
+// trapezoids move deeper and c_q = dI_q / A_q, the intensity deposited below bin edge E is,
+// inside zone q = [lo_q, lo_{q+1}),
+//     F(E) = F(lo_q) + c_q x + xc (d_q + g_q xc),  x = E - lo_q, xc = min(x, w_q),
+//     d_q = c_{q-1} - c_q,  g_q = -d_q / (2 w_q),  w_q = hi_q - lo_q,
+// and bin m = [E_m, E_{m+1}) receives F(E_{m+1}) - F(E_m): the trapezoid overlaps of P:L320-331
+// (device_depth_resolve_pixel / device_get_trapezoid_height) summed over the pairs
+// (P:L332-334), one owner per (bin, pixel), no atomics.  dI_q = s (I_q - I_{q+1})
+// (readings R1, R2) is formed from the streamed planes.
+//
+// Schedule.  One warp = one row tile: RW_ROWS detector rows x RW_COLS columns.  Lane l owns
+// columns col0 + l + 32 p (p = 0, 1) of both rows: two walk pairs (rows 0 / 1 of one column,
+// packed fp32x2).  A pair advances one wire step (point) per iteration: it closes the zone its new
+// point ends and evaluates that zone's bin edges in a warp-uniform, fully unrolled predicated loop
+// (at most RW_KT edges).  Different columns sit at different depths for the same step
+// (0.68 bins per column at C4), so each pair starts at its own window and keeps its own visit
+// index; a pair whose walks are more than RW_LEAD bins ahead of the slowest walk of the warp waits
+// (its state is untouched), which keeps all 128 walks of the warp within a few bins of each other.
+// Pausing never changes a walk's arithmetic, only when it happens, and the schedule depends on
+// geometry alone (inactive walks keep advancing, they just store nothing), so an active walk's
+// output is bit-identical whatever the cutoff.
+//
+//   input : TMA loads of [RW_G steps][2 rows][64 cols] (128-byte rows) into an RW_NB-slot ring, one
+//           mbarrier per group; lane 0 refills the slots every pair has read past.
+//   output: a ring of RB staged planes [2][64] fp32 (+ RW_KT - 1 overflow planes, so that the
+//           unrolled edge stores use immediate offsets); once the slowest walk has passed a batch
+//           of RW_PB planes, lane 0 writes the batch with one TMA store of a [RW_PB][2][64] box
+//           (256-byte rows: the pattern that reaches the copy ceiling, profiles/r02b_membench.md);
+//           its slots are zeroed at the next drain, after the store has read them.
+// The pre-pass (row_admit_kernel) replays every warp's schedule with the kernel's own fp32
+// arithmetic and admits a tile only if the output ring, the unrolled edge loop and the input ring
+// provably suffice; the rest goes to the general kernel.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <limits.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <type_traits>
+
+#include "daxm_internal.cuh"
+#include "fp2.cuh"
+#include "ptx.cuh"
+
+#define DAXM_PRAGMA_(x) _Pragma(#x)
+#define DAXM_PRAGMA_UNROLL(n) DAXM_PRAGMA_(unroll n)
+#ifndef DAXM_ROW_CHECK
+#define DAXM_ROW_CHECK 0  // 1: count schedule violations in the kernel (the pre-pass makes them impossible)
+#endif
+
+namespace daxm {
+namespace {
+using namespace ptx;
+
+constexpr int PLANE_B = RW_ROWS * RW_COLS * 4;  // one staged output plane (512 B)
+constexpr int NG = RW_NB / RW_G;                // input groups in the ring
+
+template <typename T, int RB>
+struct RowSmem {
+    static constexpr int OUT_SLOTS = RB + RW_KT - 1;
+    static constexpr int IN_SLOT = RW_ROWS * 32 * (int)sizeof(T);  // one step of one column half
+    static constexpr int IN_GROUP = RW_G * IN_SLOT;                // one TMA box
+    static constexpr int IN_HALF = RW_NB * IN_SLOT;                // a half's ring
+    static constexpr int OFF_OUT = 0;
+    static constexpr int OFF_IN = OFF_OUT + OUT_SLOTS * PLANE_B;
+    static constexpr int OFF_BAR = OFF_IN + RW_H * IN_HALF;
+    static constexpr int OFF_TAU = OFF_BAR + NG * 8;
+    static size_t bytes(int max_nv) { return (size_t)OFF_TAU + 4 * (size_t)(max_nv + 4) + 128; }
+};
+
+__device__ __forceinline__ void sts_zero4(uint32_t addr) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(addr), "f"(0.f) : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ uint4 lds128u(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts128u(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+constexpr uint32_t SENT = 0x7fbadbadu;  // overflow slot not written this lap (a NaN no arithmetic yields)
+__device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+// Edge store of trip k: if k < cnt, staged[addr + OFF] = o and Fp = F (one FSETP, no branch).
+template <int OFF>
+__device__ __forceinline__ void edge_st(uint32_t addr, float o, float F, float kf, float cnt, float& Fp) {
+    asm volatile(
+        "{\n .reg .pred q;\n setp.lt.f32 q, %3, %4;\n @q st.shared.f32 [%1+%6], %2;\n @q mov.f32 %0, %5;\n}\n"
+        : "+f"(Fp)
+        : "r"(addr), "f"(o), "f"(kf), "f"(cnt), "f"(F), "n"(OFF)
+        : "memory");
+}
+template <typename T, int OFF>
+__device__ __forceinline__ float lds_in(uint32_t addr) {
+    if constexpr (sizeof(T) == 2) {
+        unsigned short v;
+        asm volatile("ld.shared.u16 %0, [%1+%2];" : "=h"(v) : "r"(addr), "n"(OFF) : "memory");
+        return (float)v;
+    } else {
+        float v;
+        asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF) : "memory");
+        return v;
+    }
+}
+
+// compile-time loop: f(integral_constant<int, k>) for k = K0 .. KN - 1 while f returns true
+template <int K0, int KN, typename F>
+__device__ __forceinline__ void static_for(F&& f) {
+    if constexpr (K0 < KN) {
+        if (f(std::integral_constant<int, K0>{})) static_for<K0 + 1, KN>(f);
+    }
+}
+
+// ---- per-walk geometry shared by the kernel and its replay
+struct RowWalk {
+    int v0, npts;  // first visit (index into the tile's step list, ascending depth), points (0: none)
+};
+__device__ __forceinline__ RowWalk row_walk(const RowArgs& a, const RowTile& ti, int j, int i) {
+    RowWalk w{0, 0};
+    if (j < a.row_begin || j >= a.row_end || i >= a.C) return w;
+    const int2 win = a.win[(size_t)(j - a.pre_row0) * a.C + i];
+    if (win.y <= win.x) return w;
+    w.v0 = ti.dir > 0 ? win.x - ti.k_lo : ti.k_hi - win.y;
+    w.npts = win.y - win.x + 1;
+    return w;
+}
+// depth polynomials of a walk's two pixel edges: edge column e (back) and e + 1 (front; POINT: e)
+__device__ __forceinline__ void row_coef(const RowArgs& a, int rt, int row, int e, float c[3]) {
+#pragma unroll
+    for (int m = 0; m < 3; ++m) c[m] = a.coef[(((size_t)rt * NCOEF + m) * (RW_COLS + 1) + e) * RW_ROWS + row];
+}
+
+// ------------------------------------------------------------------ kernel
+static_assert(RW_H == 2 && RW_ROWS == 2, "deposit_row: two column halves per lane, two rows");
+
+// Loop-carried state of one lane: walk pair p = column half p (column col0 + lane + 32 p), rows
+// row0 (x) and row0 + 1 (y); the point last visited (plo, phi, ps = lo + hi, pI) and the
+// prefetched next one (tq, Iq).
+struct RowState {
+    float2 plo[2], phi[2], ps[2], pI[2], cq[2], zF[2], Fp[2], En[2], Iq[2];
+    float tq[2];
+};
+
+// warp-wide integer min / max (redux.sync, full mask; the loop is convergent by construction)
+__device__ __forceinline__ int warp_min(int x) {
+    int r;
+    asm volatile("redux.sync.min.s32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(x));
+    return r;
+}
+__device__ __forceinline__ int warp_max(int x) {
+    int r;
+    asm volatile("redux.sync.max.s32 %0, %1, 0xffffffff;" : "=r"(r) : "r"(x));
+    return r;
+}
+
+// (a << 9) + b in one instruction (LEA): the byte offset of staged plane slot a
+__device__ __forceinline__ uint32_t lea9(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("{\n .reg .u32 t;\n shl.b32 t, %1, 9;\n add.u32 %0, t, %2;\n}\n" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+// make a value opaque to the compiler, so that it stays in a register instead of being recomputed
+// from constants inside the loop
+__device__ __forceinline__ float opaque(float x) {
+    asm volatile("" : "+f"(x));
+    return x;
+}
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+    asm volatile("" : "+r"(x));
+    return x;
+}
+__device__ __forceinline__ int opaque(int x) {
+    asm volatile("" : "+r"(x));
+    return x;
+}
+
+// Lock-step starts of the warp's walk pairs (kernel and replay).  A pair covers its two walks'
+// windows [ws, we] (visits from the tile's first step).  All pairs advance one visit per iteration,
+// but their depth per visit differs slightly across the 64 columns (2.6 % at C4), so pairs that
+// started together drift apart by the end of their windows.  Aligning the windows' MIDDLES instead
+// halves the largest spread: pair q starts (T - len_q) / 2 visits before its window, T = the
+// warp's longest window (a point before a window lies below the bins: no edge), clamped at the
+// tile's first step (row_tile_kernel extends the step range by RW_EXT for that).  Visits of column
+// half p are then counted from vmin[p], the half's earliest start.
+__device__ __forceinline__ void row_starts(const RowWalk wk[2][2], int vmin[2], int vs[2], int ve[2], int vs_max[2],
+                                           int vend[2]) {
+    int ws[2], we[2], len = -1;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        ws[p] = INT_MAX;
+        we[p] = -1;
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+            if (wk[p][r].npts > 0) {
+                ws[p] = min(ws[p], wk[p][r].v0);
+                we[p] = max(we[p], wk[p][r].v0 + wk[p][r].npts - 1);
+            }
+        if (we[p] >= 0) len = max(len, we[p] - ws[p]);
+    }
+    len = __reduce_max_sync(0xffffffffu, len);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const int st = we[p] >= 0 ? max(ws[p] - ((len - (we[p] - ws[p])) >> 1), 0) : INT_MAX;
+        vmin[p] = __reduce_min_sync(0xffffffffu, st);
+        if (vmin[p] == INT_MAX) vmin[p] = 0;  // a half without windows
+        vs[p] = we[p] >= 0 ? st - vmin[p] : 0;  // no window in the column: done at once
+        ve[p] = we[p] >= 0 ? we[p] - vmin[p] : 0;
+        vs_max[p] = __reduce_max_sync(0xffffffffu, vs[p]);
+        vend[p] = __reduce_max_sync(0xffffffffu, ve[p]);
+    }
+}
+
+template <typename T, bool POINT, int RB>
+__global__ void __launch_bounds__(32) deposit_row(const __grid_constant__ CUtensorMap in_map,
+                                                  const __grid_constant__ CUtensorMap out_map, const RowArgs a) {
+    using L = RowSmem<T, RB>;
+    static_assert(RB % RW_PB == 0 && (RB & (RB - 1)) == 0, "ring");
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
+    unsigned char* smem = smem_raw + (sbase - smem_u32(smem_raw));
+    const int lane = threadIdx.x;
+    const int rt = a.list[blockIdx.x];
+    const RowTile ti = a.rt[rt];
+    const int rr = rt / a.n_rc, rc = rt % a.n_rc;
+    const int row0 = a.row_org + rr * RW_ROWS;  // global row of the tile's first row
+    const int col0 = rc * RW_COLS;
+    const int rowl = row0 - a.row_begin;           // band-local (< 0 for a band start inside the tile: TMA skips)
+    const int nvt = ti.k_hi >= ti.k_lo ? ti.k_hi - ti.k_lo + 1 : 0;
+    const int dir = ti.dir;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+    float* tau = reinterpret_cast<float*>(smem + L::OFF_TAU);
+
+    for (int q = lane; q < nvt; q += 32) tau[q] = (float)(a.t[dir > 0 ? ti.k_lo + q : ti.k_hi - q] - ti.t_ref);
+    if (lane == 0) {
+        for (int g = 0; g < NG; ++g) mbar_init(&bars[g], 1);
+        fence_mbar_init();
+    }
+#pragma unroll
+    for (int s = 0; s < RB; ++s) sts_zero4(sbase + L::OFF_OUT + s * PLANE_B + lane * 16);
+#pragma unroll
+    for (int s = RB; s < L::OUT_SLOTS; ++s)
+        sts128u(sbase + L::OFF_OUT + s * PLANE_B + lane * 16, make_uint4(SENT, SENT, SENT, SENT));
+    __syncwarp();
+
+    // ---- walks: pair p = column col0 + lane + 32 p, rows row0 (x) and row0 + 1 (y)
+    const float E0 = (float)(-a.m_ref);
+    float2 cb[2][3], cf[2][3], gate[2];
+    bool any_act = false;
+    RowWalk wk[2][2];
+    int vmin[2];  // per column half: its earliest start (row_starts)
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const int c = col0 + lane + 32 * p;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int j = row0 + r;
+            wk[p][r] = row_walk(a, ti, j, c);
+            bool on = wk[p][r].npts > 0;
+            if (on && a.use_cutoff) {  // intensity cutoff (f1, reading R14)
+                const T* s0 = static_cast<const T*>(a.stack) + (size_t)(j - a.row_begin) * a.C + c;
+                on = (float)s0[0] >= a.cutoff;
+            }
+            any_act |= on;
+            (r ? gate[p].y : gate[p].x) = on ? 0.f : 1.0e9f;  // inactive: edge counts below zero
+            float cl[3], ch[3];
+            const int e = lane + 32 * p;
+            row_coef(a, rt, r, (ti.cls & RW_CLS_FRONT_LO) && !POINT ? e + 1 : e, cl);
+            row_coef(a, rt, r, (ti.cls & RW_CLS_FRONT_LO) || POINT ? e : e + 1, ch);
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+                (r ? cb[p][m].y : cb[p][m].x) = cl[m];
+                (r ? cf[p][m].y : cf[p][m].x) = ch[m];
+            }
+        }
+    }
+    if (!__any_sync(0xffffffffu, any_act)) {  // no active walk: the tile's output is zero
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            for (int P = 0; P < a.M; P += RW_PB) tma_store_3d(&out_map, col0, rowl, P, smem + L::OFF_OUT);
+            bulk_commit();
+            bulk_wait<0>();
+        }
+        return;
+    }
+    // visits of half p are counted from its earliest start (vmin[p]); lane l's pair p starts at vs[p]
+    // and ends at ve[p]; all pairs advance in lock step
+    int vs[2], ve[2], vs_max[2], vend[2];
+    row_starts(wk, vmin, vs, ve, vs_max, vend);
+
+    // ---- input rings, one per column half: visit v of half p in slot (v ^ xr) mod RW_NB; group g =
+    // visits [RW_G g, RW_G g + RW_G) of both halves = two TMA boxes of consecutive steps on one
+    // mbarrier (ascending k: for dir < 0 a group's visits land in reverse slot order)
+    const int xr = dir > 0 ? 0 : RW_G - 1;
+    const int ngroups = max(vend[0], vend[1]) / RW_G + 1;
+    const int kb0 = dir > 0 ? ti.k_lo + vmin[0] : ti.k_hi - vmin[0] - (RW_G - 1);
+    const int kb1 = dir > 0 ? ti.k_lo + vmin[1] : ti.k_hi - vmin[1] - (RW_G - 1);
+    int g_issue = 0, g_wait = 0;
+    auto issue_upto = [&](int lim) {  // groups <= lim (clamped) may be in flight
+        lim = min(lim, ngroups - 1);
+        if (lim < g_issue) return;
+        if (lane == 0)
+            for (int g = g_issue; g <= lim; ++g) {
+                const int b = g & (NG - 1);
+                const int dk = dir > 0 ? g * RW_G : -g * RW_G;
+                mbar_arrive_expect_tx(&bars[b], 2 * L::IN_GROUP);
+                tma_load_3d(smem + L::OFF_IN + b * L::IN_GROUP, &in_map, col0, rowl, kb0 + dk, &bars[b]);
+                tma_load_3d(smem + L::OFF_IN + L::IN_HALF + b * L::IN_GROUP, &in_map, col0 + 32, rowl, kb1 + dk, &bars[b]);
+            }
+        g_issue = lim + 1;
+    };
+    const uint32_t s_bar = sbase + L::OFF_BAR;
+    auto wait_for = [&](int v) {  // every group up to visit v's has landed (v warp-uniform, >= 0)
+        const int gn = (int)((unsigned)v / RW_G);
+        if (gn < g_wait) return;
+        for (; g_wait <= gn; ++g_wait)
+            while (!mbar_try(s_bar + (uint32_t)(g_wait & (NG - 1)) * 8u, (uint32_t)(g_wait / NG) & 1u)) {
+            }
+        __syncwarp();
+    };
+    issue_upto(NG - 1);  // nothing consumed yet: visits below every pair's start are never read
+    wait_for(__reduce_max_sync(0xffffffffu, max(min(vs[0] + 1, ve[0]), min(vs[1] + 1, ve[1]))));
+
+    // loop invariants, kept in registers
+    const uint32_t s_copy = opaque(sbase + L::OFF_OUT + (uint32_t)lane * 16u);  // lane's 16 bytes of a plane
+    const float EM = opaque((float)(a.M - a.m_ref));
+    const uint32_t in_lane = opaque(sbase + L::OFF_IN + (uint32_t)lane * (uint32_t)sizeof(T));
+    const uint32_t tau0 = opaque(sbase + L::OFF_TAU + 4u * (uint32_t)vmin[0]);
+    const uint32_t tau1 = opaque(sbase + L::OFF_TAU + 4u * (uint32_t)vmin[1]);
+    const uint32_t ob = opaque(sbase + L::OFF_OUT + (uint32_t)lane * 4u);     // lane's column in a staged plane
+    const float2 sdir2 = f2(opaque(2.f * a.sign * (float)dir));  // c = 2 s dir dI / (sum_{q+1} - sum_q)
+    const int m_ref = a.m_ref;
+    // bits(E + fbias) = 0x4B000000 + e - 1 + RB for edge index e = E + m_ref: its plane's slot in the low bits
+    const float fbias = opaque(8388608.f + (float)(m_ref - 1 + RB));
+    const int xr_ = opaque(xr);
+    const int ve0 = opaque(ve[0]), ve1 = opaque(ve[1]), vs0 = opaque(vs[0]), vs1 = opaque(vs[1]);
+    const int need_hi = max(vs_max[0], vs_max[1]), need_end = max(vend[0], vend[1]);
+
+    // wire travel and the pair's two intensities at visit v of half P
+    auto fetch = [&](auto pc, int v, float& t, float2& I) {
+        constexpr int P = decltype(pc)::value;
+        t = lds_f32((P ? tau1 : tau0) + 4u * (uint32_t)v);
+        const uint32_t ad = in_lane + (uint32_t)(P * L::IN_HALF) + (uint32_t)((v ^ xr_) & (RW_NB - 1)) * (uint32_t)L::IN_SLOT;
+        I = make_float2(lds_in<T, 0>(ad), lds_in<T, 32 * (int)sizeof(T)>(ad));
+    };
+
+    RowState A, B;
+    static_for<0, 2>([&](auto pc) {
+        constexpr int p = decltype(pc)::value;
+        float t0;
+        const int v0 = p ? vs1 : vs0, v1 = min(v0 + 1, p ? ve1 : ve0);
+        fetch(pc, v0, t0, A.pI[p]);
+        A.plo[p] = poly2(cb[p], f2(t0));
+        A.phi[p] = POINT ? A.plo[p] : poly2(cf[p], f2(t0));
+        A.ps[p] = add2(A.plo[p], A.phi[p]);
+        A.cq[p] = A.zF[p] = A.Fp[p] = f2(0.f);
+        A.En[p].x = wk[p][0].npts > 0 ? fmaxf(E0, floorf(A.plo[p].x) + 1.f) : EM + 1.f;
+        A.En[p].y = wk[p][1].npts > 0 ? fmaxf(E0, floorf(A.plo[p].y) + 1.f) : EM + 1.f;
+        fetch(pc, v1, A.tq[p], A.Iq[p]);
+        return true;
+    });
+    auto frontier = [&](const RowState& S) {  // slowest walk's next edge index (no window: EM + 1)
+        return warp_min((int)fminf(fminf(S.En[0].x, S.En[0].y), fminf(S.En[1].x, S.En[1].y)) + m_ref);
+    };
+    // Output batches: once the slowest walk has passed a batch of RW_PB planes, lane 0 stores it
+    // with one TMA store (end of an iteration).  No slot is ever zeroed: each walk writes each plane
+    // from its first edge on exactly once, so the next lap simply overwrites its position (positions
+    // a walk never writes keep their initial 0).  The exception is a plane written through an
+    // overflow slot (RB + s): overflow slots hold the sentinel SENT until a walk writes them, and the
+    // fold at the batch's store takes the overflow value where one was written, else the direct
+    // slot's, and re-arms SENT.  A slot may be rewritten once the store that read it has completed
+    // its shared-memory read (released at the start of the next iteration).
+    int issued_b = 0, zeroed_b = 0;  // batches stored / released for rewriting
+    const int n_batches = (a.M + RW_PB - 1) / RW_PB;
+    auto release = [&]() {
+        if (zeroed_b >= issued_b) return;
+        if (lane == 0) bulk_wait_read<0>();
+        __syncwarp();
+        zeroed_b = issued_b;
+    };
+    auto issue_final = [&](int final_planes) {  // planes [0, final_planes) hold their final values
+        const int nb = final_planes >= a.M ? n_batches : (int)((unsigned)max(final_planes, 0) / RW_PB);
+        if (nb <= issued_b) return;
+        const int b0 = issued_b;
+#pragma unroll 1
+        for (int b = b0; b < nb; ++b) {
+            const int s0 = (b * RW_PB) & (RB - 1);
+            if (s0 < RW_KT - 1) {  // the ring's first slots: fold their overflow planes in
+#pragma unroll
+                for (int q = 0; q < RW_PB; ++q) {
+                    const int s = s0 + q;
+                    if (s >= RW_KT - 1) break;
+                    const uint4 x = lds128u(s_copy + s * PLANE_B), y = lds128u(s_copy + (RB + s) * PLANE_B);
+                    sts128u(s_copy + s * PLANE_B, make_uint4(y.x == SENT ? x.x : y.x, y.y == SENT ? x.y : y.y,
+                                                             y.z == SENT ? x.z : y.z, y.w == SENT ? x.w : y.w));
+                    sts128u(s_copy + (RB + s) * PLANE_B, make_uint4(SENT, SENT, SENT, SENT));
+                }
+            }
+        }
+        issued_b = nb;
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll 1
+            for (int b = b0; b < nb; ++b)
+                tma_store_3d(&out_map, col0, rowl, b * RW_PB, smem + L::OFF_OUT + ((b * RW_PB) & (RB - 1)) * PLANE_B);
+            bulk_commit();
+        }
+    };
+#if DAXM_ROW_CHECK
+    unsigned viol = 0u;
+#endif
+    int fr_e = frontier(A);
+
+    // One iteration: every pair advances one point: point v + 1 closes the zone [lo_v, lo_{v+1}) of
+    // each of its walks, whose bin edges are then evaluated.  A pair past its last visit re-reads it
+    // (its points lie above EM: no edge, whatever the arithmetic yields).  S -> D, no register copies.
+    // Lock step: at iteration it pair p of lane l sits at visit vs + it of its half and reads visit
+    // vs + it + 2 (clamped to its last).  Every pair has read the visits below it + 2 of its half (the
+    // smallest start is 0), and no pair reads beyond min(max vs + it + 2, last visit): warp-uniform
+    // bounds the replay checks with the same formulas (deadlock-free iff the latter's group is loadable).
+    int it2 = 2;  // it + 2
+    // the next it2 at which group g_issue becomes loadable / group g_wait is needed (warp-uniform)
+    int next_issue = g_issue >= ngroups ? INT_MAX : RW_G * g_issue + RW_G - RW_NB;
+    int next_wait = g_wait * RW_G > need_end ? INT_MAX : RW_G * g_wait - need_hi;
+    auto step = [&](const RowState& S, RowState& D) {
+        // input rings: refill the slots every pair has read past (group g is loadable from it2 =
+        // 4 g + 4 - NB on), wait for what the pairs read next (visit need_hi + it2, group (..)/4)
+        if (it2 >= next_issue) {
+            issue_upto((int)((unsigned)(it2 + RW_NB - RW_G) / RW_G));
+            next_issue = g_issue >= ngroups ? INT_MAX : RW_G * g_issue + RW_G - RW_NB;
+        }
+        if (it2 >= next_wait) {
+            const int need = min(need_hi + it2, need_end);
+#if DAXM_ROW_CHECK
+            if ((int)((unsigned)need / RW_G) >= g_issue) viol |= 1u;
+#endif
+            wait_for(need);
+            next_wait = g_wait * RW_G - need_hi;  // (once need_end's group is in, this stays below it2 forever)
+            if (g_wait * RW_G > need_end) next_wait = INT_MAX;
+        }
+        float2 zw[2], zc[2], zd[2], zg[2], x[2], cnt[2];
+        uint32_t es[4];
+        static_for<0, 2>([&](auto pc) {
+            constexpr int p = decltype(pc)::value;
+            float2 In;
+            fetch(pc, min((p ? vs1 : vs0) + it2, p ? ve1 : ve0), D.tq[p], In);
+            const float2 lo = poly2(cb[p], f2(S.tq[p])), hi = POINT ? lo : poly2(cf[p], f2(S.tq[p]));
+            const float2 s = add2(lo, hi);
+            const float2 c = mul2(mul2(sdir2, sub2(S.pI[p], S.Iq[p])), rcp2(sub2(s, S.ps[p])));
+            const float2 w = sub2(S.phi[p], S.plo[p]);
+            const float2 d = sub2(S.cq[p], c);
+            zw[p] = w;
+            zc[p] = c;
+            zd[p] = d;
+            zg[p] = POINT ? f2(0.f) : mul2(d, mul2(rcp2(w), f2(-0.5f)));
+            // F at the next zone's start: F(lo) = F(plo) + c (lo - plo) + w d / 2
+            D.zF[p] = POINT ? fma2(c, sub2(lo, S.plo[p]), S.zF[p])
+                            : fma2(f2(0.5f), mul2(w, d), fma2(c, sub2(lo, S.plo[p]), S.zF[p]));
+            // edges of the zone [plo, lo): En .. floor(min(lo, EM))
+            const float2 fl = add2(floor2(min2(lo, f2(EM))), f2(1.f));
+            cnt[p] = sub2(fl, add2(S.En[p], gate[p]));
+            x[p] = sub2(S.En[p], S.plo[p]);
+            es[2 * p] = lea9((uint32_t)__float_as_int(S.En[p].x + fbias) & (uint32_t)(RB - 1), ob);
+            es[2 * p + 1] = lea9((uint32_t)__float_as_int(S.En[p].y + fbias) & (uint32_t)(RB - 1), ob);
+            D.En[p] = max2(S.En[p], fl);
+            D.plo[p] = lo;
+            D.phi[p] = hi;
+            D.ps[p] = s;
+            D.pI[p] = S.Iq[p];
+            D.cq[p] = c;
+            D.Iq[p] = In;
+            D.Fp[p] = S.Fp[p];
+            return true;
+        });
+        ++it2;
+        release();
+        // ---- bin edges of the closed zones: a warp-uniform trip count, stores at immediate offsets
+        const int K = warp_max((int)fmaxf(fmaxf(fmaxf(cnt[0].x, cnt[0].y), fmaxf(cnt[1].x, cnt[1].y)), 0.f));
+#if DAXM_ROW_CHECK
+        if (K > RW_KT) viol |= 2u;
+        {   // every plane written this iteration lies below the zeroed part of the ring + RB
+            float pl = -1.0e30f;
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                if (cnt[p].x > 0.f) pl = fmaxf(pl, D.En[p].x - 1.f);
+                if (cnt[p].y > 0.f) pl = fmaxf(pl, D.En[p].y - 1.f);
+            }
+            if (pl > -1.0e29f && (int)pl + m_ref - 1 >= zeroed_b * RW_PB + RB) viol |= 4u;
+        }
+#endif
+        static_for<0, RW_KT>([&](auto kc) {
+            constexpr int k = decltype(kc)::value;
+            if (k >= K) return false;
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
+                float2 F;
+                if (POINT) {
+                    F = fma2(zc[p], x[p], S.zF[p]);
+                } else {
+                    const float2 xc = min2(x[p], zw[p]);
+                    F = fma2(xc, fma2(zg[p], xc, zd[p]), fma2(zc[p], x[p], S.zF[p]));
+                }
+                const float2 o = sub2(F, D.Fp[p]);
+                // staged plane [RW_ROWS][RW_COLS]: rows 0 (x) / 1 (y), column half p
+                constexpr int R1 = RW_COLS * 4;
+                if (p == 0) {
+                    edge_st<k * PLANE_B>(es[0], o.x, F.x, (float)k, cnt[0].x, D.Fp[0].x);
+                    edge_st<k * PLANE_B + R1>(es[1], o.y, F.y, (float)k, cnt[0].y, D.Fp[0].y);
+                } else {
+                    edge_st<k * PLANE_B + 128>(es[2], o.x, F.x, (float)k, cnt[1].x, D.Fp[1].x);
+                    edge_st<k * PLANE_B + R1 + 128>(es[3], o.y, F.y, (float)k, cnt[1].y, D.Fp[1].y);
+                }
+                x[p] = add2(x[p], f2(1.f));
+            }
+            return true;
+        });
+        fr_e = frontier(D);
+        issue_final(fr_e - 1);  // edge e completes plane e - 1: planes below the slowest walk's next are final
+    };
+    // the replay's iteration count, rounded up to even (an extra iteration after every pair has
+    // finished changes nothing: no edges, nothing left to load)
+    const int npair = (ti.niter + 1) >> 1;
+#pragma unroll 1
+    for (int it = 0; it < npair; ++it) {
+        step(A, B);
+        step(B, A);
+    }
+    issue_final(a.M);
+    if (lane == 0) {
+        bulk_wait<0>();
+        // every issued input load must have landed before the CTA exits
+        for (; g_wait < g_issue; ++g_wait)
+            while (!mbar_try(s_bar + (uint32_t)(g_wait & (NG - 1)) * 8u, (uint32_t)(g_wait / NG) & 1u)) {
+            }
+    }
+#if DAXM_ROW_CHECK
+    viol = __reduce_or_sync(0xffffffffu, viol);
+    if (viol && lane == 0 && a.err) atomicOr(a.err, viol);
+#endif
+}
+
+// ------------------------------------------------------------------ admission replay
+// One warp per row tile replays the kernel's schedule (lanes, pauses, frontier, drains) with the
+// kernel's own fp32 arithmetic for the geometry (the intensities do not enter the schedule) and
+// admits the tile (cls != 0) only if
+//   * the same pixel edge is the shallower one at every evaluated point (RW_CLS_FRONT_LO),
+//   * consecutive points of every walk have distinct edge sums and (finite pixels) edge spans
+//     >= 1e-6 bins, so the zone density and ramp slope are finite,
+//   * every window's last point lies at or above the top edge EM (a finished walk has no edge left),
+//   * no iteration closes more than RW_KT edges of one walk,
+//   * the input ring never waits for a group it could not yet load (no deadlock), and
+//   * the planes written at every iteration lie below (zeroed batches) * RW_PB + RB: the ring holds
+//     them (RB = RW_RB_SMALL or RW_RB_LARGE, the smaller that suffices).
+// Walks with a window take part whatever the cutoff (the kernel's schedule is geometric), so the
+// plan-time answer holds for every cutoff.  ti.niter = the schedule's iteration count.
+// d_stats: [0] RB small, [1] RB large, [2] not admitted, [3] max ring need.
+__global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __restrict__ rts, int n_rt,
+                                                       int* __restrict__ d_stats) {
+    const int rt = blockIdx.x;
+    const int lane = threadIdx.x;
+    RowTile ti = rts[rt];
+    const int rr = rt / a.n_rc, rc = rt % a.n_rc;
+    const int row0 = a.row_org + rr * RW_ROWS, col0 = rc * RW_COLS;
+    const bool empty = ti.k_hi < ti.k_lo;  // no pixel window: the kernel streams zeros
+    const bool eligible = !empty && ti.sep == MODE_SEPARATED && ti.k_hi - ti.k_lo + 1 <= MAX_FAST_NV;
+    unsigned bad = (!eligible && !empty) ? RW_WHY_MODE : 0u;  // reasons (RW_WHY_*)
+    bool back_lo = true, front_lo = true;
+    int need = 0, iters = 0;
+    if (eligible) {
+        const int nvt = ti.k_hi - ti.k_lo + 1;
+        const float E0 = (float)(-a.m_ref), EM = (float)(a.M - a.m_ref);
+        float cb[2][2][3], cf[2][2][3], En[2][2], ps[2][2];
+        RowWalk wk[2][2];
+        for (int p = 0; p < 2; ++p)
+            for (int r = 0; r < 2; ++r) {
+                const int e = lane + 32 * p;
+                wk[p][r] = row_walk(a, ti, row0 + r, col0 + e);
+                row_coef(a, rt, r, e, cb[p][r]);
+                row_coef(a, rt, r, a.point_mode ? e : e + 1, cf[p][r]);
+            }
+        int vmin[2], vs[2], ve[2], vsm[2], vnd[2];
+        row_starts(wk, vmin, vs, ve, vsm, vnd);
+        auto tau_of = [&](int p, int v) {  // v relative to vmin[p], exactly as the kernel's table
+            const int vv = vmin[p] + v;
+            return (float)(a.t[ti.dir > 0 ? ti.k_lo + vv : ti.k_hi - vv] - ti.t_ref);
+        };
+        auto point = [&](int p, int r, int v, float& lo, float& hi) {  // walks with a window only
+            const float t = tau_of(p, v);
+            const float x0 = lock_poly(cb[p][r][0], cb[p][r][1], cb[p][r][2], t);
+            const float x1 = a.point_mode ? x0 : lock_poly(cf[p][r][0], cf[p][r][1], cf[p][r][2], t);
+            back_lo &= x0 <= x1;
+            front_lo &= x1 <= x0;
+            lo = fminf(x0, x1);
+            hi = fmaxf(x0, x1);
+        };
+        int v[2], vs_max = 0, vend = 0, pro = 0;
+        for (int p = 0; p < 2; ++p) {
+            for (int r = 0; r < 2; ++r)
+                if (wk[p][r].npts > 0) {
+                    float lo, hi;  // the window's last point at or above the top edge
+                    point(p, r, wk[p][r].v0 + wk[p][r].npts - 1 - vmin[p], lo, hi);
+                    if (!(lo >= EM)) bad |= RW_WHY_TOP;
+                }
+            v[p] = vs[p];
+            vs_max = max(vs_max, vs[p]);
+            vend = max(vend, ve[p]);
+            pro = max(pro, min(vs[p] + 1, ve[p]));
+            for (int r = 0; r < 2; ++r) {
+                En[p][r] = EM + 1.f;  // a walk without a window never has an edge
+                ps[p][r] = 0.f;
+                if (wk[p][r].npts == 0) continue;
+                float lo, hi;
+                point(p, r, vs[p], lo, hi);
+                En[p][r] = fmaxf(E0, floorf(lo) + 1.f);
+                ps[p][r] = lo + hi;
+            }
+        }
+        vs_max = __reduce_max_sync(0xffffffffu, vs_max);
+        vend = __reduce_max_sync(0xffffffffu, vend);
+        const int ngroups = vend / RW_G + 1;
+        int g_issue = min(NG, ngroups);
+        if (__reduce_max_sync(0xffffffffu, pro) / RW_G >= g_issue) bad |= RW_WHY_INPUT;
+        auto frontier = [&]() {
+            return __reduce_min_sync(
+                0xffffffffu, (int)fminf(fminf(En[0][0], En[0][1]), fminf(En[1][0], En[1][1])) + a.m_ref);
+        };
+        int fr_e = frontier();
+        int issued_b = 0, zeroed_b = 0;
+        const int n_batches = (a.M + RW_PB - 1) / RW_PB;
+        for (;;) {
+            if (!__any_sync(0xffffffffu, v[0] < ve[0] || v[1] < ve[1])) break;
+            if (++iters > 4 * nvt + 64) {  // cannot happen (every pair advances every iteration)
+                bad |= RW_WHY_ITER;
+                break;
+            }
+            // the kernel's lock-step input bounds (it = iters - 1): loadable groups, the visit waited for
+            const int it2 = iters + 1;
+            g_issue = max(g_issue, min((it2 + RW_NB - RW_G) / RW_G, ngroups - 1) + 1);
+            const int nd_ = min(vs_max + it2, vend);
+            if (nd_ / RW_G >= g_issue) bad |= RW_WHY_INPUT;  // would wait for a group not yet loadable
+            int kmax = 0, pmax = INT_MIN;
+            for (int p = 0; p < 2; ++p) {
+                if (v[p] < ve[p])
+                    for (int r = 0; r < 2; ++r) {
+                        if (wk[p][r].npts == 0) continue;
+                        float lo, hi;
+                        point(p, r, v[p] + 1, lo, hi);
+                        const float s = lo + hi;
+                        if (!(s != ps[p][r])) bad |= RW_WHY_DENSITY;
+                        if (!a.point_mode && !(hi - lo >= 1e-6f)) bad |= RW_WHY_DENSITY;
+                        ps[p][r] = s;
+                        const float fl = floorf(fminf(lo, EM)) + 1.f;
+                        const float cnt = fl - En[p][r];
+                        if (cnt > 0.f) {
+                            kmax = max(kmax, (int)cnt);
+                            pmax = max(pmax, (int)fl - 2 + a.m_ref);  // plane of the last edge stored
+                        }
+                        En[p][r] = fmaxf(En[p][r], fl);
+                    }
+                ++v[p];
+            }
+            kmax = __reduce_max_sync(0xffffffffu, kmax);
+            pmax = __reduce_max_sync(0xffffffffu, pmax);
+            if (kmax > RW_KT) bad |= RW_WHY_KT;
+            zeroed_b = issued_b;  // zero_pending: batches stored at the previous iteration
+            if (pmax != INT_MIN) need = max(need, pmax - zeroed_b * RW_PB + 1);
+            fr_e = frontier();
+            {   // issue_final, exactly as the kernel
+                const int fp = fr_e - 1;
+                const int nb = fp >= a.M ? n_batches : fp / RW_PB;
+                if (nb > issued_b) issued_b = nb;
+            }
+        }
+        // a finished schedule leaves every walk with a window past the top edge
+        for (int p = 0; p < 2; ++p)
+            for (int r = 0; r < 2; ++r)
+                if (wk[p][r].npts > 0 && !(En[p][r] >= EM + 1.f)) bad |= RW_WHY_TOP;
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    back_lo = __all_sync(0xffffffffu, back_lo);
+    front_lo = __all_sync(0xffffffffu, front_lo);
+    if (lane == 0) {
+        int cls = 0;
+        if (!(back_lo || front_lo)) bad |= RW_WHY_ORDER;
+        if (need > RW_RB_LARGE) bad |= RW_WHY_RING;
+        if (!bad) {
+            cls = need <= RW_RB_SMALL ? RW_RB_SMALL : RW_RB_LARGE;
+            if (!back_lo) cls |= RW_CLS_FRONT_LO;
+        }
+        ti.cls = cls;
+        ti.why = (int)bad;
+        ti.niter = iters;
+        rts[rt] = ti;
+        atomicAdd(&d_stats[(cls & RW_CLS_RB) == RW_RB_SMALL ? 0 : (cls & RW_CLS_RB) == RW_RB_LARGE ? 1 : 2], 1);
+        atomicMax(&d_stats[3], need);
+    }
+}
+
+template <typename T, bool POINT, int RB>
+cudaError_t set_attr_one(int max_nv) {
+    (void)max_nv;
+    cudaError_t e = cudaFuncSetAttribute(deposit_row<T, POINT, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)RowSmem<T, RB>::bytes(MAX_FAST_NV));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(deposit_row<T, POINT, RB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared);
+}
+
+template <typename T, bool POINT, int RB>
+cudaError_t launch_one(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int max_nv,
+                       cudaStream_t st) {
+    const size_t sm = RowSmem<T, RB>::bytes(max_nv);
+    deposit_row<T, POINT, RB><<<(unsigned)a.n_list, 32, sm, st>>>(*in_map, *out_map, a);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_t(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int rb, int max_nv,
+                     cudaStream_t st) {
+    if (rb == RW_RB_SMALL)
+        return a.point_mode ? launch_one<T, true, RW_RB_SMALL>(a, in_map, out_map, max_nv, st)
+                            : launch_one<T, false, RW_RB_SMALL>(a, in_map, out_map, max_nv, st);
+    return a.point_mode ? launch_one<T, true, RW_RB_LARGE>(a, in_map, out_map, max_nv, st)
+                        : launch_one<T, false, RW_RB_LARGE>(a, in_map, out_map, max_nv, st);
+}
+
+}  // namespace
+
+size_t row_smem_bytes(int dtype, int rb, int max_nv) {
+    if (dtype == DAXM_U16)
+        return rb == RW_RB_SMALL ? RowSmem<uint16_t, RW_RB_SMALL>::bytes(max_nv)
+                                 : RowSmem<uint16_t, RW_RB_LARGE>::bytes(max_nv);
+    return rb == RW_RB_SMALL ? RowSmem<float, RW_RB_SMALL>::bytes(max_nv) : RowSmem<float, RW_RB_LARGE>::bytes(max_nv);
+}
+
+// The dynamic shared memory limit is a per-device function attribute: set it on the current
+// device for every instance (daxm_create calls this on the plan's device).
+cudaError_t row_set_attributes(int max_nv) {
+    cudaError_t e;
+    if ((e = set_attr_one<uint16_t, false, RW_RB_SMALL>(max_nv)) != cudaSuccess) return e;
+    if ((e = set_attr_one<uint16_t, false, RW_RB_LARGE>(max_nv)) != cudaSuccess) return e;
+    if ((e = set_attr_one<uint16_t, true, RW_RB_SMALL>(max_nv)) != cudaSuccess) return e;
+    if ((e = set_attr_one<uint16_t, true, RW_RB_LARGE>(max_nv)) != cudaSuccess) return e;
+    if ((e = set_attr_one<float, false, RW_RB_SMALL>(max_nv)) != cudaSuccess) return e;
+    if ((e = set_attr_one<float, false, RW_RB_LARGE>(max_nv)) != cudaSuccess) return e;
+    if ((e = set_attr_one<float, true, RW_RB_SMALL>(max_nv)) != cudaSuccess) return e;
+    return set_attr_one<float, true, RW_RB_LARGE>(max_nv);
+}
+
+cudaError_t launch_row(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int dtype, int rb,
+                       cudaStream_t st) {
+    if (a.n_list <= 0) return cudaSuccess;
+    const int max_nv = a.max_nv;
+    return dtype == DAXM_U16 ? launch_t<uint16_t>(a, in_map, out_map, rb, max_nv, st)
+                             : launch_t<float>(a, in_map, out_map, rb, max_nv, st);
+}
+
+cudaError_t launch_row_admit(const RowArgs& a, RowTile* rt, int n_rt, int* d_stats, cudaStream_t st) {
+    if (n_rt <= 0) return cudaSuccess;
+    row_admit_kernel<<<(unsigned)n_rt, 32, 0, st>>>(a, rt, n_rt, d_stats);
+    return cudaGetLastError();
+}
+
+}  // namespace daxm

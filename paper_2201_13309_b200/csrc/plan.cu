@@ -80,12 +80,24 @@ struct daxm_plan {
     float cutoff = 0.f;
     unsigned long long* d_hist = nullptr;  // cutoff selection scratch (256 counters)
     unsigned char* d_live = nullptr;       // [n_tr][n_tc] cutoff: tile has a pixel above it
+    // row-segment kernel (deposit_row.cu): row tiles of RW_ROWS x RW_COLS pixels
+    bool row_ok = false;                   // the row path is available for this plan
+    int row_org = 0, n_rr = 0, n_rc = 0;   // global row of row-tile row 0 (= row_begin), rows, columns
+    int max_nv_row = 0;                    // largest row-tile step range
+    RowTile* d_rt = nullptr;
+    float* d_rcoef = nullptr;
+    int* d_rlist = nullptr;                // class lists [small][large][general], each ascending
+    std::vector<int> h_rlist;
+    int n_rcls[3] = {0, 0, 0};
+    unsigned* d_row_err = nullptr;         // DAXM_ROW_CHECK builds: schedule violations
+    CUtensorMap row_in_map{}, row_out_map{};
     daxm_plan_stats stats{};
     std::string err;
 };
 
 static thread_local std::string g_create_err;
 static DepositArgs make_args(const daxm_plan* p, int dtype);
+static RowArgs make_row_args(const daxm_plan* p);
 
 namespace {
 
@@ -164,6 +176,12 @@ __global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire
     const int jl = blockIdx.y * blockDim.y + threadIdx.y;
     if (i >= g.C || jl >= pre_rows) return;
     const int j = pre_row0 + jl;
+    if (j < band_r0 || j >= band_r1) {  // rows of a boundary tile outside the band: never output
+        win[(size_t)jl * g.C + i] = make_int2(0, 0);
+        pdir[(size_t)jl * g.C + i] = 0;
+        psep[(size_t)jl * g.C + i] = 3;
+        return;
+    }
     double Qb[3], Qf[3];
     edge_point(g, j, i, Qb);
     edge_point(g, j, g.point_mode ? i : i + 1, Qf);
@@ -174,10 +192,12 @@ __global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire
     double ub0 = tangent_u(g, Qb, sb, wire), uf0 = tangent_u(g, Qf, sf, wire);
     int first = -1, last = -1;
     bool prev_nan = false, first_prev_nan = false, pending_nan = false, next_nan = false, nan_inside = false;
+    bool any_valid = false;
     for (int k = 0; k + 1 < g.S; ++k) {
         double ub1 = tangent_u(g, Qb, sb, wire + 3 * (k + 1)), uf1 = tangent_u(g, Qf, sf, wire + 3 * (k + 1));
         bool isn = isnan(ub0) || isnan(uf0) || isnan(ub1) || isnan(uf1);
         if (last >= 0 && k == last + 1) next_nan = isn;
+        any_valid |= !isn;
         if (!isn) {
             double lo = fmin(fmin(ub0, uf0), fmin(ub1, uf1)), hi = fmax(fmax(ub0, uf0), fmax(ub1, uf1));
             if (hi > lower && lo < upper) {
@@ -197,12 +217,13 @@ __global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire
     }
     int2 w = make_int2(0, 0);
     signed char dir = 0, sep = 3;
+    if (any_valid) atomicAdd(&counters[4], 1ull);  // a pixel with every pair NaN is invalid (reading R8)
     if (first >= 0) {
+        // NaN pairs inside the window (the pixel edge inside the wire cylinder at some step): the
+        // pairs are skipped (reading R8) by the exact-table general kernel the host then selects
         if (nan_inside) atomicOr(flags, FLAG_NAN_IN_WINDOW);
-        if (j >= band_r0 && j < band_r1) {
-            atomicAdd(&counters[2], (unsigned long long)(last - first + 1));
-            atomicAdd(&counters[3], 1ull);
-        }
+        atomicAdd(&counters[2], (unsigned long long)(last - first + 1));
+        atomicAdd(&counters[3], 1ull);
         int kb = first, ke = last + 1;  // pairs [kb, ke)
         if (kb > 0 && !first_prev_nan) --kb;             // one guard pair each side (fp32 rounding)
         if (ke <= g.S - 2 && !next_nan) ++ke;
@@ -395,14 +416,81 @@ __global__ void __launch_bounds__(1024) tile_kernel(GeomConst g, const double* _
     }
 }
 
-// ------------------------------------------------------------ cubic fit
+// ------------------------------------------------------------ depth polynomial fit
+// One edge point Q (edge side sg): the depth u(t) in bins relative to m_ref as a polynomial of
+// degree NCOEF-1 in tau = t - t_ref, Chebyshev-interpolated in fp64 over the tile's step range
+// [t_{k_lo}, t_{k_hi}], stored fp32, and verified against the exact depth at every step the
+// deposit kernels can read: model error (fp64 polynomial) and stored error (fp32 coefficients,
+// fp32 tau, the kernels' evaluation).
+__device__ void fit_point(const GeomConst& g, const double* __restrict__ t, const double* __restrict__ wire,
+                          double t_ref, int k_lo, int k_hi, const double Q[3], double sg, unsigned* flags,
+                          float cf[NCOEF], double& local_err, double& local_model) {
+    const double h = 0.5 * (t[k_hi] - t[k_lo]);
+    double b[NCOEF];
+    for (int m = 0; m < NCOEF; ++m) b[m] = 0.0;
+    if (h > 0.0) {
+        // Chebyshev interpolation at the NCOEF first-kind nodes of [t_lo, t_hi]
+        double a[NCOEF];
+        for (int m = 0; m < NCOEF; ++m) a[m] = 0.0;
+        for (int n = 0; n < NCOEF; ++n) {
+            const double th = M_PI * (2 * n + 1) / (2.0 * NCOEF);
+            const double x = cos(th);
+            const double tn = t_ref + h * x;
+            double W[3] = {g.w0[0] + tn * g.d[0], g.w0[1] + tn * g.d[1], g.w0[2] + tn * g.d[2]};
+            const double u = tangent_u(g, Q, sg, W);
+            if (isnan(u)) atomicOr(flags, FLAG_FIT_NAN);
+            for (int m = 0; m < NCOEF; ++m) a[m] += u * cos(m * th);
+        }
+        for (int m = 0; m < NCOEF; ++m) a[m] *= (m == 0 ? 1.0 : 2.0) / NCOEF;
+        // Chebyshev -> monomial in x (T_{n+1} = 2x T_n - T_{n-1}), then x = tau / h
+        double Tm[NCOEF], Tc[NCOEF], Tn[NCOEF], bx[NCOEF];
+        for (int m = 0; m < NCOEF; ++m) Tm[m] = Tc[m] = bx[m] = 0.0;
+        Tm[0] = 1.0;                 // T_0
+        if (NCOEF > 1) Tc[1] = 1.0;  // T_1
+        for (int m = 0; m < NCOEF; ++m) bx[m] += a[0] * Tm[m];
+        if (NCOEF > 1)
+            for (int m = 0; m < NCOEF; ++m) bx[m] += a[1] * Tc[m];
+        for (int n = 2; n < NCOEF; ++n) {
+            for (int m = 0; m < NCOEF; ++m) Tn[m] = (m > 0 ? 2.0 * Tc[m - 1] : 0.0) - Tm[m];
+            for (int m = 0; m < NCOEF; ++m) {
+                bx[m] += a[n] * Tn[m];
+                Tm[m] = Tc[m];
+                Tc[m] = Tn[m];
+            }
+        }
+        double hp = 1.0;
+        for (int m = 0; m < NCOEF; ++m) {
+            b[m] = bx[m] / hp;
+            hp *= h;
+        }
+    } else {
+        double W[3] = {g.w0[0] + t_ref * g.d[0], g.w0[1] + t_ref * g.d[1], g.w0[2] + t_ref * g.d[2]};
+        b[0] = tangent_u(g, Q, sg, W);
+        if (isnan(b[0])) atomicOr(flags, FLAG_FIT_NAN);
+    }
+    for (int m = 0; m < NCOEF; ++m) cf[m] = (float)b[m];
+    for (int k = k_lo; k <= k_hi; ++k) {
+        const double ex = tangent_u(g, Q, sg, wire + 3 * k);
+        if (isnan(ex)) continue;
+        const double td = t[k] - t_ref;
+        const double tau = (double)(float)td;
+        double pm = b[NCOEF - 1], pp = (double)cf[NCOEF - 1];
+        for (int m = NCOEF - 2; m >= 0; --m) {
+            pm = b[m] + td * pm;
+            pp = (double)cf[m] + tau * pp;
+        }
+        local_model = fmax(local_model, fabs(pm - ex));
+        local_err = fmax(local_err, fabs(pp - ex));
+    }
+}
+
 __global__ void __launch_bounds__(1024) fit_kernel(GeomConst g, const double* __restrict__ t, const double* __restrict__ wire, int tr0,
                            int n_tc, const TileInfo* __restrict__ tiles, float* __restrict__ coef,
                            unsigned* __restrict__ flags, double* __restrict__ max_err) {
     const int tile = blockIdx.x;
     const int tr = tile / n_tc, tc = tile % n_tc;
     const TileInfo ti = tiles[tile];
-    const int r = threadIdx.x;  // row in tile (32)
+    const int r = threadIdx.x;  // row in tile
     const int j = (tr0 + tr) * TILE_R + r;
     double local_err = 0.0, local_model = 0.0;
     for (int e = threadIdx.y; e < TILE_E; e += blockDim.y) {
@@ -413,71 +501,88 @@ __global__ void __launch_bounds__(1024) fit_kernel(GeomConst g, const double* __
         if (ti.k_hi >= ti.k_lo && j < g.R && eg < n_edges) {
             double Q[3];
             edge_point(g, j, eg, Q);
-            const double sg = edge_sigma(g, Q);
-            const double h = 0.5 * (t[ti.k_hi] - t[ti.k_lo]);
-            double b[NCOEF];
-            for (int m = 0; m < NCOEF; ++m) b[m] = 0.0;
-            if (h > 0.0) {
-                // Chebyshev interpolation at the NCOEF first-kind nodes of [t_lo, t_hi]
-                double a[NCOEF];
-                for (int m = 0; m < NCOEF; ++m) a[m] = 0.0;
-                for (int n = 0; n < NCOEF; ++n) {
-                    const double th = M_PI * (2 * n + 1) / (2.0 * NCOEF);
-                    const double x = cos(th);
-                    const double tn = ti.t_ref + h * x;
-                    double W[3] = {g.w0[0] + tn * g.d[0], g.w0[1] + tn * g.d[1], g.w0[2] + tn * g.d[2]};
-                    const double u = tangent_u(g, Q, sg, W);
-                    if (isnan(u)) atomicOr(flags, FLAG_FIT_NAN);
-                    for (int m = 0; m < NCOEF; ++m) a[m] += u * cos(m * th);
-                }
-                for (int m = 0; m < NCOEF; ++m) a[m] *= (m == 0 ? 1.0 : 2.0) / NCOEF;
-                // Chebyshev -> monomial in x (T_{n+1} = 2x T_n - T_{n-1}), then x = tau / h
-                double Tm[NCOEF], Tc[NCOEF], Tn[NCOEF], bx[NCOEF];
-                for (int m = 0; m < NCOEF; ++m) Tm[m] = Tc[m] = bx[m] = 0.0;
-                Tm[0] = 1.0;           // T_0
-                if (NCOEF > 1) Tc[1] = 1.0;  // T_1
-                for (int m = 0; m < NCOEF; ++m) bx[m] += a[0] * Tm[m];
-                if (NCOEF > 1)
-                    for (int m = 0; m < NCOEF; ++m) bx[m] += a[1] * Tc[m];
-                for (int n = 2; n < NCOEF; ++n) {
-                    for (int m = 0; m < NCOEF; ++m) Tn[m] = (m > 0 ? 2.0 * Tc[m - 1] : 0.0) - Tm[m];
-                    for (int m = 0; m < NCOEF; ++m) {
-                        bx[m] += a[n] * Tn[m];
-                        Tm[m] = Tc[m];
-                        Tc[m] = Tn[m];
-                    }
-                }
-                double hp = 1.0;
-                for (int m = 0; m < NCOEF; ++m) {
-                    b[m] = bx[m] / hp;
-                    hp *= h;
-                }
-            } else {
-                double W[3] = {g.w0[0] + ti.t_ref * g.d[0], g.w0[1] + ti.t_ref * g.d[1],
-                               g.w0[2] + ti.t_ref * g.d[2]};
-                b[0] = tangent_u(g, Q, sg, W);
-                if (isnan(b[0])) atomicOr(flags, FLAG_FIT_NAN);
-            }
-            for (int m = 0; m < NCOEF; ++m) cf[m] = (float)b[m];
-            // verify against the exact depth at every step the kernel can read:
-            //   model error  -- fp64 cubic (approximation quality, hard limit)
-            //   stored error -- what the kernel evaluates: fp32 coefficients, fp32 tau
-            for (int k = ti.k_lo; k <= ti.k_hi; ++k) {
-                const double ex = tangent_u(g, Q, sg, wire + 3 * k);
-                if (isnan(ex)) continue;
-                const double td = t[k] - ti.t_ref;
-                const double tau = (double)(float)td;
-                double pm = b[NCOEF - 1], p = (double)cf[NCOEF - 1];
-                for (int m = NCOEF - 2; m >= 0; --m) {
-                    pm = b[m] + td * pm;
-                    p = (double)cf[m] + tau * p;
-                }
-                local_model = fmax(local_model, fabs(pm - ex));
-                local_err = fmax(local_err, fabs(p - ex));
-            }
+            fit_point(g, t, wire, ti.t_ref, ti.k_lo, ti.k_hi, Q, edge_sigma(g, Q), flags, cf, local_err, local_model);
         }
         for (int m = 0; m < NCOEF; ++m) coef[(((size_t)tile * NCOEF + m) * TILE_E + e) * TILE_R + r] = cf[m];
     }
+    if (local_err > 0.0) atomic_max_pos_double(max_err, local_err);
+    if (local_model > 0.0) atomic_max_pos_double(max_err + 1, local_model);
+}
+
+// ------------------------------------------------------------ row tiles (deposit_row.cu)
+// One CTA per row tile (RW_ROWS x RW_COLS pixels): union of the band pixels' windows, direction,
+// span regime, t_ref.  Rows outside the band carry no window (pixel_window_kernel).
+__global__ void __launch_bounds__(RW_ROWS * RW_COLS) row_tile_kernel(
+    GeomConst g, const double* __restrict__ t, int row_org, int n_rc, int pre_row0, int pre_rows,
+    const int2* __restrict__ win, const signed char* __restrict__ pdir, const signed char* __restrict__ psep,
+    RowTile* __restrict__ rts, unsigned* __restrict__ flags) {
+    const int rt = blockIdx.x;
+    const int rr = rt / n_rc, rc = rt % n_rc;
+    const int j = row_org + rr * RW_ROWS + (int)threadIdx.y, i = rc * RW_COLS + (int)threadIdx.x;
+    __shared__ int s_kb, s_ke, s_pos, s_neg, s_nsep, s_novl;
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        s_kb = INT_MAX;
+        s_ke = INT_MIN;
+        s_pos = s_neg = s_nsep = s_novl = 0;
+    }
+    __syncthreads();
+    if (i < g.C && j >= pre_row0 && j < pre_row0 + pre_rows) {
+        const size_t q = (size_t)(j - pre_row0) * g.C + i;
+        const int2 w = win[q];
+        if (w.y > w.x) {
+            atomicMin(&s_kb, w.x);
+            atomicMax(&s_ke, w.y);
+            if (pdir[q] > 0) atomicOr(&s_pos, 1);
+            if (pdir[q] < 0) atomicOr(&s_neg, 1);
+            if (!(psep[q] & 1)) atomicOr(&s_nsep, 1);
+            if (!(psep[q] & 2)) atomicOr(&s_novl, 1);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        RowTile ti;
+        ti.cls = 0;
+        ti.niter = 0;
+        ti.why = 0;
+        if (s_kb == INT_MAX) {
+            ti.t_ref = 0.0;
+            ti.k_lo = 0;
+            ti.k_hi = -1;
+            ti.dir = 1;
+            ti.sep = MODE_SEPARATED;
+        } else {
+            ti.dir = s_neg ? -1 : 1;
+            // room for the lock-step starts before the windows (deposit_row.cu row_starts)
+            ti.k_lo = ti.dir > 0 ? max(s_kb - RW_EXT, 0) : s_kb;
+            ti.k_hi = ti.dir > 0 ? s_ke : min(s_ke + RW_EXT, g.S - 1);
+            ti.t_ref = 0.5 * (t[ti.k_lo] + t[ti.k_hi]);
+            ti.sep = !s_nsep ? MODE_SEPARATED : !s_novl ? MODE_OVERLAP : MODE_GENERAL;
+            if (s_pos && s_neg) atomicOr(flags, FLAG_MIXED_DIR);
+        }
+        rts[rt] = ti;
+    }
+}
+
+// Depth polynomials of a row tile's edge points: [rt][NCOEF][RW_COLS + 1 edge columns][RW_ROWS].
+__global__ void __launch_bounds__(RW_ROWS * (RW_COLS + 1)) row_fit_kernel(
+    GeomConst g, const double* __restrict__ t, const double* __restrict__ wire, int row_org, int n_rc,
+    const RowTile* __restrict__ rts, float* __restrict__ coef, unsigned* __restrict__ flags,
+    double* __restrict__ max_err) {
+    const int rt = blockIdx.x;
+    const RowTile ti = rts[rt];
+    const int rr = rt / n_rc, rc = rt % n_rc;
+    const int r = threadIdx.x, e = threadIdx.y;  // RW_ROWS x (RW_COLS + 1)
+    const int j = row_org + rr * RW_ROWS + r, eg = rc * RW_COLS + e;
+    const int n_edges = g.point_mode ? g.C : g.C + 1;
+    double local_err = 0.0, local_model = 0.0;
+    float cf[NCOEF];
+    for (int m = 0; m < NCOEF; ++m) cf[m] = 0.f;
+    if (ti.k_hi >= ti.k_lo && j < g.R && eg < n_edges) {
+        double Q[3];
+        edge_point(g, j, eg, Q);
+        fit_point(g, t, wire, ti.t_ref, ti.k_lo, ti.k_hi, Q, edge_sigma(g, Q), flags, cf, local_err, local_model);
+    }
+    for (int m = 0; m < NCOEF; ++m) coef[(((size_t)rt * NCOEF + m) * (RW_COLS + 1) + e) * RW_ROWS + r] = cf[m];
     if (local_err > 0.0) atomic_max_pos_double(max_err, local_err);
     if (local_model > 0.0) atomic_max_pos_double(max_err + 1, local_model);
 }
@@ -532,6 +637,14 @@ void free_plan_memory(daxm_plan* p) {
     cudaFree(p->d_toff);
     cudaFree(p->d_lock_err);
     p->d_lock_err = nullptr;
+    cudaFree(p->d_rt);
+    cudaFree(p->d_rcoef);
+    cudaFree(p->d_rlist);
+    cudaFree(p->d_row_err);
+    p->d_rt = nullptr;
+    p->d_rcoef = nullptr;
+    p->d_rlist = nullptr;
+    p->d_row_err = nullptr;
     for (int i = 0; i < 2; ++i)
         if (p->st_cls[i]) cudaStreamDestroy(p->st_cls[i]);
     for (int i = 0; i < 3; ++i)
@@ -638,6 +751,89 @@ __global__ void __launch_bounds__(1024) table_kernel(GeomConst g, const double* 
     }
 }
 
+// Row tiles of the row-segment kernel (deposit_row.cu): union windows, depth polynomials, and the
+// admission replay; per-class lists (ascending row-tile index) for the launches.
+daxm_status row_prepass(daxm_plan* p, int) {
+    const daxm_geometry& g = p->g;
+    GeomConst& gc = p->gc;
+    // row tiles start at the band's first row (a band start inside a tile would need a negative TMA
+    // row coordinate, which bulk-tensor stores reject); for even band starts they stay aligned to
+    // global rows, so such a band reproduces the full-detector plan bit for bit
+    p->row_org = g.row_begin;
+    p->n_rr = (g.row_end - g.row_begin + RW_ROWS - 1) / RW_ROWS;
+    p->n_rc = (g.n_cols + RW_COLS - 1) / RW_COLS;
+    const size_t n_rt = (size_t)p->n_rr * p->n_rc;
+    CK(cudaMalloc(&p->d_rt, sizeof(RowTile) * n_rt));
+    CK(cudaMalloc(&p->d_rcoef, sizeof(float) * n_rt * NCOEF * (RW_COLS + 1) * RW_ROWS));
+    CK(cudaMalloc(&p->d_row_err, 64));
+    CK(cudaMemset(p->d_row_err, 0, 64));
+    unsigned* d_flags = p->d_row_err + 4;  // [4] flags, [6..9] fit errors (doubles), [10..13] stats
+    double* d_err = reinterpret_cast<double*>(p->d_row_err + 6);
+    int* d_stats = reinterpret_cast<int*>(p->d_row_err + 10);
+    row_tile_kernel<<<(unsigned)n_rt, dim3(RW_COLS, RW_ROWS)>>>(gc, p->d_t, p->row_org, p->n_rc, p->pre_row0,
+                                                                p->pre_rows, p->d_win, p->d_pdir, p->d_psep, p->d_rt,
+                                                                d_flags);
+    CK(cudaGetLastError());
+    row_fit_kernel<<<(unsigned)n_rt, dim3(RW_ROWS, RW_COLS + 1)>>>(gc, p->d_t, p->d_wire, p->row_org, p->n_rc,
+                                                                   p->d_rt, p->d_rcoef, d_flags, d_err);
+    CK(cudaGetLastError());
+    std::vector<RowTile> ht(n_rt);
+    CK(cudaMemcpy(ht.data(), p->d_rt, sizeof(RowTile) * n_rt, cudaMemcpyDeviceToHost));
+    p->max_nv_row = 1;
+    for (const RowTile& t : ht)
+        if (t.k_hi >= t.k_lo) p->max_nv_row = std::max(p->max_nv_row, t.k_hi - t.k_lo + 1);
+    {
+        RowArgs ra = make_row_args(p);
+        CK(launch_row_admit(ra, p->d_rt, (int)n_rt, d_stats, 0));
+    }
+    unsigned char hb[64];
+    CK(cudaMemcpy(hb, p->d_row_err, 64, cudaMemcpyDeviceToHost));
+    unsigned flags;
+    double ferr[2];
+    int hs[4];
+    memcpy(&flags, hb + 16, 4);
+    memcpy(ferr, hb + 24, 16);
+    memcpy(hs, hb + 40, 16);
+    CK(cudaMemset(p->d_row_err, 0, 64));
+    CK(cudaMemcpy(ht.data(), p->d_rt, sizeof(RowTile) * n_rt, cudaMemcpyDeviceToHost));
+    // the row path needs the same depth-model tolerance as the deposit tiles' (else: old path)
+    if ((flags & (FLAG_FIT_NAN | FLAG_MIXED_DIR)) || !(ferr[1] <= MODEL_ERR_MAX) || !(ferr[0] <= 1e-3)) return DAXM_OK;
+    std::vector<int> lists[3];
+    p->stats.row_reject_bits = 0;
+    for (size_t q = 0; q < n_rt; ++q) {
+        p->stats.row_reject_bits |= ht[q].why;
+        for (int b = 0; b < 8; ++b)
+            if (ht[q].why & (1 << b)) ++p->stats.row_reject[b];
+        const int rb = ht[q].cls & RW_CLS_RB;
+        lists[rb == RW_RB_SMALL ? 0 : rb == RW_RB_LARGE ? 1 : 2].push_back((int)q);
+    }
+    p->h_rlist.clear();
+    for (int c = 0; c < 3; ++c) {
+        p->n_rcls[c] = (int)lists[c].size();
+        p->h_rlist.insert(p->h_rlist.end(), lists[c].begin(), lists[c].end());
+    }
+    CK(cudaMalloc(&p->d_rlist, sizeof(int) * std::max<size_t>(p->h_rlist.size(), 1)));
+    CK(cudaMemcpy(p->d_rlist, p->h_rlist.data(), sizeof(int) * p->h_rlist.size(), cudaMemcpyHostToDevice));
+    CK(row_set_attributes(p->max_nv_row));
+    p->stats.row_tiles_small = p->n_rcls[0];
+    p->stats.row_tiles_large = p->n_rcls[1];
+    p->stats.row_tiles_general = p->n_rcls[2];
+    p->stats.row_ring_need_max = hs[3];
+    // one path per plan: the row-segment kernel when it admits every row tile, else the deposit-tile
+    // kernels (step-locked, fast, general) of round 1, which cover the overlapping-span regime
+    if (p->n_rcls[2] > 0 && getenv("DAXM_ROW_PARTIAL") == nullptr) return DAXM_OK;
+    p->stats.fit_max_err_bins = std::max(p->stats.fit_max_err_bins, ferr[0]);
+    p->stats.fit_model_err_bins = std::max(p->stats.fit_model_err_bins, ferr[1]);
+    p->stats.device_bytes += (int64_t)(sizeof(RowTile) * n_rt + sizeof(float) * n_rt * NCOEF * (RW_COLS + 1) * RW_ROWS +
+                                       sizeof(int) * p->h_rlist.size());
+    p->row_ok = true;
+    if (p->n_rcls[1] + p->n_rcls[2] > 0 && !p->st_cls[0]) {  // class launches fork onto two streams
+        for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&p->st_cls[i], cudaStreamNonBlocking));
+        for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&p->ev_cls[i], cudaEventDisableTiming));
+    }
+    return DAXM_OK;
+}
+
 daxm_status device_prepass(daxm_plan* p) {
     const daxm_geometry& g = p->g;
     GeomConst& gc = p->gc;
@@ -706,11 +902,11 @@ daxm_status device_prepass(daxm_plan* p) {
     cudaFree(d_flags);
     unsigned flags;
     double max_err, model_err;
-    unsigned long long cnt[4];
+    unsigned long long cnt[5];
     memcpy(&flags, hb, 4);
     memcpy(&max_err, hb + 8, 8);
     memcpy(&model_err, hb + 16, 8);
-    memcpy(cnt, hb + 24, 32);
+    memcpy(cnt, hb + 24, 40);
 
     daxm_plan_stats& st = p->stats;
     st.n_bins = p->M;
@@ -734,10 +930,13 @@ daxm_status device_prepass(daxm_plan* p) {
     if (flags & (FLAG_NONMONOTONE | FLAG_MIXED_DIR))
         return fail(nullptr, DAXM_ERR_NONMONOTONE_SCAN,
                     "a pixel edge's tangent depth is not monotone in the wire step inside its window (flags 0x%x)", flags);
-    if (flags & FLAG_NAN_IN_WINDOW)
-        return fail(nullptr, DAXM_ERR_GEOMETRY, "NaN tangent depth inside a pixel's contributing window");
-    // depth source: the travel polynomial where it holds its tolerance, else the exact table
-    const bool use_table = !p->straight || (flags & FLAG_FIT_NAN) || !(model_err <= MODEL_ERR_MAX) ||
+    if (cnt[4] == 0)
+        return fail(nullptr, DAXM_ERR_GEOMETRY,
+                    "every pixel is invalid: each pixel edge lies inside the wire cylinder or its tangent plane is "
+                    "parallel to the beam at every wire step");
+    // depth source: the travel polynomial where it holds its tolerance, else the exact table (also
+    // when a pixel's window holds NaN pairs: the table keeps them NaN and the general kernel skips them)
+    const bool use_table = !p->straight || (flags & (FLAG_FIT_NAN | FLAG_NAN_IN_WINDOW)) || !(model_err <= MODEL_ERR_MAX) ||
                            !(max_err <= 1e-3) || getenv("DAXM_FORCE_TABLE") != nullptr;
     {
         std::vector<TileInfo> ht(n_tiles);
@@ -811,6 +1010,10 @@ daxm_status device_prepass(daxm_plan* p) {
             for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&p->st_cls[i], cudaStreamNonBlocking));
             for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&p->ev_cls[i], cudaEventDisableTiming));
         }
+    }
+    if (!use_table) {
+        daxm_status rs = row_prepass(p, 0);
+        if (rs != DAXM_OK) return rs;
     }
     return DAXM_OK;
 }
@@ -928,6 +1131,15 @@ daxm_status daxm_plan_stats_get(const daxm_plan* p, daxm_plan_stats* st) {
         }
         st->lock_ring_violations = v;
     }
+    if (p->d_row_err) {  // row-segment kernel schedule violations (DAXM_ROW_CHECK builds)
+        DeviceGuard guard(p->device);
+        unsigned v = 0;
+        if (cudaMemcpy(&v, p->d_row_err, sizeof v, cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cudaGetLastError();
+            return DAXM_ERR_CUDA;
+        }
+        st->lock_ring_violations += v;
+    }
     return DAXM_OK;
 }
 
@@ -977,6 +1189,34 @@ static DepositArgs make_args(const daxm_plan* p, int dtype) {
     a.lock_ov_enabled = getenv("DAXM_NO_LOCK_OV") == nullptr;
     a.lock_rest = a.lock_enabled ? p->lock_rest : 1;
     a.lock_err = p->d_lock_err;
+    return a;
+}
+
+static RowArgs make_row_args(const daxm_plan* p) {
+    RowArgs a;
+    a.t = p->d_t;
+    a.rt = p->d_rt;
+    a.win = p->d_win;
+    a.coef = p->d_rcoef;
+    a.list = nullptr;
+    a.n_list = 0;
+    a.R = p->g.n_rows;
+    a.C = p->C;
+    a.S = p->S;
+    a.M = p->M;
+    a.m_ref = p->gc.m_ref;
+    a.row_begin = p->g.row_begin;
+    a.row_end = p->g.row_end;
+    a.pre_row0 = p->pre_row0;
+    a.row_org = p->row_org;
+    a.n_rc = p->n_rc;
+    a.max_nv = p->max_nv_row;
+    a.point_mode = p->gc.point_mode;
+    a.sign = p->g.edge == DAXM_EDGE_TRAILING ? -1.f : 1.f;
+    a.stack = nullptr;
+    a.use_cutoff = p->use_cutoff;
+    a.cutoff = p->cutoff;
+    a.err = p->d_row_err;
     return a;
 }
 
@@ -1043,15 +1283,93 @@ static daxm_status encode_maps(daxm_plan* p, const void* d_stack, int dt, float*
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return fail(p, DAXM_ERR_CUDA, "cuTensorMapEncodeTiled(lock stack) failed: %d", (int)r);
     }
+    if (p->row_ok) {  // row-segment kernel: [RW_G steps][RW_ROWS][RW_COLS] loads, [RW_PB planes][...] stores
+        cuuint64_t dims[3] = {C, R, (cuuint64_t)p->S};
+        cuuint64_t strides[2] = {C * es, C * R * es};
+        cuuint32_t box[3] = {32u, (cuuint32_t)RW_ROWS, (cuuint32_t)RW_G};  // one column half
+        cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = enc(&p->row_in_map, dt == DAXM_U16 ? CU_TENSOR_MAP_DATA_TYPE_UINT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                         3, const_cast<void*>(d_stack), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(p, DAXM_ERR_CUDA, "cuTensorMapEncodeTiled(row stack) failed: %d", (int)r);
+        cuuint64_t odims[3] = {C, R, (cuuint64_t)p->M};
+        cuuint64_t ostrides[2] = {C * 4, C * R * 4};
+        cuuint32_t obox[3] = {(cuuint32_t)RW_COLS, (cuuint32_t)RW_ROWS, (cuuint32_t)RW_PB};
+        r = enc(&p->row_out_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_out, odims, ostrides, obox, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(p, DAXM_ERR_CUDA, "cuTensorMapEncodeTiled(row out) failed: %d", (int)r);
+    }
     p->map_stack = d_stack;
     p->map_out = d_out;
     p->map_dtype = dt;
     return DAXM_OK;
 }
 
+// Row-segment path: one launch per admission class (ring of 16 / 32 planes) plus the general kernel
+// for the row tiles not admitted, forked onto the plan's class streams and joined back into st.
+// tr_begin / tr_end (deposit-tile rows, host pipeline) select the row tiles of those rows.
+static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_out, cudaStream_t st, int tr_begin,
+                           int tr_end) {
+    daxm_status s = encode_maps(p, d_stack, dt, d_out);
+    if (s != DAXM_OK) return s;
+    int ra = 0, rb = p->n_rr;
+    if (tr_end >= 0) {
+        // a row tile straddling a band boundary (odd band start) goes with the later band, whose rows
+        // are copied after the earlier band's
+        const int g0 = (p->tr0 + tr_begin) * TILE_R, g1 = (p->tr0 + tr_end) * TILE_R;
+        ra = g0 <= p->row_org ? 0 : (g0 - p->row_org) / RW_ROWS;
+        rb = g1 >= p->g.row_end ? p->n_rr : std::max(0, (g1 - p->row_org) / RW_ROWS);
+    }
+    int seg[3][2], n_launch = 0, off = 0;
+    for (int c = 0; c < 3; ++c) {
+        const int* b0 = p->h_rlist.data() + off;
+        const int* b1 = b0 + p->n_rcls[c];
+        seg[c][0] = (int)(std::lower_bound(b0, b1, ra * p->n_rc) - p->h_rlist.data());
+        seg[c][1] = (int)(std::lower_bound(b0, b1, rb * p->n_rc) - p->h_rlist.data());
+        n_launch += seg[c][1] > seg[c][0];
+        off += p->n_rcls[c];
+    }
+    const bool fork = n_launch >= 2 && p->st_cls[0] != nullptr && getenv("DAXM_NO_FORK") == nullptr;
+    cudaStream_t sts[3] = {st, fork ? p->st_cls[0] : st, fork ? p->st_cls[1] : st};
+    cudaError_t e = cudaSuccess;
+    if (fork) {
+        e = cudaEventRecord(p->ev_cls[0], st);
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(p->st_cls[i], p->ev_cls[0], 0);
+    }
+    RowArgs a = make_row_args(p);
+    a.stack = d_stack;
+    for (int c = 0; c < 2 && e == cudaSuccess; ++c) {
+        a.list = p->d_rlist + seg[c][0];
+        a.n_list = seg[c][1] - seg[c][0];
+        e = launch_row(a, &p->row_in_map, &p->row_out_map, dt, c == 0 ? RW_RB_SMALL : RW_RB_LARGE, sts[c]);
+    }
+    if (e == cudaSuccess && seg[2][1] > seg[2][0]) {
+        DepositArgs ga = make_args(p, dt);
+        ga.stack = d_stack;
+        e = launch_general_rows(ga, p->d_rlist + seg[2][0], seg[2][1] - seg[2][0], p->n_rc, p->row_org, d_stack, dt,
+                                d_out, sts[2]);
+    }
+    if (fork) {  // join even after a failed launch, so a capture or the caller's stream stays consistent
+        for (int i = 0; i < 2; ++i) {
+            cudaError_t j = cudaEventRecord(p->ev_cls[1 + i], p->st_cls[i]);
+            if (j == cudaSuccess) j = cudaStreamWaitEvent(st, p->ev_cls[1 + i], 0);
+            if (e == cudaSuccess) e = j;
+        }
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(p, DAXM_ERR_CUDA, "row deposit launch: %s", cudaGetErrorString(e));
+    }
+    return DAXM_OK;
+}
+
 static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float* d_out, cudaStream_t st,
                                int tr_begin = 0, int tr_end = -1) {
     const bool fast = fast_possible(p, dt);
+    if (fast && p->row_ok && getenv("DAXM_NO_ROW") == nullptr)
+        return run_row(p, d_stack, dt, d_out, st, tr_begin, tr_end < 0 ? -1 : tr_end);
     if (fast) {
         daxm_status s = encode_maps(p, d_stack, dt, d_out);
         if (s != DAXM_OK) return s;

@@ -61,6 +61,10 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, int c0, int c
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
+}
+template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
@@ -217,6 +221,111 @@ __global__ void __launch_bounds__(128, 4) generic(const __grid_constant__ CUtens
     }
 }
 
+
+// generic with TMA output stores of [4 planes][WR][WC] boxes from a zeroed smem batch, 1 warp per CTA,
+// occupancy set by the dynamic shared memory (sm_bytes)
+template <int WR, int WC>
+__global__ void __launch_bounds__(32) gen_tma(const __grid_constant__ CUtensorMap in_map,
+                                              const __grid_constant__ CUtensorMap out_map) {
+    constexpr int GB = 4 * WR * WC * 2;
+    extern __shared__ __align__(128) unsigned char smem_raw2[];
+    unsigned char* smem = smem_raw2 + ((128 - (smem_u32(smem_raw2) & 127)) & 127);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 4 * GB);
+    float* so = reinterpret_cast<float*>(smem + 4 * GB + 128);
+    const int lane = threadIdx.x;
+    const int n_wc = C / WC;
+    const int wg = blockIdx.x;
+    const int wr = wg / n_wc, wc = wg % n_wc;
+    const int row = wr * WR, col0 = wc * WC;
+    const int k0 = k_first(col0 / 8);
+    if (lane == 0) {
+        for (int g = 0; g < 4; ++g) mbar_init(&bars[g], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int q = lane; q < 4 * WR * WC; q += 32) so[q] = 0.f;
+    __syncwarp();
+    fence_async();
+    int issued = 0;
+    auto issue = [&](int upto) {
+        for (; issued < upto && issued < NIT / 4; ++issued)
+            if (lane == 0) {
+                mbar_expect(&bars[issued & 3], GB);
+                tma_load_3d(smem + (issued & 3) * GB, &in_map, col0, row, k0 + 4 * issued, &bars[issued & 3]);
+            }
+    };
+    issue(4);
+    int done = 0;
+    for (int it = 0; it < NIT; ++it) {
+        if ((it & 3) == 0) {
+            const int g = it >> 2;
+            mbar_wait(&bars[g & 3], (g >> 2) & 1);
+            __syncwarp();
+            issue(g + 4);
+        }
+        const int upto = ((it + 1) * M) / NIT;
+        while (done + 4 <= upto || (upto == M && done < M)) {
+            if (lane == 0) {
+                tma_store_3d(&out_map, col0, row, done, so);
+                bulk_commit();
+            }
+            done += 4;
+        }
+    }
+    if (lane == 0) bulk_wait<0>();
+}
+
+
+// 2 x 64 output boxes, input as two [4][2][32] boxes per group (the column halves at different steps)
+__global__ void __launch_bounds__(32) gen_split(const __grid_constant__ CUtensorMap in_map,
+                                                const __grid_constant__ CUtensorMap out_map) {
+    constexpr int WR = 2, WC = 64, GBH = 4 * WR * 32 * 2;  // one half-box
+    extern __shared__ __align__(128) unsigned char smem_raw3[];
+    unsigned char* smem = smem_raw3 + ((128 - (smem_u32(smem_raw3) & 127)) & 127);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 8 * GBH);
+    float* so = reinterpret_cast<float*>(smem + 8 * GBH + 128);
+    const int lane = threadIdx.x;
+    const int n_wc = C / WC;
+    const int wg = blockIdx.x;
+    const int wr = wg / n_wc, wc = wg % n_wc;
+    const int row = wr * WR, col0 = wc * WC;
+    const int k0 = k_first(col0 / 8), k1 = k_first((col0 + 32) / 8);
+    if (lane == 0) {
+        for (int g = 0; g < 4; ++g) mbar_init(&bars[g], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    for (int q = lane; q < 4 * WR * WC; q += 32) so[q] = 0.f;
+    __syncwarp();
+    fence_async();
+    int issued = 0;
+    auto issue = [&](int upto) {
+        for (; issued < upto && issued < NIT / 4; ++issued)
+            if (lane == 0) {
+                mbar_expect(&bars[issued & 3], 2 * GBH);
+                tma_load_3d(smem + (issued & 3) * 2 * GBH, &in_map, col0, row, k0 + 4 * issued, &bars[issued & 3]);
+                tma_load_3d(smem + (issued & 3) * 2 * GBH + GBH, &in_map, col0 + 32, row, k1 + 4 * issued, &bars[issued & 3]);
+            }
+    };
+    issue(4);
+    int done = 0;
+    for (int it = 0; it < NIT; ++it) {
+        if ((it & 3) == 0) {
+            const int g = it >> 2;
+            mbar_wait(&bars[g & 3], (g >> 2) & 1);
+            __syncwarp();
+            issue(g + 4);
+        }
+        const int upto = ((it + 1) * M) / NIT;
+        while (done + 4 <= upto || (upto == M && done < M)) {
+            if (lane == 0) {
+                tma_store_3d(&out_map, col0, row, done, so);
+                bulk_commit();
+            }
+            done += 4;
+        }
+    }
+    if (lane == 0) bulk_wait<0>();
+}
+
 // coalesced reference: every thread writes 16-byte chunks of a contiguous span and reads the stack
 __global__ void copy_ref(const uint4* __restrict__ in, size_t n_in, float4* __restrict__ out, size_t n_out) {
     uint32_t acc = 0;
@@ -283,11 +392,11 @@ int main() {
     CK(cudaFuncSetAttribute(pattern<2, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb(2, 8)));
     CK(cudaFuncSetAttribute(pattern<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb(2, 4)));
     CK(cudaFuncSetAttribute(pattern<3, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smb(3, 4)));
-    timeit("lock", out_bytes + rd8, [&] { pattern<0, 4><<<grid8, 128, smb(0, 4)>>>(in8, out4, (float*)d_out); });
-    timeit("lockw", out_bytes, [&] { pattern<1, 4><<<grid8, 128, smb(1, 4)>>>(in8, out4, (float*)d_out); });
-    timeit("tma4", out_bytes + rd8, [&] { pattern<2, 4><<<grid8, 128, smb(2, 4)>>>(in8, out4, (float*)d_out); });
-    timeit("tma8", out_bytes + rd8, [&] { pattern<2, 8><<<grid8, 128, smb(2, 8)>>>(in8, out8, (float*)d_out); });
-    timeit("wide", out_bytes + 2 * rd8, [&] { pattern<3, 4><<<grid16, 128, smb(3, 4)>>>(in16, out4, (float*)d_out); });
+    // timeit("lock", out_bytes + rd8, [&] { pattern<0, 4><<<grid8, 128, smb(0, 4)>>>(in8, out4, (float*)d_out); });
+    // timeit("lockw", out_bytes, [&] { pattern<1, 4><<<grid8, 128, smb(1, 4)>>>(in8, out4, (float*)d_out); });
+    // timeit("tma4", out_bytes + rd8, [&] { pattern<2, 4><<<grid8, 128, smb(2, 4)>>>(in8, out4, (float*)d_out); });
+    // timeit("tma8", out_bytes + rd8, [&] { pattern<2, 8><<<grid8, 128, smb(2, 8)>>>(in8, out8, (float*)d_out); });
+    // timeit("wide", out_bytes + 2 * rd8, [&] { pattern<3, 4><<<grid16, 128, smb(3, 4)>>>(in16, out4, (float*)d_out); });
 
     auto mk_in2 = [&](int wr, int wc) {
         CUtensorMap m;
@@ -306,16 +415,48 @@ int main() {
         const int nw = (R / WR) * (C / WC);                                                                \
         timeit(NAME, out_bytes + (IN ? rd8 : 0.0), [&] { generic<WR, WC, IN, ST><<<nw / 4, 128, sb>>>(im, (float*)d_out); }); \
     }
-    GEN("g16x8_out", 16, 8, false, false)
-    GEN("g16x8_out_stag", 16, 8, false, true)
-    GEN("g16x16_out", 16, 16, false, false)
-    GEN("g8x32_out", 8, 32, false, false)
-    GEN("g4x32_out", 4, 32, false, false)
-    GEN("g4x32_out_stag", 4, 32, false, true)
-    GEN("g4x32_in", 4, 32, true, false)
-    GEN("g4x32_in_stag", 4, 32, true, true)
-    GEN("g8x32_in", 8, 32, true, false)
-    GEN("g2x64_in", 2, 64, true, false)
+    // GEN("g16x8_out", 16, 8, false, false)
+    // GEN("g16x8_out_stag", 16, 8, false, true)
+    // GEN("g16x16_out", 16, 16, false, false)
+    // GEN("g8x32_out", 8, 32, false, false)
+    // GEN("g4x32_out", 4, 32, false, false)
+    // GEN("g4x32_out_stag", 4, 32, false, true)
+    // GEN("g4x32_in", 4, 32, true, false)
+    // GEN("g4x32_in_stag", 4, 32, true, true)
+    // GEN("g8x32_in", 8, 32, true, false)
+    // GEN("g2x64_in", 2, 64, true, false)
+
+    auto mk_out2 = [&](int wr, int wc) {
+        CUtensorMap m;
+        cuuint64_t dims[3] = {C, R, M}, str[2] = {C * 4ull, (cuuint64_t)C * R * 4};
+        cuuint32_t box[3] = {(cuuint32_t)wc, (cuuint32_t)wr, 4}, es[3] = {1, 1, 1};
+        if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, d_out, dims, str, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE))
+            exit(5);
+        return m;
+    };
+#define GTMA(NAME, WR, WC, SMB)                                                                               \
+    {                                                                                                          \
+        const CUtensorMap im = mk_in2(WR, WC), om = mk_out2(WR, WC);                                            \
+        CK(cudaFuncSetAttribute(gen_tma<WR, WC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(SMB)));     \
+        const int nw = (R / WR) * (C / WC);                                                                    \
+        timeit(NAME, out_bytes + rd8, [&] { gen_tma<WR, WC><<<nw, 32, SMB>>>(im, om); });                       \
+    }
+    {
+        const CUtensorMap im = mk_in2(2, 32), om = mk_out2(2, 64);
+        for (int smb : {19700, 13500}) {
+            CK(cudaFuncSetAttribute(gen_split, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
+            timeit(smb > 15000 ? "split_2x64_11w" : "split_2x64_16w", out_bytes + rd8,
+                   [&] { gen_split<<<(R / 2) * (C / 64), 32, smb>>>(im, om); });
+        }
+    }
+    GTMA("tma_4x32_11w", 4, 32, 19700)
+    GTMA("tma_4x32_16w", 4, 32, 13500)
+    // GTMA("tma_8x16_11w", 8, 16, 19700)
+    // GTMA("tma_8x16_15w", 8, 16, 14500)
+    GTMA("tma_2x64_11w", 2, 64, 19700)
+    GTMA("tma_2x64_16w", 2, 64, 13500)
+    // GTMA("tma_16x8_11w", 16, 8, 19700)
     int sms = 148;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     timeit("copy", out_bytes + rd8, [&] {

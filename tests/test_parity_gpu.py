@@ -31,7 +31,9 @@ def run_gpu(daxm, g, host_stack, rows=None):
         st = torch.from_numpy(np.ascontiguousarray(host_stack)).to("cuda:0")
         out = plan.reconstruct(st)
         torch.cuda.synchronize()
-        return out.cpu().numpy(), plan.stats()
+        stats = plan.stats()
+        assert stats["lock_ring_violations"] == 0, stats  # counted by DAXM_*_CHECK builds only
+        return out.cpu().numpy(), stats
 
 
 @pytest.mark.parametrize("edge", ["leading", "trailing"])
@@ -44,7 +46,8 @@ def test_c1_full(daxm, edge, pixel_model, dtype):
     gpu, st = run_gpu(daxm, g, host)
     ref = oracle.reconstruct(g, host)
     parity.check(gpu, ref, host, f"C1 {edge} {pixel_model} {dtype}")
-    assert st["fit_model_err_bins"] < 1e-6 and st["fit_max_err_bins"] < 1e-4
+    # the library's depth-model tolerance (MODEL_ERR_MAX = 2e-5 bins, daxm_internal.cuh)
+    assert st["fit_model_err_bins"] < 2e-5 and st["fit_max_err_bins"] < 1e-4
 
 
 @pytest.mark.parametrize("edge", ["leading", "trailing"])
