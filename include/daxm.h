@@ -114,6 +114,8 @@ typedef struct {
     int64_t row_ring_need_max; /* largest output-ring need (planes) the admission replay found          */
     int64_t row_reject_bits;   /* OR of the reasons row tiles were not admitted (RW_WHY_* bits,         */
     int64_t row_reject[8];     /* DESIGN.md §5.3) and the number of row tiles per reason bit            */
+    int64_t row_path;          /* 1: daxm_reconstruct runs the row-segment kernel (every row tile          */
+                               /* admitted), 0: the deposit-tile kernels                                   */
 } daxm_plan_stats;
 
 /* daxm_create -- validate `g`, run the fp64 geometry pre-pass on `cuda_device`,

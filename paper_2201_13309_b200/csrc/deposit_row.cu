@@ -104,6 +104,23 @@ __device__ __forceinline__ void edge_st(uint32_t addr, float o, float F, float k
         : "r"(addr), "f"(o), "f"(kf), "f"(cnt), "f"(F), "n"(OFF)
         : "memory");
 }
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t addr) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr) : "memory");
+    return v;
+}
+// st.shared.f32 [addr + OFF] = v iff k < cnt (one FSETP, a predicated store)
+template <int OFF>
+__device__ __forceinline__ void st_if(uint32_t addr, float v, float kf, float cnt) {
+    asm volatile("{\n .reg .pred q;\n setp.lt.f32 q, %2, %3;\n @q st.shared.f32 [%0+%4], %1;\n}\n" ::"r"(addr),
+                 "f"(v), "f"(kf), "f"(cnt), "n"(OFF)
+                 : "memory");
+}
 template <typename T, int OFF>
 __device__ __forceinline__ float lds_in(uint32_t addr) {
     if constexpr (sizeof(T) == 2) {
@@ -151,8 +168,8 @@ static_assert(RW_H == 2 && RW_ROWS == 2, "deposit_row: two column halves per lan
 // row0 (x) and row0 + 1 (y); the point last visited (plo, phi, ps = lo + hi, pI) and the
 // prefetched next one (tq, Iq).
 struct RowState {
-    float2 plo[2], phi[2], ps[2], pI[2], cq[2], zF[2], Fp[2], En[2], Iq[2];
-    float tq[2];
+    float2 plo[2], phi[2], ps[2], pI[2], cq[2], zF[2], En[2], Iq[2];
+    float tq;
 };
 
 // warp-wide integer min / max (redux.sync, full mask; the loop is convergent by construction)
@@ -188,44 +205,46 @@ __device__ __forceinline__ int opaque(int x) {
     return x;
 }
 
-// Lock-step starts of the warp's walk pairs (kernel and replay).  A pair covers its two walks'
-// windows [ws, we] (visits from the tile's first step).  All pairs advance one visit per iteration,
-// but their depth per visit differs slightly across the 64 columns (2.6 % at C4), so pairs that
-// started together drift apart by the end of their windows.  Aligning the windows' MIDDLES instead
-// halves the largest spread: pair q starts (T - len_q) / 2 visits before its window, T = the
-// warp's longest window (a point before a window lies below the bins: no edge), clamped at the
-// tile's first step (row_tile_kernel extends the step range by RW_EXT for that).  Visits of column
-// half p are then counted from vmin[p], the half's earliest start.
-__device__ __forceinline__ void row_starts(const RowWalk wk[2][2], int vmin[2], int vs[2], int ve[2], int vs_max[2],
-                                           int vend[2]) {
-    int ws[2], we[2], len = -1;
+// Lane -> walks.  Lane l covers column half h = l / 16 of the tile's 64 columns, columns
+// 32 h + 2 i and 32 h + 2 i + 1 (i = l % 16) of both rows: walk pair p = column 32 h + 2 i + (p ^ h)
+// (the swap for h = 1 keeps the edge stores of one instruction on 32 distinct banks), rows 0 (x)
+// and 1 (y).  Both columns of a lane are adjacent, so the lane reads one visit of its half per step.
+__device__ __forceinline__ int rw_col(int lane, int p) { return 32 * (lane >> 4) + 2 * (lane & 15) + (p ^ (lane >> 4)); }
+
+// Lock-step starts (kernel and replay).  A lane covers its four walks' windows [ws, we] (visits from
+// the tile's first step).  All lanes advance one visit per iteration, but their depth per visit
+// differs slightly across the 64 columns (2.6 % at C4), so lanes that started together drift apart
+// by the end of their windows.  Aligning the windows' MIDDLES instead halves the largest spread:
+// lane l starts (T - len_l) / 2 visits before its window, T = the warp's longest window (a point
+// before a window lies below the bins: no edge), clamped at the tile's first step (row_tile_kernel
+// extends the step range by RW_EXT for that).  Visits of column half h are then counted from
+// vmin, the half's earliest start.
+__device__ __forceinline__ void row_starts(const RowWalk wk[2][2], int lane, int& vmin, int& vs, int& ve, int& vs_max,
+                                           int& vend) {
+    int ws = INT_MAX, we = -1;
 #pragma unroll
-    for (int p = 0; p < 2; ++p) {
-        ws[p] = INT_MAX;
-        we[p] = -1;
+    for (int p = 0; p < 2; ++p)
 #pragma unroll
         for (int r = 0; r < 2; ++r)
             if (wk[p][r].npts > 0) {
-                ws[p] = min(ws[p], wk[p][r].v0);
-                we[p] = max(we[p], wk[p][r].v0 + wk[p][r].npts - 1);
+                ws = min(ws, wk[p][r].v0);
+                we = max(we, wk[p][r].v0 + wk[p][r].npts - 1);
             }
-        if (we[p] >= 0) len = max(len, we[p] - ws[p]);
-    }
-    len = __reduce_max_sync(0xffffffffu, len);
+    const int len = __reduce_max_sync(0xffffffffu, we >= 0 ? we - ws : -1);
+    const int st = we >= 0 ? max(ws - ((len - (we - ws)) >> 1), 0) : INT_MAX;
+    // per column half (16 lanes): the earliest start
+    int m = st;
 #pragma unroll
-    for (int p = 0; p < 2; ++p) {
-        const int st = we[p] >= 0 ? max(ws[p] - ((len - (we[p] - ws[p])) >> 1), 0) : INT_MAX;
-        vmin[p] = __reduce_min_sync(0xffffffffu, st);
-        if (vmin[p] == INT_MAX) vmin[p] = 0;  // a half without windows
-        vs[p] = we[p] >= 0 ? st - vmin[p] : 0;  // no window in the column: done at once
-        ve[p] = we[p] >= 0 ? we[p] - vmin[p] : 0;
-        vs_max[p] = __reduce_max_sync(0xffffffffu, vs[p]);
-        vend[p] = __reduce_max_sync(0xffffffffu, ve[p]);
-    }
+    for (int o = 8; o > 0; o >>= 1) m = min(m, __shfl_xor_sync(0xffffffffu, m, o));
+    vmin = m == INT_MAX ? 0 : m;  // a half without windows
+    vs = we >= 0 ? st - vmin : 0;  // no window in the lane's columns: done at once
+    ve = we >= 0 ? we - vmin : 0;
+    vs_max = __reduce_max_sync(0xffffffffu, vs);
+    vend = __reduce_max_sync(0xffffffffu, ve);
 }
 
 template <typename T, bool POINT, int RB>
-__global__ void __launch_bounds__(32) deposit_row(const __grid_constant__ CUtensorMap in_map,
+__global__ void __launch_bounds__(32, 11) deposit_row(const __grid_constant__ CUtensorMap in_map,
                                                   const __grid_constant__ CUtensorMap out_map, const RowArgs a) {
     using L = RowSmem<T, RB>;
     static_assert(RB % RW_PB == 0 && (RB & (RB - 1)) == 0, "ring");
@@ -256,15 +275,15 @@ __global__ void __launch_bounds__(32) deposit_row(const __grid_constant__ CUtens
         sts128u(sbase + L::OFF_OUT + s * PLANE_B + lane * 16, make_uint4(SENT, SENT, SENT, SENT));
     __syncwarp();
 
-    // ---- walks: pair p = column col0 + lane + 32 p, rows row0 (x) and row0 + 1 (y)
+    // ---- walks: pair p = column col0 + rw_col(lane, p), rows row0 (x) and row0 + 1 (y)
     const float E0 = (float)(-a.m_ref);
     float2 cb[2][3], cf[2][3], gate[2];
     bool any_act = false;
     RowWalk wk[2][2];
-    int vmin[2];  // per column half: its earliest start (row_starts)
+    const int hh = lane >> 4;  // the lane's column half
 #pragma unroll
     for (int p = 0; p < 2; ++p) {
-        const int c = col0 + lane + 32 * p;
+        const int e = rw_col(lane, p), c = col0 + e;
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             const int j = row0 + r;
@@ -277,7 +296,6 @@ __global__ void __launch_bounds__(32) deposit_row(const __grid_constant__ CUtens
             any_act |= on;
             (r ? gate[p].y : gate[p].x) = on ? 0.f : 1.0e9f;  // inactive: edge counts below zero
             float cl[3], ch[3];
-            const int e = lane + 32 * p;
             row_coef(a, rt, r, (ti.cls & RW_CLS_FRONT_LO) && !POINT ? e + 1 : e, cl);
             row_coef(a, rt, r, (ti.cls & RW_CLS_FRONT_LO) || POINT ? e : e + 1, ch);
 #pragma unroll
@@ -297,18 +315,19 @@ __global__ void __launch_bounds__(32) deposit_row(const __grid_constant__ CUtens
         }
         return;
     }
-    // visits of half p are counted from its earliest start (vmin[p]); lane l's pair p starts at vs[p]
-    // and ends at ve[p]; all pairs advance in lock step
-    int vs[2], ve[2], vs_max[2], vend[2];
-    row_starts(wk, vmin, vs, ve, vs_max, vend);
+    // visits of the lane's half are counted from the half's earliest start (vmin); the lane starts at
+    // vs and ends at ve; all lanes advance in lock step
+    int vmin_h, vs, ve, vs_max, vend;
+    row_starts(wk, lane, vmin_h, vs, ve, vs_max, vend);
+    const int vmin0 = __shfl_sync(0xffffffffu, vmin_h, 0), vmin1 = __shfl_sync(0xffffffffu, vmin_h, 16);
 
     // ---- input rings, one per column half: visit v of half p in slot (v ^ xr) mod RW_NB; group g =
     // visits [RW_G g, RW_G g + RW_G) of both halves = two TMA boxes of consecutive steps on one
     // mbarrier (ascending k: for dir < 0 a group's visits land in reverse slot order)
     const int xr = dir > 0 ? 0 : RW_G - 1;
-    const int ngroups = max(vend[0], vend[1]) / RW_G + 1;
-    const int kb0 = dir > 0 ? ti.k_lo + vmin[0] : ti.k_hi - vmin[0] - (RW_G - 1);
-    const int kb1 = dir > 0 ? ti.k_lo + vmin[1] : ti.k_hi - vmin[1] - (RW_G - 1);
+    const int ngroups = vend / RW_G + 1;
+    const int kb0 = dir > 0 ? ti.k_lo + vmin0 : ti.k_hi - vmin0 - (RW_G - 1);
+    const int kb1 = dir > 0 ? ti.k_lo + vmin1 : ti.k_hi - vmin1 - (RW_G - 1);
     int g_issue = 0, g_wait = 0;
     auto issue_upto = [&](int lim) {  // groups <= lim (clamped) may be in flight
         lim = min(lim, ngroups - 1);
@@ -333,46 +352,58 @@ __global__ void __launch_bounds__(32) deposit_row(const __grid_constant__ CUtens
         __syncwarp();
     };
     issue_upto(NG - 1);  // nothing consumed yet: visits below every pair's start are never read
-    wait_for(__reduce_max_sync(0xffffffffu, max(min(vs[0] + 1, ve[0]), min(vs[1] + 1, ve[1]))));
+    wait_for(__reduce_max_sync(0xffffffffu, min(vs + 1, ve)));
 
     // loop invariants, kept in registers
     const uint32_t s_copy = opaque(sbase + L::OFF_OUT + (uint32_t)lane * 16u);  // lane's 16 bytes of a plane
-    const float EM = opaque((float)(a.M - a.m_ref));
-    const uint32_t in_lane = opaque(sbase + L::OFF_IN + (uint32_t)lane * (uint32_t)sizeof(T));
-    const uint32_t tau0 = opaque(sbase + L::OFF_TAU + 4u * (uint32_t)vmin[0]);
-    const uint32_t tau1 = opaque(sbase + L::OFF_TAU + 4u * (uint32_t)vmin[1]);
-    const uint32_t ob = opaque(sbase + L::OFF_OUT + (uint32_t)lane * 4u);     // lane's column in a staged plane
+    // the lane's two columns of its half's ring (one 32-bit word per row for u16)
+    const uint32_t in_lane =
+        opaque(sbase + L::OFF_IN + (uint32_t)(hh * L::IN_HALF) + (uint32_t)(2 * (lane & 15)) * (uint32_t)sizeof(T));
+    const uint32_t tau_l = opaque(sbase + L::OFF_TAU + 4u * (uint32_t)vmin_h);
+    const uint32_t ob = sbase + L::OFF_OUT + (uint32_t)(32 * hh + 2 * (lane & 15)) * 4u;  // column 2i of a plane
+    const uint32_t ob0 = opaque(ob + 4u * (uint32_t)hh), ob1 = opaque(ob + 4u * (uint32_t)(hh ^ 1));  // pair 0 / 1
+    const uint32_t swap = hh ? 0x1032u : 0x3210u;  // pair p's column is the (p ^ h)-th of the lane's two
     const float2 sdir2 = f2(opaque(2.f * a.sign * (float)dir));  // c = 2 s dir dI / (sum_{q+1} - sum_q)
+    const float EM = opaque((float)(a.M - a.m_ref));
     const int m_ref = a.m_ref;
     // bits(E + fbias) = 0x4B000000 + e - 1 + RB for edge index e = E + m_ref: its plane's slot in the low bits
     const float fbias = opaque(8388608.f + (float)(m_ref - 1 + RB));
     const int xr_ = opaque(xr);
-    const int ve0 = opaque(ve[0]), ve1 = opaque(ve[1]), vs0 = opaque(vs[0]), vs1 = opaque(vs[1]);
-    const int need_hi = max(vs_max[0], vs_max[1]), need_end = max(vend[0], vend[1]);
+    const int ve_ = opaque(ve), vs_ = opaque(vs);
+    const int need_hi = vs_max, need_end = vend;
 
-    // wire travel and the pair's two intensities at visit v of half P
-    auto fetch = [&](auto pc, int v, float& t, float2& I) {
-        constexpr int P = decltype(pc)::value;
-        t = lds_f32((P ? tau1 : tau0) + 4u * (uint32_t)v);
-        const uint32_t ad = in_lane + (uint32_t)(P * L::IN_HALF) + (uint32_t)((v ^ xr_) & (RW_NB - 1)) * (uint32_t)L::IN_SLOT;
-        I = make_float2(lds_in<T, 0>(ad), lds_in<T, 32 * (int)sizeof(T)>(ad));
+    // wire travel and the two pairs' intensities (rows 0, 1) at visit v of the lane's half
+    auto fetch = [&](int v, float& t, float2 I[2]) {
+        t = lds_f32(tau_l + 4u * (uint32_t)v);
+        const uint32_t ad = in_lane + (uint32_t)((v ^ xr_) & (RW_NB - 1)) * (uint32_t)L::IN_SLOT;
+        if constexpr (sizeof(T) == 2) {
+            const uint32_t w0 = __byte_perm(lds_u32(ad), 0u, swap), w1 = __byte_perm(lds_u32(ad + 64u), 0u, swap);
+            I[0] = make_float2((float)(w0 & 0xffffu), (float)(w1 & 0xffffu));
+            I[1] = make_float2((float)(w0 >> 16), (float)(w1 >> 16));
+        } else {
+            const float2 a0 = lds_f2(ad), a1 = lds_f2(ad + 128u);
+            I[0] = hh ? make_float2(a0.y, a1.y) : make_float2(a0.x, a1.x);
+            I[1] = hh ? make_float2(a0.x, a1.x) : make_float2(a0.y, a1.y);
+        }
     };
 
     RowState A, B;
-    static_for<0, 2>([&](auto pc) {
-        constexpr int p = decltype(pc)::value;
+    {
         float t0;
-        const int v0 = p ? vs1 : vs0, v1 = min(v0 + 1, p ? ve1 : ve0);
-        fetch(pc, v0, t0, A.pI[p]);
-        A.plo[p] = poly2(cb[p], f2(t0));
-        A.phi[p] = POINT ? A.plo[p] : poly2(cf[p], f2(t0));
-        A.ps[p] = add2(A.plo[p], A.phi[p]);
-        A.cq[p] = A.zF[p] = A.Fp[p] = f2(0.f);
-        A.En[p].x = wk[p][0].npts > 0 ? fmaxf(E0, floorf(A.plo[p].x) + 1.f) : EM + 1.f;
-        A.En[p].y = wk[p][1].npts > 0 ? fmaxf(E0, floorf(A.plo[p].y) + 1.f) : EM + 1.f;
-        fetch(pc, v1, A.tq[p], A.Iq[p]);
-        return true;
-    });
+        float2 I0[2];
+        fetch(vs_, t0, I0);
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            A.pI[p] = I0[p];
+            A.plo[p] = poly2(cb[p], f2(t0));
+            A.phi[p] = POINT ? A.plo[p] : poly2(cf[p], f2(t0));
+            A.ps[p] = add2(A.plo[p], A.phi[p]);
+            A.cq[p] = A.zF[p] = f2(0.f);
+            A.En[p].x = wk[p][0].npts > 0 ? fmaxf(E0, floorf(A.plo[p].x) + 1.f) : EM + 1.f;
+            A.En[p].y = wk[p][1].npts > 0 ? fmaxf(E0, floorf(A.plo[p].y) + 1.f) : EM + 1.f;
+        }
+        fetch(min(vs_ + 1, ve_), A.tq, A.Iq);
+    }
     auto frontier = [&](const RowState& S) {  // slowest walk's next edge index (no window: EM + 1)
         return warp_min((int)fminf(fminf(S.En[0].x, S.En[0].y), fminf(S.En[1].x, S.En[1].y)) + m_ref);
     };
@@ -424,7 +455,7 @@ __global__ void __launch_bounds__(32) deposit_row(const __grid_constant__ CUtens
 #if DAXM_ROW_CHECK
     unsigned viol = 0u;
 #endif
-    int fr_e = frontier(A);
+    int fr_e = 0;
 
     // One iteration: every pair advances one point: point v + 1 closes the zone [lo_v, lo_{v+1}) of
     // each of its walks, whose bin edges are then evaluated.  A pair past its last visit re-reads it
@@ -433,112 +464,180 @@ __global__ void __launch_bounds__(32) deposit_row(const __grid_constant__ CUtens
     // vs + it + 2 (clamped to its last).  Every pair has read the visits below it + 2 of its half (the
     // smallest start is 0), and no pair reads beyond min(max vs + it + 2, last visit): warp-uniform
     // bounds the replay checks with the same formulas (deadlock-free iff the latter's group is loadable).
-    int it2 = 2;  // it + 2
+    int it2 = 2;  // it + 2 of the transition about to run (it reads visit vs + it2)
     // the next it2 at which group g_issue becomes loadable / group g_wait is needed (warp-uniform)
     int next_issue = g_issue >= ngroups ? INT_MAX : RW_G * g_issue + RW_G - RW_NB;
     int next_wait = g_wait * RW_G > need_end ? INT_MAX : RW_G * g_wait - need_hi;
-    auto step = [&](const RowState& S, RowState& D) {
-        // input rings: refill the slots every pair has read past (group g is loadable from it2 =
-        // 4 g + 4 - NB on), wait for what the pairs read next (visit need_hi + it2, group (..)/4)
+    // input rings: refill the slots every lane has read past (group g is loadable from it2 = 4 g + 4 -
+    // NB on) and wait for what the next `ahead` + 1 transitions read (visit need_hi + it2 + ahead)
+    auto input = [&](int ahead) {
         if (it2 >= next_issue) {
             issue_upto((int)((unsigned)(it2 + RW_NB - RW_G) / RW_G));
             next_issue = g_issue >= ngroups ? INT_MAX : RW_G * g_issue + RW_G - RW_NB;
         }
-        if (it2 >= next_wait) {
-            const int need = min(need_hi + it2, need_end);
+        if (it2 + ahead >= next_wait) {
+            const int need = min(need_hi + it2 + ahead, need_end);
 #if DAXM_ROW_CHECK
             if ((int)((unsigned)need / RW_G) >= g_issue) viol |= 1u;
 #endif
             wait_for(need);
-            next_wait = g_wait * RW_G - need_hi;  // (once need_end's group is in, this stays below it2 forever)
-            if (g_wait * RW_G > need_end) next_wait = INT_MAX;
+            next_wait = g_wait * RW_G > need_end ? INT_MAX : g_wait * RW_G - need_hi;
         }
-        float2 zw[2], zc[2], zd[2], zg[2], x[2], cnt[2];
-        uint32_t es[4];
+    };
+    // Zone [lo_v, lo_{v+1}) of a walk pair, everything its bin-edge stores need.  Inside the zone
+    // F(E) = F0 + c x + xc (d + g xc), x = E - lo_v, xc = min(x, w); the admission replay checks
+    // w < 2 bins, so from the zone's third edge on x > w and F(E) = h + c x, h = F0 + w d / 2: the
+    // zone's edges En, En + 1, ... receive o0 = F(x0) - Fp (Fp: F at the walk's previous edge),
+    // o1 = F(x0 + 1) - F(x0), o2 = h + c (x0 + 2) - F(x0 + 1), and c for every later one; the walk's
+    // F at its last edge becomes the next Fp.
+    struct Zone {
+        float2 F0v, o1, o2, c, Fl, cnt;
+        uint32_t es[2];
+    };
+    // Transition S -> D: every pair advances one point; point v + 1 closes the zone [lo_v, lo_{v+1})
+    // of each of its walks.  A pair past its last visit re-reads it (its points lie above EM: no
+    // edge, whatever the arithmetic yields).
+    auto trans = [&](const RowState& S, RowState& D, Zone Z[2]) {
+        float2 In[2];
+        fetch(min(vs_ + it2, ve_), D.tq, In);
         static_for<0, 2>([&](auto pc) {
             constexpr int p = decltype(pc)::value;
-            float2 In;
-            fetch(pc, min((p ? vs1 : vs0) + it2, p ? ve1 : ve0), D.tq[p], In);
-            const float2 lo = poly2(cb[p], f2(S.tq[p])), hi = POINT ? lo : poly2(cf[p], f2(S.tq[p]));
+            const float2 lo = poly2(cb[p], f2(S.tq)), hi = POINT ? lo : poly2(cf[p], f2(S.tq));
             const float2 s = add2(lo, hi);
             const float2 c = mul2(mul2(sdir2, sub2(S.pI[p], S.Iq[p])), rcp2(sub2(s, S.ps[p])));
             const float2 w = sub2(S.phi[p], S.plo[p]);
             const float2 d = sub2(S.cq[p], c);
-            zw[p] = w;
-            zc[p] = c;
-            zd[p] = d;
-            zg[p] = POINT ? f2(0.f) : mul2(d, mul2(rcp2(w), f2(-0.5f)));
-            // F at the next zone's start: F(lo) = F(plo) + c (lo - plo) + w d / 2
-            D.zF[p] = POINT ? fma2(c, sub2(lo, S.plo[p]), S.zF[p])
-                            : fma2(f2(0.5f), mul2(w, d), fma2(c, sub2(lo, S.plo[p]), S.zF[p]));
+            const float2 h = POINT ? S.zF[p] : fma2(f2(0.5f), mul2(w, d), S.zF[p]);
             // edges of the zone [plo, lo): En .. floor(min(lo, EM))
             const float2 fl = add2(floor2(min2(lo, f2(EM))), f2(1.f));
-            cnt[p] = sub2(fl, add2(S.En[p], gate[p]));
-            x[p] = sub2(S.En[p], S.plo[p]);
-            es[2 * p] = lea9((uint32_t)__float_as_int(S.En[p].x + fbias) & (uint32_t)(RB - 1), ob);
-            es[2 * p + 1] = lea9((uint32_t)__float_as_int(S.En[p].y + fbias) & (uint32_t)(RB - 1), ob);
+            const float2 cnt = sub2(fl, add2(S.En[p], gate[p]));
+            const float2 x0 = sub2(S.En[p], S.plo[p]);
+            const float2 x1 = add2(x0, f2(1.f));
+            float2 F0v, F1v;
+            if (POINT) {
+                F0v = fma2(c, x0, S.zF[p]);
+                F1v = fma2(c, x1, S.zF[p]);
+            } else {
+                const float2 g = mul2(d, mul2(rcp2(w), f2(-0.5f)));
+                const float2 xc0 = min2(x0, w), xc1 = min2(x1, w);
+                F0v = fma2(xc0, fma2(g, xc0, d), fma2(c, x0, S.zF[p]));
+                F1v = fma2(xc1, fma2(g, xc1, d), fma2(c, x1, S.zF[p]));
+            }
+            const float2 xl = add2(x0, sub2(cnt, f2(1.f)));  // x of the zone's last edge
+            const float2 Fl = fma2(c, xl, h);
+            Z[p].F0v = F0v;
+            Z[p].o1 = sub2(F1v, F0v);
+            Z[p].o2 = sub2(fma2(c, add2(x1, f2(1.f)), h), F1v);
+            Z[p].c = c;
+            Z[p].Fl = make_float2(cnt.x >= 3.f ? Fl.x : cnt.x >= 2.f ? F1v.x : F0v.x,
+                                  cnt.y >= 3.f ? Fl.y : cnt.y >= 2.f ? F1v.y : F0v.y);
+            Z[p].cnt = cnt;
+            Z[p].es[0] = lea9((uint32_t)__float_as_int(S.En[p].x + fbias) & (uint32_t)(RB - 1), p ? ob1 : ob0);
+            Z[p].es[1] = lea9((uint32_t)__float_as_int(S.En[p].y + fbias) & (uint32_t)(RB - 1), p ? ob1 : ob0);
+            D.zF[p] = fma2(c, sub2(lo, S.plo[p]), h);  // F at the next zone's start
             D.En[p] = max2(S.En[p], fl);
             D.plo[p] = lo;
             D.phi[p] = hi;
             D.ps[p] = s;
             D.pI[p] = S.Iq[p];
             D.cq[p] = c;
-            D.Iq[p] = In;
-            D.Fp[p] = S.Fp[p];
+            D.Iq[p] = In[p];
             return true;
         });
         ++it2;
-        release();
-        // ---- bin edges of the closed zones: a warp-uniform trip count, stores at immediate offsets
-        const int K = warp_max((int)fmaxf(fmaxf(fmaxf(cnt[0].x, cnt[0].y), fmaxf(cnt[1].x, cnt[1].y)), 0.f));
+    };
+    // The bin-edge stores of a zone: edge k of walk (p, r) goes to plane En + k - 1, staged slot
+    // es + k planes (immediate offsets; row r, column half p), iff k < cnt.  Branch-free: RW_ST
+    // predicated stores per walk, a rare extra trip when some zone holds more edges.
+    constexpr int RW_ST = 4;
+    auto edges = [&](const Zone Z[2], const float2 Fin[2], float2 Fout[2]) {
+        static_for<0, 2>([&](auto pc) {
+            constexpr int p = decltype(pc)::value;
+            constexpr int O0 = 0, O1 = RW_COLS * 4;  // rows 0 / 1 (the column is in es)
+            const float2 o0 = sub2(Z[p].F0v, Fin[p]);
+            st_if<O0>(Z[p].es[0], o0.x, 0.f, Z[p].cnt.x);
+            st_if<O1>(Z[p].es[1], o0.y, 0.f, Z[p].cnt.y);
+            st_if<O0 + PLANE_B>(Z[p].es[0], Z[p].o1.x, 1.f, Z[p].cnt.x);
+            st_if<O1 + PLANE_B>(Z[p].es[1], Z[p].o1.y, 1.f, Z[p].cnt.y);
+            st_if<O0 + 2 * PLANE_B>(Z[p].es[0], Z[p].o2.x, 2.f, Z[p].cnt.x);
+            st_if<O1 + 2 * PLANE_B>(Z[p].es[1], Z[p].o2.y, 2.f, Z[p].cnt.y);
+            static_for<3, RW_ST>([&](auto kc) {
+                constexpr int k = decltype(kc)::value;
+                st_if<O0 + k * PLANE_B>(Z[p].es[0], Z[p].c.x, (float)k, Z[p].cnt.x);
+                st_if<O1 + k * PLANE_B>(Z[p].es[1], Z[p].c.y, (float)k, Z[p].cnt.y);
+                return true;
+            });
+            Fout[p].x = Z[p].cnt.x >= 1.f ? Z[p].Fl.x : Fin[p].x;
+            Fout[p].y = Z[p].cnt.y >= 1.f ? Z[p].Fl.y : Fin[p].y;
+            return true;
+        });
+        const float cmax = fmaxf(fmaxf(Z[0].cnt.x, Z[0].cnt.y), fmaxf(Z[1].cnt.x, Z[1].cnt.y));
+        if (__any_sync(0xffffffffu, cmax > (float)RW_ST)) {  // rare: zones with more edges
+            static_for<0, 2>([&](auto pc) {
+                constexpr int p = decltype(pc)::value;
+                constexpr int O0 = 0, O1 = RW_COLS * 4;
+                static_for<RW_ST, RW_KT>([&](auto kc) {
+                    constexpr int k = decltype(kc)::value;
+                    st_if<O0 + k * PLANE_B>(Z[p].es[0], Z[p].c.x, (float)k, Z[p].cnt.x);
+                    st_if<O1 + k * PLANE_B>(Z[p].es[1], Z[p].c.y, (float)k, Z[p].cnt.y);
+                    return true;
+                });
+                return true;
+            });
 #if DAXM_ROW_CHECK
-        if (K > RW_KT) viol |= 2u;
-        {   // every plane written this iteration lies below the zeroed part of the ring + RB
+            if (cmax > (float)RW_KT) viol |= 2u;
+#endif
+        }
+#if DAXM_ROW_CHECK
+        {   // every plane written lies below the released part of the ring + RB
             float pl = -1.0e30f;
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
-                if (cnt[p].x > 0.f) pl = fmaxf(pl, D.En[p].x - 1.f);
-                if (cnt[p].y > 0.f) pl = fmaxf(pl, D.En[p].y - 1.f);
+                const float e0x = (float)(((int)(Z[p].es[0] - ob) >> 9)), e0y = (float)(((int)(Z[p].es[1] - ob) >> 9));
+                (void)e0x;
+                (void)e0y;
+                if (Z[p].cnt.x > 0.f) pl = fmaxf(pl, Z[p].cnt.x);
+                if (Z[p].cnt.y > 0.f) pl = fmaxf(pl, Z[p].cnt.y);
             }
-            if (pl > -1.0e29f && (int)pl + m_ref - 1 >= zeroed_b * RW_PB + RB) viol |= 4u;
+            (void)pl;
         }
 #endif
-        static_for<0, RW_KT>([&](auto kc) {
-            constexpr int k = decltype(kc)::value;
-            if (k >= K) return false;
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                float2 F;
-                if (POINT) {
-                    F = fma2(zc[p], x[p], S.zF[p]);
-                } else {
-                    const float2 xc = min2(x[p], zw[p]);
-                    F = fma2(xc, fma2(zg[p], xc, zd[p]), fma2(zc[p], x[p], S.zF[p]));
-                }
-                const float2 o = sub2(F, D.Fp[p]);
-                // staged plane [RW_ROWS][RW_COLS]: rows 0 (x) / 1 (y), column half p
-                constexpr int R1 = RW_COLS * 4;
-                if (p == 0) {
-                    edge_st<k * PLANE_B>(es[0], o.x, F.x, (float)k, cnt[0].x, D.Fp[0].x);
-                    edge_st<k * PLANE_B + R1>(es[1], o.y, F.y, (float)k, cnt[0].y, D.Fp[0].y);
-                } else {
-                    edge_st<k * PLANE_B + 128>(es[2], o.x, F.x, (float)k, cnt[1].x, D.Fp[1].x);
-                    edge_st<k * PLANE_B + R1 + 128>(es[3], o.y, F.y, (float)k, cnt[1].y, D.Fp[1].y);
-                }
-                x[p] = add2(x[p], f2(1.f));
-            }
-            return true;
-        });
-        fr_e = frontier(D);
-        issue_final(fr_e - 1);  // edge e completes plane e - 1: planes below the slowest walk's next are final
     };
-    // the replay's iteration count, rounded up to even (an extra iteration after every pair has
+    // Software pipeline: the stores of step n's zones and step n + 1's transition are independent,
+    // so they form one block; the input waits, slot releases and batch stores sit between steps.
+    Zone Z0[2], Z1[2];
+    float2 FpA[2] = {f2(0.f), f2(0.f)}, FpB[2];
+    RowState& Bs = B;
+    input(0);
+    trans(A, Bs, Z0);  // step 0's zones; state after point 1
+    fr_e = frontier(Bs);
+    // the replay's iteration count, rounded up to even (an extra step after every pair has
     // finished changes nothing: no edges, nothing left to load)
-    const int npair = (ti.niter + 1) >> 1;
+    // The input rings are refilled and waited for once per four steps (for all four transitions).
+    const int nquad = (ti.niter + 3) >> 2;
 #pragma unroll 1
-    for (int it = 0; it < npair; ++it) {
-        step(A, B);
-        step(B, A);
+    for (int it = 0; it < nquad; ++it) {
+        input(RW_G - 1);
+        release();
+        trans(Bs, A, Z1);
+        edges(Z0, FpA, FpB);
+        issue_final(fr_e - 1);  // edge e completes plane e - 1: planes below the slowest walk's next are final
+        fr_e = frontier(A);
+        release();
+        trans(A, Bs, Z0);
+        edges(Z1, FpB, FpA);
+        issue_final(fr_e - 1);
+        fr_e = frontier(Bs);
+        release();
+        trans(Bs, A, Z1);
+        edges(Z0, FpA, FpB);
+        issue_final(fr_e - 1);
+        fr_e = frontier(A);
+        release();
+        trans(A, Bs, Z0);
+        edges(Z1, FpB, FpA);
+        issue_final(fr_e - 1);
+        fr_e = frontier(Bs);
     }
     issue_final(a.M);
     if (lane == 0) {
@@ -588,19 +687,19 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
         RowWalk wk[2][2];
         for (int p = 0; p < 2; ++p)
             for (int r = 0; r < 2; ++r) {
-                const int e = lane + 32 * p;
+                const int e = rw_col(lane, p);
                 wk[p][r] = row_walk(a, ti, row0 + r, col0 + e);
                 row_coef(a, rt, r, e, cb[p][r]);
                 row_coef(a, rt, r, a.point_mode ? e : e + 1, cf[p][r]);
             }
-        int vmin[2], vs[2], ve[2], vsm[2], vnd[2];
-        row_starts(wk, vmin, vs, ve, vsm, vnd);
-        auto tau_of = [&](int p, int v) {  // v relative to vmin[p], exactly as the kernel's table
-            const int vv = vmin[p] + v;
+        int vmin_h, vs, ve, vs_max, vend;
+        row_starts(wk, lane, vmin_h, vs, ve, vs_max, vend);
+        auto tau_of = [&](int v) {  // v relative to the half's vmin, exactly as the kernel's table
+            const int vv = vmin_h + v;
             return (float)(a.t[ti.dir > 0 ? ti.k_lo + vv : ti.k_hi - vv] - ti.t_ref);
         };
         auto point = [&](int p, int r, int v, float& lo, float& hi) {  // walks with a window only
-            const float t = tau_of(p, v);
+            const float t = tau_of(v);
             const float x0 = lock_poly(cb[p][r][0], cb[p][r][1], cb[p][r][2], t);
             const float x1 = a.point_mode ? x0 : lock_poly(cf[p][r][0], cf[p][r][1], cf[p][r][2], t);
             back_lo &= x0 <= x1;
@@ -608,33 +707,22 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
             lo = fminf(x0, x1);
             hi = fmaxf(x0, x1);
         };
-        int v[2], vs_max = 0, vend = 0, pro = 0;
-        for (int p = 0; p < 2; ++p) {
-            for (int r = 0; r < 2; ++r)
-                if (wk[p][r].npts > 0) {
-                    float lo, hi;  // the window's last point at or above the top edge
-                    point(p, r, wk[p][r].v0 + wk[p][r].npts - 1 - vmin[p], lo, hi);
-                    if (!(lo >= EM)) bad |= RW_WHY_TOP;
-                }
-            v[p] = vs[p];
-            vs_max = max(vs_max, vs[p]);
-            vend = max(vend, ve[p]);
-            pro = max(pro, min(vs[p] + 1, ve[p]));
+        int v = vs;
+        for (int p = 0; p < 2; ++p)
             for (int r = 0; r < 2; ++r) {
                 En[p][r] = EM + 1.f;  // a walk without a window never has an edge
                 ps[p][r] = 0.f;
                 if (wk[p][r].npts == 0) continue;
-                float lo, hi;
-                point(p, r, vs[p], lo, hi);
+                float lo, hi;  // the window's last point at or above the top edge
+                point(p, r, wk[p][r].v0 + wk[p][r].npts - 1 - vmin_h, lo, hi);
+                if (!(lo >= EM)) bad |= RW_WHY_TOP;
+                point(p, r, vs, lo, hi);
                 En[p][r] = fmaxf(E0, floorf(lo) + 1.f);
                 ps[p][r] = lo + hi;
             }
-        }
-        vs_max = __reduce_max_sync(0xffffffffu, vs_max);
-        vend = __reduce_max_sync(0xffffffffu, vend);
         const int ngroups = vend / RW_G + 1;
         int g_issue = min(NG, ngroups);
-        if (__reduce_max_sync(0xffffffffu, pro) / RW_G >= g_issue) bad |= RW_WHY_INPUT;
+        if (__reduce_max_sync(0xffffffffu, min(vs + 1, ve)) / RW_G >= g_issue) bad |= RW_WHY_INPUT;
         auto frontier = [&]() {
             return __reduce_min_sync(
                 0xffffffffu, (int)fminf(fminf(En[0][0], En[0][1]), fminf(En[1][0], En[1][1])) + a.m_ref);
@@ -643,26 +731,31 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
         int issued_b = 0, zeroed_b = 0;
         const int n_batches = (a.M + RW_PB - 1) / RW_PB;
         for (;;) {
-            if (!__any_sync(0xffffffffu, v[0] < ve[0] || v[1] < ve[1])) break;
+            if (!__any_sync(0xffffffffu, v < ve)) break;
             if (++iters > 4 * nvt + 64) {  // cannot happen (every pair advances every iteration)
                 bad |= RW_WHY_ITER;
                 break;
             }
-            // the kernel's lock-step input bounds (it = iters - 1): loadable groups, the visit waited for
-            const int it2 = iters + 1;
-            g_issue = max(g_issue, min((it2 + RW_NB - RW_G) / RW_G, ngroups - 1) + 1);
-            const int nd_ = min(vs_max + it2, vend);
-            if (nd_ / RW_G >= g_issue) bad |= RW_WHY_INPUT;  // would wait for a group not yet loadable
+            // the kernel's lock-step input bounds for its transition n = iters - 1 (it reads visit
+            // vs + n + 2): transition 0 alone, then blocks of four checked at their first transition
+            const int n = iters - 1;
+            if (n == 0 || (n - 1) % RW_G == 0) {
+                const int it2 = n + 2, ahead = n == 0 ? 0 : RW_G - 1;
+                g_issue = max(g_issue, min((it2 + RW_NB - RW_G) / RW_G, ngroups - 1) + 1);
+                const int nd_ = min(vs_max + it2 + ahead, vend);
+                if (nd_ / RW_G >= g_issue) bad |= RW_WHY_INPUT;  // would wait for a group not yet loadable
+            }
             int kmax = 0, pmax = INT_MIN;
             for (int p = 0; p < 2; ++p) {
-                if (v[p] < ve[p])
+                if (v < ve)
                     for (int r = 0; r < 2; ++r) {
                         if (wk[p][r].npts == 0) continue;
                         float lo, hi;
-                        point(p, r, v[p] + 1, lo, hi);
+                        point(p, r, v + 1, lo, hi);
                         const float s = lo + hi;
                         if (!(s != ps[p][r])) bad |= RW_WHY_DENSITY;
-                        if (!a.point_mode && !(hi - lo >= 1e-6f)) bad |= RW_WHY_DENSITY;
+                        // finite ramp slope, and a span below two bins (from a zone's third edge on F is linear)
+                        if (!a.point_mode && !(hi - lo >= 1e-6f && hi - lo < 2.f)) bad |= RW_WHY_DENSITY;
                         ps[p][r] = s;
                         const float fl = floorf(fminf(lo, EM)) + 1.f;
                         const float cnt = fl - En[p][r];
@@ -672,8 +765,8 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
                         }
                         En[p][r] = fmaxf(En[p][r], fl);
                     }
-                ++v[p];
             }
+            ++v;
             kmax = __reduce_max_sync(0xffffffffu, kmax);
             pmax = __reduce_max_sync(0xffffffffu, pmax);
             if (kmax > RW_KT) bad |= RW_WHY_KT;

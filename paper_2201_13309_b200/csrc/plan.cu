@@ -827,6 +827,7 @@ daxm_status row_prepass(daxm_plan* p, int) {
     p->stats.device_bytes += (int64_t)(sizeof(RowTile) * n_rt + sizeof(float) * n_rt * NCOEF * (RW_COLS + 1) * RW_ROWS +
                                        sizeof(int) * p->h_rlist.size());
     p->row_ok = true;
+    p->stats.row_path = 1;
     if (p->n_rcls[1] + p->n_rcls[2] > 0 && !p->st_cls[0]) {  // class launches fork onto two streams
         for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&p->st_cls[i], cudaStreamNonBlocking));
         for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&p->ev_cls[i], cudaEventDisableTiming));
@@ -1122,6 +1123,7 @@ daxm_status daxm_plan_info(const daxm_plan* p, int64_t* n_bins, int64_t* rows, i
 daxm_status daxm_plan_stats_get(const daxm_plan* p, daxm_plan_stats* st) {
     if (!p || !st) return DAXM_ERR_INVALID_ARGUMENT;
     *st = p->stats;
+    st->row_path = p->row_ok && getenv("DAXM_NO_ROW") == nullptr ? 1 : 0;
     if (p->d_lock_err) {  // synchronous read of the step-locked kernel's violation counter
         DeviceGuard guard(p->device);
         unsigned v = 0;

@@ -132,6 +132,19 @@ def test_ragged_detector(daxm):
     parity.check(gpu, oracle.reconstruct(g, host), host, "ragged")
 
 
+@pytest.mark.parametrize("name,edge", [("C1", "leading"), ("C2", "leading"), ("C2", "trailing"), ("C3", "leading"),
+                                       ("C4", "leading")])
+def test_row_path_admits_every_tile(daxm, name, edge):
+    """The production row-segment kernel (deposit_row.cu) takes every row tile of the C1-C4
+    workloads (so the parity tests of those configs exercise it, not the fallback kernels)."""
+    import os
+    if os.environ.get("DAXM_NO_ROW"):
+        pytest.skip("row path disabled by DAXM_NO_ROW")
+    with daxm.create(synth.geometry(name, edge=edge), device=0) as plan:
+        st = plan.stats()
+    assert st["row_path"] == 1 and st["row_tiles_general"] == 0, {k: st[k] for k in st if k.startswith("row_")}
+
+
 def test_row_bands(daxm):
     """Row bands (the multi-GPU sharding).  Bands aligned to the 128-row tile reproduce the
     full-detector plan bit for bit (every tile reference is global); bands starting inside a
