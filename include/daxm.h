@@ -152,7 +152,12 @@ daxm_status daxm_plan_stats_get(const daxm_plan *p, daxm_plan_stats *st);
  * default stream).  Asynchronous; no allocation; graph-capturable.  Caller
  * owns both buffers; they must stay valid until the stream reaches the work.
  * Errors: INVALID_ARGUMENT (NULL pointers, misalignment, unknown dtype), CUDA
- * (launch failure; detail in daxm_last_error). */
+ * (launch failure; detail in daxm_last_error).
+ * Concurrency: at most ONE call on a plan may be in flight at a time.  Calls issued on one stream
+ * are ordered by it; calls on different streams (or a captured graph replayed beside eager calls)
+ * must be ordered by the caller, because the plan owns scratch they share (cutoff liveness flags,
+ * the class-launch fork streams and events, the host-path buffers).  Use one plan per concurrent
+ * stream.  A plan is not thread-safe: serialise calls from several host threads. */
 daxm_status daxm_reconstruct(daxm_plan *p, const void *d_stack, daxm_dtype dt, float *d_out, void *cuda_stream);
 
 /* daxm_reconstruct_host -- end-to-end path from HOST memory: copies h_stack

@@ -12,7 +12,10 @@ Parity status of each exported function:
   oracle_reconstruct[_pixels]                  pinned (conservation, background, linearity,
                                                reversal identity, forward-model round trip)
   select_cutoff, active_pixels (python)        pinned (order-statistic definition, tests/test_oracle_cutoff.py)
-  depth_profile (python)                       pinned (conservation: sum of the profile = sum of dI)
+  depth_profile (python)                       pinned (conservation: the profile's total = sum_p s (I_0 - I_{S-1})
+                                               when every trapezoid lies inside the bins; a single non-constant
+                                               pixel's profile = its oracle_reconstruct_pixels column;
+                                               tests/test_oracle_cutoff.py)
 """
 from __future__ import annotations
 

@@ -129,6 +129,10 @@ class Plan:
         M, R, Cc = C.c_int64(), C.c_int64(), C.c_int64()
         lib().daxm_plan_info(self._h, C.byref(M), C.byref(R), C.byref(Cc))
         self.n_bins, self.rows, self.cols = M.value, R.value, Cc.value
+        self.n_steps = self.stats()["n_steps"]
+
+    def stack_shape(self):
+        return (self.n_steps, self.rows, self.cols)
 
     def _check(self, st: int):
         if st != 0:
@@ -150,19 +154,30 @@ class Plan:
         if out is None:
             out = torch.empty(self.output_shape(), dtype=torch.float32, device=stack.device)
         if not (out.is_cuda and out.is_contiguous() and out.dtype == torch.float32 and
-                tuple(out.shape) == self.output_shape()):
-            raise ValueError("out must be a contiguous float32 CUDA tensor of shape [M][rows][C]")
+                tuple(out.shape) == self.output_shape() and out.device == stack.device):
+            raise ValueError("out must be a contiguous float32 CUDA tensor of shape [M][rows][C] on the "
+                             "stack's device")
         if stream is None:
             stream = torch.cuda.current_stream(stack.device)
         self._check(lib().daxm_reconstruct(self._h, C.c_void_p(stack.data_ptr()), dt, C.c_void_p(out.data_ptr()),
                                            C.c_void_p(stream.cuda_stream)))
         return out
 
-    @staticmethod
-    def _dtype_of(stack):
+    def _dtype_of(self, stack, plane0_only=False):
+        """Validate a device stack (shape [S][rows][C] -- or at least its first plane --, contiguous,
+        on the plan's device) and return its daxm_dtype."""
         import torch
         if not (stack.is_cuda and stack.is_contiguous()):
             raise ValueError("stack must be a contiguous CUDA tensor")
+        if stack.device.index != self.device:
+            raise ValueError(f"stack is on {stack.device}, the plan on cuda:{self.device}")
+        shape = tuple(stack.shape)
+        if plane0_only:
+            ok = len(shape) == 3 and shape[1:] == self.stack_shape()[1:] and shape[0] >= 1
+        else:
+            ok = shape == self.stack_shape()
+        if not ok:
+            raise ValueError(f"stack shape {shape}, the plan needs {self.stack_shape()} [S][rows][C]")
         dt = {torch.uint16: 0, torch.float32: 1}.get(stack.dtype)
         if dt is None:
             raise ValueError(f"unsupported stack dtype {stack.dtype}")
@@ -176,7 +191,7 @@ class Plan:
     def select_cutoff(self, stack, fraction, stream=None):
         """The cutoff keeping `fraction` of the plan's pixels (k-th largest first-step intensity)."""
         import torch
-        dt = self._dtype_of(stack)
+        dt = self._dtype_of(stack, plane0_only=True)
         if stream is None:
             stream = torch.cuda.current_stream(stack.device)
         val = C.c_double()
@@ -206,8 +221,17 @@ class Plan:
         dt = {torch.uint16: 0, torch.float32: 1}.get(stack.dtype)
         if dt is None or stack.is_cuda or not stack.is_contiguous():
             raise ValueError("stack must be a contiguous host uint16/float32 tensor or array")
+        if tuple(stack.shape) != self.stack_shape():
+            raise ValueError(f"stack shape {tuple(stack.shape)}, the plan needs {self.stack_shape()} [S][rows][C]")
         if out is None:
             out = torch.empty(self.output_shape(), dtype=torch.float32, pin_memory=stack.is_pinned())
+        elif isinstance(out, np.ndarray):
+            if not (out.dtype == np.float32 and out.flags.c_contiguous and out.shape == self.output_shape()):
+                raise ValueError("out must be a C-contiguous float32 array of shape [M][rows][C]")
+            out = torch.from_numpy(out)
+        elif not (not out.is_cuda and out.is_contiguous() and out.dtype == torch.float32 and
+                  tuple(out.shape) == self.output_shape()):
+            raise ValueError("out must be a contiguous float32 host tensor of shape [M][rows][C]")
         st = 0 if stream is None else stream.cuda_stream
         self._check(lib().daxm_reconstruct_host(self._h, C.c_void_p(stack.data_ptr()), dt,
                                                 C.c_void_p(out.data_ptr()), C.c_void_p(st)))

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "daxm.h"
 
 namespace daxm {
@@ -239,6 +241,21 @@ struct RowArgs {
 // pre-pass ring check and the step-locked kernel evaluate exactly this expression.
 __device__ __forceinline__ float lock_poly(float c0, float c1, float c2, float t) {
     return fmaf(fmaf(c2, t, c1), t, c0);
+}
+
+// One-time per DEVICE setup of a kernel's function attributes (cudaFuncSetAttribute acts on the
+// current device): `done` holds one bit per device ordinal already set up.  Idempotent, so two
+// threads racing on the same device both set the same attributes harmlessly.
+template <typename F>
+inline cudaError_t once_per_device(std::atomic<unsigned long long>& done, F&& set) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const unsigned long long bit = dev < 64 ? 1ull << dev : 0ull;
+    if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+    if ((e = set()) != cudaSuccess) return e;
+    done.fetch_or(bit, std::memory_order_acq_rel);
+    return cudaSuccess;
 }
 
 // Launchers (deposit.cu, profile.cu, select.cu).

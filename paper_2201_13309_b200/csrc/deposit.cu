@@ -745,17 +745,16 @@ template <typename T, int NB, bool POINT, int MODE>
 cudaError_t launch_fast(const CUtensorMap* in_map, const CUtensorMap* out_map, const DepositArgs& a, int n_tiles,
                         cudaStream_t st) {
     const size_t sm = FastSmem<T, NB>::bytes(a.max_nv);
-    static bool attr_set = false;  // per template instance
-    if (!attr_set) {
+    static std::atomic<unsigned long long> attr_done{0};  // per template instance and device
+    cudaError_t ea = once_per_device(attr_done, []() {
         cudaError_t e = cudaFuncSetAttribute(deposit_fast<T, NB, POINT, MODE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)FastSmem<T, NB>::bytes(MAX_FAST_NV));
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(deposit_fast<T, NB, POINT, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 (int)cudaSharedmemCarveoutMaxShared);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+        return cudaFuncSetAttribute(deposit_fast<T, NB, POINT, MODE>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    (int)cudaSharedmemCarveoutMaxShared);
+    });
+    if (ea != cudaSuccess) return ea;
     if (sm > FastSmem<T, NB>::bytes(MAX_FAST_NV)) return cudaErrorInvalidValue;
     deposit_fast<T, NB, POINT, MODE><<<n_tiles, FAST_THREADS, sm, st>>>(*in_map, *out_map, a);
     return cudaGetLastError();

@@ -924,16 +924,15 @@ template <typename T, bool POINT, int RB, bool OV>
 cudaError_t launch_lock_rb(const CUtensorMap* in_map, float* out, const DepositArgs& a, int n_tiles, cudaStream_t st) {
     const size_t sm = LockSmem<T, RB>::bytes(a.max_nv);
     auto kern = OV ? deposit_lock_ov<T, POINT, RB> : deposit_lock<T, POINT, RB>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<unsigned long long> attr_done{0};  // per device (attributes are per device)
+    cudaError_t ea = once_per_device(attr_done, [&]() {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)LockSmem<T, RB>::bytes(MAX_FAST_NV));
         if (e != cudaSuccess) return e;
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                 (int)cudaSharedmemCarveoutMaxShared);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+        return cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    (int)cudaSharedmemCarveoutMaxShared);
+    });
+    if (ea != cudaSuccess) return ea;
     kern<<<(unsigned)(n_tiles * LOCK_SUBS), LK_THREADS, sm, st>>>(*in_map, out, a);
     return cudaGetLastError();
 }

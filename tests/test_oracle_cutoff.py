@@ -51,12 +51,56 @@ def test_cutoff_reconstruct_masks_pixels():
     assert np.array_equal(oracle.reconstruct_cutoff(g, stack, float(stack[0].min())), full)
 
 
-def test_depth_profile_conserves_intensity():
+def _inside_step_stack(g, rng):
+    """[S][R][C] stack whose intensity changes only at step pairs whose trapezoid lies inside the
+    bin range (exact depths from the independent helper tests/indep.py)."""
+    import indep
+    S, R, Cc = len(g["wire_xyz"]), g["n_rows"], g["n_cols"]
+    lo0 = g["depth_start"] - g["depth_res"] / 2
+    hi = g["depth_end"] + g["depth_res"] / 2
+    W = g["wire_xyz"]
+    d = W[-1] - W[0]
+    stack = np.empty((S, R, Cc))
+    for j in range(R):
+        for i in range(Cc):
+            D = np.array([indep.edge_depth_vec(np.repeat(indep.detector_xyz(g, x, j)[None], S, 0), W,
+                                               g["wire_axis"], g["wire_radius"], d, g["edge"])
+                          for x in (i - 0.5, i + 0.5)])
+            lo_c = np.minimum(D[:, :-1].min(0), D[:, 1:].min(0))
+            hi_c = np.maximum(D[:, :-1].max(0), D[:, 1:].max(0))
+            inside = (lo_c > lo0) & (hi_c < hi)
+            steps = np.where(inside, rng.integers(-300, 300, inside.size), 0)
+            stack[:, j, i] = 4000.0 + np.concatenate([[0.0], -np.cumsum(steps)])
+    return stack
+
+
+@pytest.mark.parametrize("edge", ["leading", "trailing"])
+def test_depth_profile_conservation(edge):
+    """image_set.depth_intensity: when every trapezoid lies inside the bins, the profile's
+    total is the total intensity change sum_p s (I_0(p) - I_{S-1}(p)) (SURVEY §8(c) conservation,
+    summed over the detector); a profile summed over the wrong axis or missing pixels fails it."""
+    g = synth.geometry("C1", edge=edge)
+    g["n_rows"] = g["n_cols"] = 16  # a 16 x 16 corner of the C1 detector geometry
+    g["pitch_col"] = g["pitch_row"] = synth.geometry("C1")["pitch_col"]
+    rng = np.random.default_rng(31)
+    stack = _inside_step_stack(g, rng)
+    prof = oracle.depth_profile(oracle.reconstruct(g, stack))
+    assert prof.shape == (oracle.Geometry(g).n_bins,)
+    s = 1.0 if edge == "leading" else -1.0
+    want = s * (stack[0] - stack[-1]).sum()
+    assert abs(want) > 100.0
+    assert np.isclose(prof.sum(), want, rtol=1e-12, atol=1e-7)
+
+
+def test_depth_profile_single_pixel_is_its_depth_column():
+    """With one non-constant pixel the profile is that pixel's reconstruction, computed here by the
+    independent per-pixel entry point (oracle_reconstruct_pixels)."""
     g = synth.geometry("C1")
-    stack = synth.stack_numpy(synth.make_maps("C1"), "f32", noise=False)
-    out = oracle.reconstruct(g, stack)
-    prof = oracle.depth_profile(out)
-    assert prof.shape == (out.shape[0],)
-    # all depth-resolved intensity is deposited: profile total = sum of the deposited pixel totals
-    assert np.isclose(prof.sum(), out.sum(), rtol=1e-12)
-    assert np.allclose(prof, [out[m].sum() for m in range(out.shape[0])], rtol=1e-12)
+    stack = np.full((len(g["wire_xyz"]), g["n_rows"], g["n_cols"]), 1000.0)
+    rng = np.random.default_rng(5)
+    j, i = 37, 22
+    stack[:, j, i] += rng.integers(0, 500, stack.shape[0])
+    prof = oracle.depth_profile(oracle.reconstruct(g, stack))
+    col = oracle.reconstruct_pixels(g, [j], [i], stack[:, j, i][None])[0]
+    assert np.abs(col).max() > 1.0
+    assert np.allclose(prof, col, rtol=1e-12, atol=1e-9)
