@@ -209,7 +209,12 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=3.0)
-    ap.add_argument("--all-gather", action="store_true", help="also time an NCCL all-gather of the output planes")
+    ap.add_argument("--all-gather", action="store_true", help="also time an all-gather of the output planes")
+    ap.add_argument("--check-gather", action="store_true",
+                    help="(N>1) rank 0 compares the gathered image set bit for bit with a single-plan run of "
+                         "the whole detector on its own GPU")
+    ap.add_argument("--backend", choices=["nccl", "gloo"], default="nccl",
+                    help="torch.distributed backend for N>1 (gloo lets several ranks share one GPU)")
     ap.add_argument("--dtype", choices=["u16", "f32"], default=None,
                     help="override the config's stack dtype (e.g. C5 in fp32, SURVEY §8(d))")
     ap.add_argument("--fraction", type=float, default=1.0,
@@ -233,10 +238,17 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    n_dev = torch.cuda.device_count()
+    if world > n_dev and args.backend == "nccl":
+        raise SystemExit(f"{world} ranks on {n_dev} GPU(s): NCCL needs one GPU per rank (use --backend gloo)")
+    local = local % max(n_dev, 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     cfg = synth.get_config(args.config)
     if args.dtype:
@@ -293,16 +305,15 @@ def main():
     alg_bytes = active * (st["contrib_pairs"] + st["contrib_pixels"]) * b_in + st["rows"] * st["cols"] * st["n_bins"] * 4
     achieved = alg_bytes / (kern_avg * 1e-3) / 1e9
     ms_step = total_ms / K
-    stats = torch.tensor([ms_step, kern_avg, -achieved], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
-    ms_step_max, kern_max, achieved_min = stats[0].item(), stats[1].item(), -stats[2].item()
+    ms_step_max, kern_max, achieved_min = multi.max_over_ranks([ms_step, kern_avg, -achieved], device=dev)
+    achieved_min = -achieved_min
     units = R * cfg.n * cfg.n_steps
     value = units / (ms_step_max * 1e-3)
 
     # optional all-gather of the output planes (timed separately, not in value)
     allgather_ms = None
-    if args.all_gather and world > 1:
+    gather_check = None
+    if (args.all_gather or args.check_gather) and world > 1:
         bands = multi.row_bands(world, R)
         full = multi.gather_rows(out, bands)  # warm
         del full
@@ -314,15 +325,18 @@ def main():
         b.record(stream)
         torch.cuda.synchronize(dev)
         allgather_ms = multi.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
+        if args.check_gather and rank == 0:
+            gather_check = check_gather(daxm, g, full, maps, cfg, noise, dev, stream, cutoff)
         del full
         torch.cuda.empty_cache()
+        dist.barrier()
 
     # end to end through the C ABI from pinned host buffers (copies inside the timed region)
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(3, K // 4)
     if e2e_steps <= 0:
         return finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_max, achieved_min, value,
                       units, st, clocks, r0, r1, alg_bytes, allgather_ms, None, (cutoff, active), out,
-                      kern_median)
+                      kern_median, gather_check)
     h_stack = stack.cpu().pin_memory()
     h_out = torch.empty(plan.output_shape(), dtype=torch.float32).pin_memory()
     del stack
@@ -337,18 +351,17 @@ def main():
         plan.reconstruct_host(h_stack, h_out, stream)
     e_b.record(stream)
     torch.cuda.synchronize(dev)
-    e2e_ms = torch.tensor([e_a.elapsed_time(e_b) / e2e_steps], dtype=torch.float64, device=dev)
     if world > 1:
         dist.barrier()
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = units / (e2e_ms.item() * 1e-3)
+    e2e_ms = multi.max_over_ranks([e_a.elapsed_time(e_b) / e2e_steps], device=dev)[0]
+    e2e_value = units / (e2e_ms * 1e-3)
     h2d = h_stack.numel() * h_stack.element_size() * world
     d2h = h_out.numel() * h_out.element_size() * world
     e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "ms_per_step": e2e_ms.item(), "path": "daxm_reconstruct_host, pinned host buffers"}
+           "ms_per_step": e2e_ms, "path": "daxm_reconstruct_host, pinned host buffers"}
     return finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_max, achieved_min, value,
                   units, st, clocks, r0, r1, alg_bytes, allgather_ms, e2e, (cutoff, active), out,
-                  kern_median)
+                  kern_median, gather_check)
 
 
 def launches_per_step(st, dtype, cutoff=False):
@@ -366,28 +379,61 @@ def launches_per_step(st, dtype, cutoff=False):
     return int(n) + (2 if cutoff else 0)
 
 
+def check_gather(daxm, g, full, maps, cfg, noise, dev, stream, cutoff):
+    """--check-gather: the all-gathered image set vs one plan over the whole detector on this
+    GPU (same kernels, same tiles: the row bands are tile aligned), compared bit for bit."""
+    import torch
+
+    import synth
+    stack = synth.stack_torch(maps, cfg.dtype, dev, noise=noise)
+    with daxm.create(g, device=dev.index) as plan:
+        if cutoff is not None:
+            plan.set_cutoff(cutoff)
+        ref = plan.reconstruct(stack, None, stream)
+        torch.cuda.synchronize(dev)
+    del stack
+    same = bool(torch.equal(ref.view(torch.int32), full.view(torch.int32)))
+    n_diff = int((ref.view(torch.int32) != full.view(torch.int32)).sum().item())
+    del ref
+    return {"bitexact": same, "differing_words": n_diff, "shape": list(full.shape),
+            "what": "all-gathered row bands vs a single plan of the whole detector"}
+
+
 def parity_spot_check(out, kept, r0, cut):
     """After timing, compare the timed output buffer with the oracle outputs the CPU-baseline
-    leg computed for its pixel sample (north_star tolerance: per bin 1e-4 * sum|dI|)."""
+    leg computed for its pixel sample (north_star tolerance: per bin 1e-4 * sum|dI|).  Under an
+    intensity cutoff the oracle's output is zeroed at the pixels reading R14 leaves inactive
+    (float32 I_0 < cutoff, oracle.active_pixels)."""
     import numpy as np
     import torch
-    if out is None or not kept or cut[0] is not None:
+
+    import oracle
+    if out is None or not kept:
         return None
     js = kept["js"] - r0
     ok = (js >= 0) & (js < out.shape[1])
     js, is_ = js[ok], kept["is_"][ok]
     gpu = out[:, torch.from_numpy(js).to(out.device), torch.from_numpy(is_).to(out.device)].double().cpu().numpy().T
-    ref = kept["out"][ok]
+    ref = kept["out"][ok].copy()
+    n_active = None
+    if cut[0] is not None:
+        act = oracle.active_pixels(kept["ser"][ok][:, 0], cut[0])
+        ref[~act] = 0.0
+        n_active = int(act.sum())
     ser = kept["ser"][ok].astype(np.float64)
     d = np.abs(np.diff(ser, axis=1)).sum(axis=1)
     err = np.abs(gpu - ref).max(axis=1) / np.maximum(d, 1e-300)
     err = np.where(d > 0, err, np.abs(gpu - ref).max(axis=1))
-    return {"pixels": int(len(js)), "max_bin_err_over_sum_abs_dI": float(err.max()), "tol": 1e-4,
-            "pass": bool(err.max() <= 1e-4), "what": "timed output buffer vs fp64 oracle at the CPU-baseline sample"}
+    r = {"pixels": int(len(js)), "max_bin_err_over_sum_abs_dI": float(err.max()), "tol": 1e-4,
+         "pass": bool(err.max() <= 1e-4), "what": "timed output buffer vs fp64 oracle at the CPU-baseline sample"}
+    if n_active is not None:
+        r["active_pixels_in_sample"] = n_active
+    return r
 
 
 def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_max, achieved_min, value, units, st,
-           clocks, r0, r1, alg_bytes, allgather_ms, e2e, cut=(None, 1.0), out=None, kern_median=None):
+           clocks, r0, r1, alg_bytes, allgather_ms, e2e, cut=(None, 1.0), out=None, kern_median=None,
+           gather_check=None):
     import torch.distributed as dist
     if rank == 0:
         peak, peak_src = peak_hbm()
@@ -444,9 +490,16 @@ def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_ma
             line["config"]["pixel_fraction"] = args.fraction
             line["config"]["cutoff_first_step_intensity"] = cut[0]
             line["config"]["active_pixels"] = cut[1]
+            # the processed work: active pixels x wire steps per second (value counts every pixel)
+            line["active_rate"] = {"value": value * cut[1], "unit": UNIT,
+                                   "what": "value x active-pixel fraction (pixels the cutoff processes)"}
             line["roofline"]["bytes_rule"] += " with the input term x active-pixel fraction (estimate)"
         if allgather_ms is not None:
             line["all_gather_ms"] = allgather_ms
+        if world > 1:
+            line["config"]["backend"] = args.backend
+        if gather_check is not None:
+            line["gather_check"] = gather_check
         print(json.dumps(line), flush=True)
     plan.close()
     if world > 1:

@@ -50,11 +50,14 @@ def gather_rows(out_band, bands, group=None):
     hmax = max(e - b for b, e in bands)
     pad = torch.zeros((M, hmax, C), dtype=out_band.dtype, device=out_band.device)
     pad[:, : out_band.shape[1]] = out_band
-    buf = torch.empty((world, M, hmax, C), dtype=out_band.dtype, device=out_band.device)
     if dist.get_backend(group) == "nccl":
+        buf = torch.empty((world, M, hmax, C), dtype=out_band.dtype, device=out_band.device)
         dist.all_gather_into_tensor(buf, pad.contiguous(), group=group)
-    else:  # gloo has no all_gather_into_tensor
+    else:  # gloo: no all_gather_into_tensor; exchange through host memory
+        pad = pad.cpu()
+        buf = torch.empty((world, M, hmax, C), dtype=out_band.dtype)
         dist.all_gather(list(buf.unbind(0)), pad.contiguous(), group=group)
+        buf = buf.to(out_band.device)
     full = torch.empty((M, bands[-1][1], C), dtype=out_band.dtype, device=out_band.device)
     for g, (b, e) in enumerate(bands):
         full[:, b:e] = buf[g, :, : e - b]
@@ -74,5 +77,7 @@ def max_over_ranks(values, device=None, group=None):
     import torch.distributed as dist
     t = torch.tensor(list(values), dtype=torch.float64, device=device)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        if dist.get_backend(group) != "nccl":
+            t = t.cpu()
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return t.tolist()

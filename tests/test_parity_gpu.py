@@ -96,20 +96,42 @@ def _sample_pixels(cfg, maps, n_rand, rng):
     return np.array(js), np.array(is_)
 
 
-@pytest.mark.parametrize("name,noise", [("C3", True), ("C4", True), ("C5", False), ("C5", True)])
-def test_full_size_sampled(daxm, name, noise):
+@pytest.mark.parametrize("name,noise,dtype,fraction", [
+    ("C3", True, None, None), ("C4", True, None, None), ("C5", False, None, None), ("C5", True, None, None),
+    # fp32 stacks at full size (C5 is quoted for u16 and fp32)
+    ("C4", True, "f32", None), ("C5", True, "f32", None),
+    # intensity cutoff at full size, as bench.py --fraction runs it (reading R14)
+    ("C5", False, None, 0.05), ("C5", True, None, 0.25), ("C4", True, None, 0.5)])
+def test_full_size_sampled(daxm, name, noise, dtype, fraction):
     """BASELINE.json full sizes, stack generated on the GPU exactly as bench.py does;
-    sampled pixels recomputed by the oracle from the generator's per-pixel series."""
+    sampled pixels recomputed by the oracle from the generator's per-pixel series.
+    With a pixel fraction the cutoff is daxm_select_cutoff's (checked against the oracle's
+    order statistic of the same first image) and the oracle zeroes the inactive pixels."""
+    import dataclasses
+
     import torch
     cfg = synth.get_config(name)
+    if dtype:
+        cfg = dataclasses.replace(cfg, dtype=dtype)
     g = synth.geometry(cfg)
     maps = synth.make_maps(cfg)
     rng = np.random.default_rng(7 + cfg.number)
     js, is_ = _sample_pixels(cfg, maps, 1500, rng)
+    cut = None
     with daxm.create(g, device=0) as plan:
         stack = synth.stack_torch(maps, cfg.dtype, "cuda:0", noise=noise)
+        if fraction is not None:
+            cut = plan.select_cutoff(stack, fraction)
+            first = stack[0].cpu().numpy()
+            assert np.float32(cut) == np.float32(oracle.select_cutoff(first, fraction))
+            plan.set_cutoff(cut)
+            # the sample must hold both active and inactive pixels
+            act = oracle.active_pixels(first[js, is_], cut)
+            assert act.any() and (~act).any()
         out = plan.reconstruct(stack)
         torch.cuda.synchronize()
+        if name == "C4":  # the production row kernel, not a fallback
+            assert plan.stats()["row_path"] == 1
         jt = torch.from_numpy(js).cuda()
         it = torch.from_numpy(is_).cuda()
         gpu = out[:, jt, it].cpu().numpy()  # [M, n]
@@ -117,7 +139,9 @@ def test_full_size_sampled(daxm, name, noise):
         torch.cuda.empty_cache()
     series = synth.pixel_series(maps, js, is_, cfg.dtype, noise=noise)  # [n, S]
     ref = oracle.reconstruct_pixels(g, js, is_, series).T
-    parity.check(gpu, ref, series.T, f"{name} sampled")
+    if cut is not None:
+        ref[:, ~oracle.active_pixels(series[:, 0], cut)] = 0.0
+    parity.check(gpu, ref, series.T, f"{name} {cfg.dtype} sampled fraction={fraction}")
 
 
 # ------------------------------------------------------------------ edge cases
