@@ -269,7 +269,7 @@ def main():
     cutoff = None
     active = 1.0
     if args.fraction < 1.0:
-        cutoff = plan.select_cutoff(stack, args.fraction, stream)
+        cutoff = multi.select_cutoff(plan, stack, args.fraction, R, cfg.n, stream=stream)  # global over bands
         plan.set_cutoff(cutoff)
         active = float((stack[0].float() >= float(cutoff)).double().mean())
 

@@ -188,6 +188,24 @@ daxm_status daxm_set_cutoff(daxm_plan *p, int enable, double cutoff);
 daxm_status daxm_select_cutoff(daxm_plan *p, const void *d_stack, daxm_dtype dtype, double fraction, double *cutoff,
                                void *cuda_stream);
 
+/* Sum-over-shards callback of daxm_select_cutoff_sharded: on return hist[0..n) must hold the
+ * element-wise sum of every shard's hist (an all-reduce of n uint64 in host memory).  Returns 0
+ * on success; anything else aborts the selection with INVALID_ARGUMENT. */
+typedef int (*daxm_hist_reduce_fn)(unsigned long long *hist, int n, void *ctx);
+
+/* daxm_select_cutoff_sharded -- daxm_select_cutoff over a detector split into row bands, one
+ * plan per band (one rank per GPU): *cutoff = the k-th largest I_0 over ALL
+ * bands, k = ceil(fraction * n_total) clamped to [1, n_total], n_total = the whole detector's
+ * pixel count.  The radix select runs on every shard in lock step; after each 8-bit digit's
+ * device histogram of this plan's rows, `reduce(hist, 256, ctx)` must sum it over the shards
+ * (every shard calls it the same number of times: 2 for u16, 4 for f32), so every shard
+ * returns the same cutoff, equal to daxm_select_cutoff of one plan over the whole detector.
+ * Synchronises the stream.  Errors: as daxm_select_cutoff; INVALID_ARGUMENT also for a NULL
+ * reduce, n_total below the plan's pixel count, or a failing callback. */
+daxm_status daxm_select_cutoff_sharded(daxm_plan *p, const void *d_stack, daxm_dtype dtype, double fraction,
+                                       unsigned long long n_total, daxm_hist_reduce_fn reduce, void *ctx,
+                                       double *cutoff, void *cuda_stream);
+
 /* daxm_depth_profile -- per-depth-bin total intensity of a reconstruction (the paper's
  * second output, image_set.depth_intensity, P:L208 / image_depth_intensity):
  * d_profile[m] = sum over the plan's rows and all columns of d_out[m][row][col], in fp64.

@@ -43,6 +43,10 @@ class Geometry(C.Structure):
     ]
 
 
+# daxm_hist_reduce_fn (include/daxm.h): int (*)(unsigned long long *hist, int n, void *ctx)
+HIST_REDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_ulonglong), C.c_int, C.c_void_p)
+
+
 class PlanStats(C.Structure):
     _fields_ = [
         ("n_bins", C.c_int64), ("rows", C.c_int64), ("cols", C.c_int64), ("n_steps", C.c_int64),
@@ -85,6 +89,9 @@ def lib():
         L.daxm_set_cutoff.restype = C.c_int
         L.daxm_select_cutoff.argtypes = [P, P, C.c_int, C.c_double, C.POINTER(C.c_double), P]
         L.daxm_select_cutoff.restype = C.c_int
+        L.daxm_select_cutoff_sharded.argtypes = [P, P, C.c_int, C.c_double, C.c_ulonglong, HIST_REDUCE_FN, P,
+                                                 C.POINTER(C.c_double), P]
+        L.daxm_select_cutoff_sharded.restype = C.c_int
         L.daxm_depth_profile.argtypes = [P, P, P, P]
         L.daxm_depth_profile.restype = C.c_int
         L.daxm_last_error.argtypes = [P]
@@ -197,6 +204,33 @@ class Plan:
         val = C.c_double()
         self._check(lib().daxm_select_cutoff(self._h, C.c_void_p(stack.data_ptr()), dt, float(fraction),
                                              C.byref(val), C.c_void_p(stream.cuda_stream)))
+        return val.value
+
+    def select_cutoff_sharded(self, stack, fraction, n_total, reduce, stream=None):
+        """daxm_select_cutoff_sharded: the cutoff keeping `fraction` of `n_total` pixels split over
+        row-band plans.  `reduce(hist)` sums a uint64 numpy array over the shards in place
+        (multi.hist_allreduce builds one for torch.distributed)."""
+        import numpy as np
+        import torch
+        dt = self._dtype_of(stack, plane0_only=True)
+        if stream is None:
+            stream = torch.cuda.current_stream(stack.device)
+        errors = []
+
+        def cb(hist, n, ctx):
+            try:
+                reduce(np.ctypeslib.as_array(hist, shape=(n,)))
+                return 0
+            except BaseException as e:  # reported after the C call returns
+                errors.append(e)
+                return 1
+        fn = HIST_REDUCE_FN(cb)
+        val = C.c_double()
+        st = lib().daxm_select_cutoff_sharded(self._h, C.c_void_p(stack.data_ptr()), dt, float(fraction),
+                                              int(n_total), fn, None, C.byref(val), C.c_void_p(stream.cuda_stream))
+        if errors:
+            raise errors[0]
+        self._check(st)
         return val.value
 
     def depth_profile(self, out, profile=None, stream=None):

@@ -259,8 +259,10 @@ inline cudaError_t once_per_device(std::atomic<unsigned long long>& done, F&& se
 }
 
 // Launchers (deposit.cu, profile.cu, select.cu).
+typedef int (*HistReduce)(unsigned long long* hist, int n, void* ctx);  // = daxm_hist_reduce_fn
 cudaError_t select_cutoff(const void* plane0, int dtype, size_t n, unsigned long long k,
-                          unsigned long long* d_hist, cudaStream_t st, double* cutoff);
+                          unsigned long long* d_hist, cudaStream_t st, double* cutoff, HistReduce reduce,
+                          void* ctx, bool* reduce_failed);
 cudaError_t launch_cutoff_tiles(const DepositArgs& a, const void* plane0, int dtype, float* out, unsigned char* live,
                                 int phase, cudaStream_t st);  // phase 0: tile flags; 1: zero fill of dead tiles
 cudaError_t launch_depth_profile(const float* out, int M, size_t plane, double* profile, cudaStream_t st);

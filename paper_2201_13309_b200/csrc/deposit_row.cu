@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(32, 11) deposit_row(const __grid_constant__ CU
         for (int b = b0; b < nb; ++b) {
             const int s0 = (b * RW_PB) & (RB - 1);
             if (s0 < RW_KT - 1) {  // the ring's first slots: fold their overflow planes in
+                __syncwarp();  // order the other lanes' slot writes before this lane's fold reads
 #pragma unroll
                 for (int q = 0; q < RW_PB; ++q) {
                     const int s = s0 + q;

@@ -1531,29 +1531,51 @@ daxm_status daxm_set_cutoff(daxm_plan* p, int enable, double cutoff) {
     return DAXM_OK;
 }
 
-daxm_status daxm_select_cutoff(daxm_plan* p, const void* d_stack, daxm_dtype dt, double fraction, double* cutoff,
-                               void* cuda_stream) {
+static daxm_status select_cutoff_impl(daxm_plan* p, const void* d_stack, daxm_dtype dt, double fraction,
+                                      unsigned long long n_total, daxm_hist_reduce_fn reduce, void* ctx,
+                                      double* cutoff, void* cuda_stream) {
     if (!p) return DAXM_ERR_INVALID_ARGUMENT;
     p->err.clear();
     if (!d_stack || !cutoff) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "NULL stack or cutoff pointer");
     if (dt != DAXM_U16 && dt != DAXM_F32) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "unknown dtype %d", (int)dt);
     if (!(fraction > 0.0 && fraction <= 1.0))
         return fail(p, DAXM_ERR_INVALID_ARGUMENT, "fraction %g outside (0, 1]", fraction);
+    const size_t n = (size_t)p->rows * p->C;
+    if (reduce && n_total < n)
+        return fail(p, DAXM_ERR_INVALID_ARGUMENT, "n_total %llu below the plan's %zu pixels", n_total, n);
     DeviceGuard guard(p->device);
     if (!p->d_hist && cudaMalloc(&p->d_hist, 256 * sizeof(unsigned long long)) != cudaSuccess) {
         cudaGetLastError();
         return fail(p, DAXM_ERR_OUT_OF_MEMORY, "cutoff histogram");
     }
-    const size_t n = (size_t)p->rows * p->C;
-    unsigned long long k = (unsigned long long)ceil(fraction * (double)n);
+    const double nk = reduce ? (double)n_total : (double)n;
+    unsigned long long k = (unsigned long long)ceil(fraction * nk);
     if (k < 1) k = 1;
-    if (k > n) k = n;
-    cudaError_t e = select_cutoff(d_stack, (int)dt, n, k, p->d_hist, (cudaStream_t)cuda_stream, cutoff);
+    if (k > (unsigned long long)nk) k = (unsigned long long)nk;
+    bool reduce_failed = false;
+    cudaError_t e = select_cutoff(d_stack, (int)dt, n, k, p->d_hist, (cudaStream_t)cuda_stream, cutoff, reduce, ctx,
+                                  &reduce_failed);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(p, DAXM_ERR_CUDA, "cutoff selection: %s", cudaGetErrorString(e));
     }
+    if (reduce_failed) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "histogram reduce callback failed");
     return DAXM_OK;
+}
+
+daxm_status daxm_select_cutoff(daxm_plan* p, const void* d_stack, daxm_dtype dt, double fraction, double* cutoff,
+                               void* cuda_stream) {
+    return select_cutoff_impl(p, d_stack, dt, fraction, 0, nullptr, nullptr, cutoff, cuda_stream);
+}
+
+daxm_status daxm_select_cutoff_sharded(daxm_plan* p, const void* d_stack, daxm_dtype dt, double fraction,
+                                       unsigned long long n_total, daxm_hist_reduce_fn reduce, void* ctx,
+                                       double* cutoff, void* cuda_stream) {
+    if (!reduce) {
+        if (p) p->err = "NULL reduce callback";
+        return DAXM_ERR_INVALID_ARGUMENT;
+    }
+    return select_cutoff_impl(p, d_stack, dt, fraction, n_total, reduce, ctx, cutoff, cuda_stream);
 }
 
 daxm_status daxm_depth_profile(daxm_plan* p, const float* d_out, double* d_profile, void* cuda_stream) {

@@ -39,9 +39,12 @@ __global__ void __launch_bounds__(256) digit_histogram(const T* __restrict__ pla
 }  // namespace
 
 // k-th largest key (1-based) of plane0[0..n); returns the key, or sets *err.
+// With `reduce`, each digit's 256-bin host histogram is summed over the shards (ranks) by the
+// caller's callback before the digit is chosen, so every shard walks to the same global key.
 template <typename T>
 static cudaError_t select_kth(const T* plane0, size_t n, unsigned long long k, unsigned long long* d_hist,
-                              cudaStream_t st, uint32_t* key_out) {
+                              cudaStream_t st, uint32_t* key_out, HistReduce reduce, void* ctx,
+                              bool* reduce_failed) {
     constexpr int BITS = sizeof(T) == 2 ? 16 : 32;
     uint32_t prefix = 0u, mask = 0u;
     int dev = 0, sms = 148;
@@ -56,6 +59,10 @@ static cudaError_t select_kth(const T* plane0, size_t n, unsigned long long k, u
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         if ((e = cudaMemcpyAsync(h, d_hist, sizeof(h), cudaMemcpyDeviceToHost, st)) != cudaSuccess) return e;
         if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+        if (reduce && reduce(h, 256, ctx) != 0) {
+            *reduce_failed = true;
+            return cudaSuccess;
+        }
         int d = 255;
         for (; d > 0; --d) {  // walk digits from the top until k is reached
             if (h[d] >= k) break;
@@ -69,14 +76,16 @@ static cudaError_t select_kth(const T* plane0, size_t n, unsigned long long k, u
 }
 
 cudaError_t select_cutoff(const void* plane0, int dtype, size_t n, unsigned long long k,
-                          unsigned long long* d_hist, cudaStream_t st, double* cutoff) {
+                          unsigned long long* d_hist, cudaStream_t st, double* cutoff, HistReduce reduce,
+                          void* ctx, bool* reduce_failed) {
     uint32_t key = 0;
     cudaError_t e;
+    *reduce_failed = false;
     if (dtype == DAXM_U16) {
-        e = select_kth(static_cast<const uint16_t*>(plane0), n, k, d_hist, st, &key);
+        e = select_kth(static_cast<const uint16_t*>(plane0), n, k, d_hist, st, &key, reduce, ctx, reduce_failed);
         *cutoff = (double)key;
     } else {
-        e = select_kth(static_cast<const float*>(plane0), n, k, d_hist, st, &key);
+        e = select_kth(static_cast<const float*>(plane0), n, k, d_hist, st, &key, reduce, ctx, reduce_failed);
         const uint32_t b = (key & 0x80000000u) ? (key & 0x7fffffffu) : ~key;
         float f;
         memcpy(&f, &b, 4);

@@ -64,6 +64,34 @@ def gather_rows(out_band, bands, group=None):
     return full
 
 
+def hist_allreduce(group=None, device=None):
+    """The daxm_select_cutoff_sharded callback for torch.distributed: sums a uint64 numpy
+    histogram over the ranks in place (through `device` for NCCL, in host memory for gloo).
+    Counts stay below 2**63, so the int64 all-reduce is exact."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    def reduce(hist):
+        t = torch.from_numpy(hist.view(np.int64).copy())
+        if dist.get_backend(group) == "nccl":
+            t = t.to(device)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        hist.view(np.int64)[:] = t.cpu().numpy()
+    return reduce
+
+
+def select_cutoff(plan, stack_band, fraction, n_rows, n_cols, group=None, stream=None):
+    """Pixel percentage (reading R14) over the whole detector when each rank holds
+    one row band: the global k-th largest I_0, identical on every rank (one 256-bin histogram
+    all-reduce per radix digit).  With one rank this is plan.select_cutoff."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1):
+        return plan.select_cutoff(stack_band, fraction, stream)
+    return plan.select_cutoff_sharded(stack_band, fraction, n_rows * n_cols,
+                                      hist_allreduce(group, stack_band.device), stream)
+
+
 def allreduce_profile(profile, group=None):
     """Sum the per-rank depth profiles (M,) in place and return it."""
     import torch.distributed as dist

@@ -56,3 +56,5 @@ if "host" in which:
 if "general" in which:
     os.environ["DAXM_FORCE_GENERAL"] = "1"
     case("C1 general", synth.geometry("C1"), synth.stack_numpy(synth.make_maps("C1"), "f32", noise=True))
+torch.cuda.synchronize()
+torch.cuda.empty_cache()  # leave no cached torch blocks for --leak-check (the plans freed theirs)

@@ -3,6 +3,7 @@ reconstruction of its own band, all-gather of the output planes, all-reduce of t
 depth profile and the max-over-ranks timing reduction.  The per-rank compute here is
 the CPU oracle (no GPU on this box); on the GPU box bench.py runs the same host logic
 over NCCL with the CUDA library."""
+import ctypes as C
 import os
 import socket
 
@@ -59,7 +60,19 @@ def _worker(rank, world, port, ret):
         prof = torch.from_numpy(out_band.sum(axis=(1, 2)))
         multi.allreduce_profile(prof)
         tmax = multi.max_over_ranks([1.0 + rank, 5.0 - rank])
+        # the daxm_select_cutoff_sharded callback: a uint64 histogram summed over the ranks in
+        # place, called through a C function pointer as the library calls it
+        from paper_2201_13309_b200 import binding
+        hist = (C.c_ulonglong * 256)(*[(rank + 1) * i + (1 << 40) for i in range(256)])
+        red = multi.hist_allreduce()
+
+        def cb(h, n, ctx):
+            red(np.ctypeslib.as_array(h, shape=(n,)))
+            return 0
+        fn = binding.HIST_REDUCE_FN(cb)
+        assert fn(hist, 256, None) == 0
         if rank == 0:
+            ret["hist"] = list(hist)
             ret["full"] = full.numpy()
             ret["prof"] = prof.numpy()
             ret["tmax"] = tmax
@@ -74,8 +87,10 @@ def test_gloo_world2_band_gather_profile():
         ret = mgr.dict()
         mp.spawn(_worker, args=(world, port, ret), nprocs=world, join=True)
         full, prof, tmax = ret["full"], ret["prof"], ret["tmax"]
+        ret_hist = ret["hist"]
     g = synth.geometry("C1")
     ref = oracle.reconstruct(g, synth.stack_numpy(synth.make_maps("C1"), "f64", noise=True))
     assert np.allclose(full, ref, rtol=0, atol=1e-9)
     assert np.allclose(prof, ref.sum(axis=(1, 2)), rtol=1e-12, atol=1e-6)
+    assert ret_hist == [3 * i + (2 << 40) for i in range(256)]
     assert tmax == [2.0, 5.0]

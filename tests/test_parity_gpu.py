@@ -379,6 +379,45 @@ def test_select_cutoff_matches_oracle(daxm, name, dtype, fraction):
     assert c == oracle.select_cutoff(host[0], fraction)
 
 
+@pytest.mark.parametrize("name,dtype,fraction", [("C3", "u16", 0.25), ("C2", "f32", 0.003), ("C2", "f32", 1.0)])
+def test_select_cutoff_sharded(daxm, name, dtype, fraction):
+    """daxm_select_cutoff_sharded with two row-band plans in lock step (two threads; the
+    reduce callback sums their digit histograms at a barrier) = the oracle's order statistic
+    of the whole first image, on both shards."""
+    import threading
+
+    import torch
+    g = synth.geometry(name)
+    host = synth.stack_numpy(synth.make_maps(name), dtype, noise=True)
+    R = g["n_rows"]
+    bands = [(0, R // 2), (R // 2, R)]
+    barrier = threading.Barrier(2, timeout=120)
+    slots = [None, None]
+    res = [None, None]
+
+    def worker(i):
+        b0, b1 = bands[i]
+        with daxm.create(g, device=0, rows=(b0, b1)) as plan:
+            st = torch.from_numpy(np.ascontiguousarray(host[:, b0:b1])).to("cuda:0")
+            stream = torch.cuda.Stream(device=0)
+
+            def reduce(h):
+                slots[i] = h.copy()
+                barrier.wait()
+                tot = slots[0] + slots[1]
+                barrier.wait()
+                h[:] = tot
+            with torch.cuda.stream(stream):
+                res[i] = plan.select_cutoff_sharded(st, fraction, R * g["n_cols"], reduce, stream)
+    th = [threading.Thread(target=worker, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(300)
+    ref = oracle.select_cutoff(host[0], fraction)
+    assert res[0] == res[1] and np.float32(res[0]) == np.float32(ref), (res, ref)
+
+
 @pytest.mark.parametrize("case", ["C2-f32", "C3-u16", "C3-u16-band", "C2-u16-general", "overlap-u16", "C3-u16-host"])
 def test_cutoff_parity(daxm, case, monkeypatch):
     """Intensity cutoff (d_cutoff; reading R14): pixels below it are not processed and
