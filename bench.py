@@ -369,6 +369,8 @@ def launches_per_step(st, dtype, cutoff=False):
     kernel once per output-ring class in use, deposit_fast (separated + dual-walk launches) if
     any non-general tile is left to it, the general kernel if any tile needs it; with a cutoff
     also tile_live and zero_dead_tiles (csrc/select.cu)."""
+    if st.get("row_path"):  # row-segment path: one launch per non-empty class, cutoff in-kernel
+        return int(st["row_launches"])
     general = st["general_tiles_u16" if dtype == "u16" else "general_tiles_f32"]
     small, large = st.get("lock_tiles_small", 0), st.get("lock_tiles_large", 0)
     ov = st.get("lock_tiles_overlap", 0)  # one launch per ring class in use (counted together: an upper bound)
@@ -475,6 +477,9 @@ def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_ma
             "clocks": clocks.summary(),
             "prepass_ms": st["prepass_ms"],
             "plan": {"contrib_pairs": st["contrib_pairs"], "window_pairs": st["window_pairs"],
+                     "row_path": st["row_path"], "row_tiles_small": st["row_tiles_small"],
+                     "row_tiles_large": st["row_tiles_large"], "row_tiles_gen": st["row_tiles_gen"],
+                     "row_tiles_general": st["row_tiles_general"],
                      "general_tiles": st["general_tiles_u16" if cfg.dtype == "u16" else "general_tiles_f32"],
                      "n_tiles": st["n_tiles"], "lock_tiles_small": st.get("lock_tiles_small"),
                      "lock_tiles_large": st.get("lock_tiles_large"), "lock_tiles_overlap": st.get("lock_tiles_overlap"),

@@ -116,6 +116,11 @@ typedef struct {
     int64_t row_reject[8];     /* DESIGN.md §5.3) and the number of row tiles per reason bit            */
     int64_t row_path;          /* 1: daxm_reconstruct runs the row-segment kernel (every row tile          */
                                /* admitted), 0: the deposit-tile kernels                                   */
+    int64_t row_tiles_gen;     /* of row_tiles_small + row_tiles_large: tiles the general-span variant    */
+                               /* runs (overlapping edge spans or spans of 2-4 bins)      */
+    int64_t row_reject_more;   /* row tiles not admitted for RW_WHY_GEN (bit 8)                          */
+    int64_t row_launches;      /* kernel launches of one daxm_reconstruct on the row path (one per       */
+                               /* non-empty class: separated / general-span x ring 16 / 32, general)    */
 } daxm_plan_stats;
 
 /* daxm_create -- validate `g`, run the fp64 geometry pre-pass on `cuda_device`,

@@ -190,6 +190,9 @@ constexpr int RW_KT = DAXM_RW_KT;   // max bin edges one walk evaluates per iter
 constexpr int RW_RB_SMALL = 16, RW_RB_LARGE = 32;  // output ring planes (+ RW_KT - 1 overflow planes)
 constexpr int RW_CLS_RB = 0xff;         // RowTile.cls: ring planes (0: not admitted -> general kernel)
 constexpr int RW_CLS_FRONT_LO = 0x100;  //   the front pixel edge is the shallower one over the tile
+constexpr int RW_CLS_GEN = 0x200;       //   general-span variant (overlapping spans, spans up to RW_NQ_GEN bins)
+constexpr int RW_KT_GEN = 6;            // max bin edges per zone and iteration, general-span variant
+constexpr int RW_NQ_GEN = 4;            // general-span variant: zone edges evaluated exactly (then linear)
 static_assert(RW_ROWS * RW_COLS == 128 && RW_COLS % 32 == 0 && (RW_ROWS == 2 || RW_ROWS == 4),
               "row tile: 4 walks per lane, two per pair");
 // pair p of a lane: column half and first row
@@ -215,6 +218,8 @@ enum : unsigned {
     RW_WHY_RING = 32u,     // output-ring need above RW_RB_LARGE
     RW_WHY_ORDER = 64u,    // neither pixel edge is the shallower one throughout
     RW_WHY_ITER = 128u,
+    RW_WHY_GEN = 256u,     // general-span variant: a ramp reaching past the next zone, knots beyond
+                           // RW_NQ_GEN bins or a vanishing rise / fall width
 };
 
 struct RowArgs {
@@ -276,10 +281,10 @@ cudaError_t launch_lock(const DepositArgs& a, const CUtensorMap* in_map, float* 
 cudaError_t launch_lock_prepass(const DepositArgs& a, int n_tiles, int* d_stats, cudaStream_t st);
 // row-segment kernel (deposit_row.cu): pre-pass replay (admission) and the class launches
 cudaError_t launch_row_admit(const RowArgs& a, RowTile* rt, int n_rt, int* d_stats, cudaStream_t st);
-size_t row_smem_bytes(int dtype, int rb, int max_nv);
+size_t row_smem_bytes(int dtype, int rb, bool gen, int max_nv);
 cudaError_t row_set_attributes(int max_nv);  // per device: dynamic shared memory of every instance
 cudaError_t launch_row(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int dtype, int rb,
-                       cudaStream_t st);
+                       bool gen, cudaStream_t st);
 cudaError_t launch_general_rows(const DepositArgs& a, const int* rt_list, int n, int n_rc, int row_org,
                                 const void* stack, int dtype, float* out, cudaStream_t st);
 

@@ -58,9 +58,9 @@ using namespace ptx;
 constexpr int PLANE_B = RW_ROWS * RW_COLS * 4;  // one staged output plane (512 B)
 constexpr int NG = RW_NB / RW_G;                // input groups in the ring
 
-template <typename T, int RB>
+template <typename T, int RB, int KT = RW_KT>
 struct RowSmem {
-    static constexpr int OUT_SLOTS = RB + RW_KT - 1;
+    static constexpr int OUT_SLOTS = RB + KT - 1;
     static constexpr int IN_SLOT = RW_ROWS * 32 * (int)sizeof(T);  // one step of one column half
     static constexpr int IN_GROUP = RW_G * IN_SLOT;                // one TMA box
     static constexpr int IN_HALF = RW_NB * IN_SLOT;                // a half's ring
@@ -169,6 +169,9 @@ static_assert(RW_H == 2 && RW_ROWS == 2, "deposit_row: two column halves per lan
 // prefetched next one (tq, Iq).
 struct RowState {
     float2 plo[2], phi[2], ps[2], pI[2], cq[2], zF[2], En[2], Iq[2];
+    // general-span variant only (dead otherwise): c_{v-2}, hi_{v-1}, M_{v-2} (start of pair v-2's
+    // falling ramp) and 1 / that ramp's width
+    float2 cq2[2], phm[2], pM[2], if2[2];
     float tq;
 };
 
@@ -243,10 +246,13 @@ __device__ __forceinline__ void row_starts(const RowWalk wk[2][2], int lane, int
     vend = __reduce_max_sync(0xffffffffu, ve);
 }
 
-template <typename T, bool POINT, int RB>
-__global__ void __launch_bounds__(32, 11) deposit_row(const __grid_constant__ CUtensorMap in_map,
-                                                  const __grid_constant__ CUtensorMap out_map, const RowArgs a) {
-    using L = RowSmem<T, RB>;
+template <typename T, bool POINT, int RB, bool GEN>
+__global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_constant__ CUtensorMap in_map,
+                                                            const __grid_constant__ CUtensorMap out_map,
+                                                            const RowArgs a) {
+    static_assert(!(GEN && POINT), "the general-span variant is for finite pixels");
+    constexpr int KT = GEN ? RW_KT_GEN : RW_KT;  // max edges per zone and iteration
+    using L = RowSmem<T, RB, KT>;
     static_assert(RB % RW_PB == 0 && (RB & (RB - 1)) == 0, "ring");
     extern __shared__ unsigned char smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
@@ -399,6 +405,10 @@ __global__ void __launch_bounds__(32, 11) deposit_row(const __grid_constant__ CU
             A.phi[p] = POINT ? A.plo[p] : poly2(cf[p], f2(t0));
             A.ps[p] = add2(A.plo[p], A.phi[p]);
             A.cq[p] = A.zF[p] = f2(0.f);
+            if constexpr (GEN) {  // no earlier pairs: zero coefficients, zero-width ramps
+                A.cq2[p] = A.if2[p] = f2(0.f);
+                A.phm[p] = A.pM[p] = A.plo[p];
+            }
             A.En[p].x = wk[p][0].npts > 0 ? fmaxf(E0, floorf(A.plo[p].x) + 1.f) : EM + 1.f;
             A.En[p].y = wk[p][1].npts > 0 ? fmaxf(E0, floorf(A.plo[p].y) + 1.f) : EM + 1.f;
         }
@@ -430,12 +440,12 @@ __global__ void __launch_bounds__(32, 11) deposit_row(const __grid_constant__ CU
 #pragma unroll 1
         for (int b = b0; b < nb; ++b) {
             const int s0 = (b * RW_PB) & (RB - 1);
-            if (s0 < RW_KT - 1) {  // the ring's first slots: fold their overflow planes in
+            if (s0 < KT - 1) {  // the ring's first slots: fold their overflow planes in
                 __syncwarp();  // order the other lanes' slot writes before this lane's fold reads
 #pragma unroll
                 for (int q = 0; q < RW_PB; ++q) {
                     const int s = s0 + q;
-                    if (s >= RW_KT - 1) break;
+                    if (s >= KT - 1) break;
                     const uint4 x = lds128u(s_copy + s * PLANE_B), y = lds128u(s_copy + (RB + s) * PLANE_B);
                     sts128u(s_copy + s * PLANE_B, make_uint4(y.x == SENT ? x.x : y.x, y.y == SENT ? x.y : y.y,
                                                              y.z == SENT ? x.z : y.z, y.w == SENT ? x.w : y.w));
@@ -493,6 +503,7 @@ __global__ void __launch_bounds__(32, 11) deposit_row(const __grid_constant__ CU
     // F at its last edge becomes the next Fp.
     struct Zone {
         float2 F0v, o1, o2, c, Fl, cnt;
+        float2 o3, o4;  // general-span variant: edges 3 and 4 of the zone (else both are c)
         uint32_t es[2];
     };
     // Transition S -> D: every pair advances one point; point v + 1 closes the zone [lo_v, lo_{v+1})
@@ -506,13 +517,73 @@ __global__ void __launch_bounds__(32, 11) deposit_row(const __grid_constant__ CU
             const float2 lo = poly2(cb[p], f2(S.tq)), hi = POINT ? lo : poly2(cf[p], f2(S.tq));
             const float2 s = add2(lo, hi);
             const float2 c = mul2(mul2(sdir2, sub2(S.pI[p], S.Iq[p])), rcp2(sub2(s, S.ps[p])));
-            const float2 w = sub2(S.phi[p], S.plo[p]);
-            const float2 d = sub2(S.cq[p], c);
-            const float2 h = POINT ? S.zF[p] : fma2(f2(0.5f), mul2(w, d), S.zF[p]);
             // edges of the zone [plo, lo): En .. floor(min(lo, EM))
             const float2 fl = add2(floor2(min2(lo, f2(EM))), f2(1.f));
             const float2 cnt = sub2(fl, add2(S.En[p], gate[p]));
             const float2 x0 = sub2(S.En[p], S.plo[p]);
+            if constexpr (GEN) {
+                // General spans ("general-span variant").  Pair q's trapezoid rises over
+                // [lo_q, m_q], m_q = min(hi_q, lo_{q+1}), and falls over [M_q, hi_{q+1}], M_q = max(hi_q,
+                // lo_{q+1}) (the sorted corners of P:L320-331).  In zone v = [lo_v, lo_{v+1}) only pairs v,
+                // v-1 and v-2 are incomplete (replay), so with x = E - lo_v and the zone's linear form
+                // h + c_v x (valid past every knot, x >= RW_NQ_GEN by the replay),
+                //   F = h + c_v x + c_v (r - xc)^2 / 2r - c_{v-1} [(f1 - y1c)^2 / 2f1 - min(y1, 0)]
+                //       - c_{v-2} (f2 - y2c)^2 / 2f2,
+                // r = m_v - lo_v, xc = min(x, r); y1 = x - a1, a1 = M_{v-1} - lo_v, f1 = hi_v - M_{v-1},
+                // y1c = clamp(y1, 0, f1); y2c = min(x + d2, f2), d2 = lo_v - M_{v-2}, f2 = hi_{v-1} - M_{v-2}.
+                const float2 st = sub2(lo, S.plo[p]);
+                const float2 r = min2(sub2(S.phi[p], S.plo[p]), st);
+                const float2 ir = rcp2(r);
+                const float2 M1 = max2(S.phm[p], S.plo[p]);
+                const float2 a1 = sub2(M1, S.plo[p]);
+                const float2 f1 = sub2(S.phi[p], M1);
+                const float2 if1 = rcp2(f1);
+                const float2 d2 = sub2(S.plo[p], S.pM[p]);
+                const float2 f2v = sub2(S.phm[p], S.pM[p]);
+                const float2 c1 = S.cq[p], c2 = S.cq2[p];
+                const float2 ch = mul2(mul2(c, ir), f2(0.5f));
+                const float2 nc1h = mul2(mul2(c1, if1), f2(-0.5f));
+                const float2 c2h = mul2(mul2(c2, S.if2[p]), f2(0.5f));
+                const float2 nc2h = mul2(c2h, f2(-1.f));
+                const float2 t20 = sub2(f2v, min2(d2, f2v));
+                // h = zF - c r / 2 + c1 (a1 + f1 / 2) + c2 (f2 - min(d2, f2))^2 / 2f2  (F = zF at x = 0)
+                float2 h = fma2(c, mul2(r, f2(-0.5f)), S.zF[p]);
+                h = fma2(c1, fma2(f1, f2(0.5f), a1), h);
+                h = fma2(mul2(c2h, t20), t20, h);
+                auto Fx = [&](float2 x) {
+                    const float2 t = sub2(r, min2(x, r));
+                    float2 e = fma2(c, x, h);
+                    e = fma2(mul2(ch, t), t, e);
+                    const float2 y1 = sub2(x, a1);
+                    const float2 t1 = sub2(f1, min2(max2(y1, f2(0.f)), f1));
+                    e = fma2(mul2(nc1h, t1), t1, e);
+                    e = fma2(c1, min2(y1, f2(0.f)), e);
+                    const float2 t2 = sub2(f2v, min2(add2(x, d2), f2v));
+                    return fma2(mul2(nc2h, t2), t2, e);
+                };
+                const float2 F0v = Fx(x0), F1v = Fx(add2(x0, f2(1.f))), F2v = Fx(add2(x0, f2(2.f)));
+                const float2 F3v = Fx(add2(x0, f2(3.f)));
+                const float2 xl = add2(x0, sub2(cnt, f2(1.f)));  // x of the zone's last edge
+                const float2 Fl = fma2(c, xl, h);
+                Z[p].F0v = F0v;
+                Z[p].o1 = sub2(F1v, F0v);
+                Z[p].o2 = sub2(F2v, F1v);
+                Z[p].o3 = sub2(F3v, F2v);
+                Z[p].o4 = sub2(fma2(c, add2(x0, f2(4.f)), h), F3v);
+                Z[p].c = c;
+                Z[p].Fl = make_float2(cnt.x >= 5.f ? Fl.x : cnt.x >= 4.f ? F3v.x : cnt.x >= 3.f ? F2v.x
+                                                          : cnt.x >= 2.f ? F1v.x : F0v.x,
+                                      cnt.y >= 5.f ? Fl.y : cnt.y >= 4.f ? F3v.y : cnt.y >= 3.f ? F2v.y
+                                                          : cnt.y >= 2.f ? F1v.y : F0v.y);
+                D.zF[p] = Fx(st);  // F at the next zone's start
+                D.cq2[p] = c1;
+                D.phm[p] = S.phi[p];
+                D.pM[p] = M1;
+                D.if2[p] = if1;
+            } else {
+            const float2 w = sub2(S.phi[p], S.plo[p]);
+            const float2 d = sub2(S.cq[p], c);
+            const float2 h = POINT ? S.zF[p] : fma2(f2(0.5f), mul2(w, d), S.zF[p]);
             const float2 x1 = add2(x0, f2(1.f));
             float2 F0v, F1v;
             if (POINT) {
@@ -532,10 +603,11 @@ __global__ void __launch_bounds__(32, 11) deposit_row(const __grid_constant__ CU
             Z[p].c = c;
             Z[p].Fl = make_float2(cnt.x >= 3.f ? Fl.x : cnt.x >= 2.f ? F1v.x : F0v.x,
                                   cnt.y >= 3.f ? Fl.y : cnt.y >= 2.f ? F1v.y : F0v.y);
+            D.zF[p] = fma2(c, sub2(lo, S.plo[p]), h);  // F at the next zone's start
+            }
             Z[p].cnt = cnt;
             Z[p].es[0] = lea9((uint32_t)__float_as_int(S.En[p].x + fbias) & (uint32_t)(RB - 1), p ? ob1 : ob0);
             Z[p].es[1] = lea9((uint32_t)__float_as_int(S.En[p].y + fbias) & (uint32_t)(RB - 1), p ? ob1 : ob0);
-            D.zF[p] = fma2(c, sub2(lo, S.plo[p]), h);  // F at the next zone's start
             D.En[p] = max2(S.En[p], fl);
             D.plo[p] = lo;
             D.phi[p] = hi;
@@ -550,7 +622,7 @@ __global__ void __launch_bounds__(32, 11) deposit_row(const __grid_constant__ CU
     // The bin-edge stores of a zone: edge k of walk (p, r) goes to plane En + k - 1, staged slot
     // es + k planes (immediate offsets; row r, column half p), iff k < cnt.  Branch-free: RW_ST
     // predicated stores per walk, a rare extra trip when some zone holds more edges.
-    constexpr int RW_ST = 4;
+    constexpr int RW_ST = GEN ? 5 : 4;  // (general-span zones, up to 5 bins, hold more edges)
     auto edges = [&](const Zone Z[2], const float2 Fin[2], float2 Fout[2]) {
         static_for<0, 2>([&](auto pc) {
             constexpr int p = decltype(pc)::value;
@@ -564,8 +636,9 @@ __global__ void __launch_bounds__(32, 11) deposit_row(const __grid_constant__ CU
             st_if<O1 + 2 * PLANE_B>(Z[p].es[1], Z[p].o2.y, 2.f, Z[p].cnt.y);
             static_for<3, RW_ST>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
-                st_if<O0 + k * PLANE_B>(Z[p].es[0], Z[p].c.x, (float)k, Z[p].cnt.x);
-                st_if<O1 + k * PLANE_B>(Z[p].es[1], Z[p].c.y, (float)k, Z[p].cnt.y);
+                const float2 v = !GEN ? Z[p].c : k == 3 ? Z[p].o3 : k == 4 ? Z[p].o4 : Z[p].c;
+                st_if<O0 + k * PLANE_B>(Z[p].es[0], v.x, (float)k, Z[p].cnt.x);
+                st_if<O1 + k * PLANE_B>(Z[p].es[1], v.y, (float)k, Z[p].cnt.y);
                 return true;
             });
             Fout[p].x = Z[p].cnt.x >= 1.f ? Z[p].Fl.x : Fin[p].x;
@@ -577,7 +650,7 @@ __global__ void __launch_bounds__(32, 11) deposit_row(const __grid_constant__ CU
             static_for<0, 2>([&](auto pc) {
                 constexpr int p = decltype(pc)::value;
                 constexpr int O0 = 0, O1 = RW_COLS * 4;
-                static_for<RW_ST, RW_KT>([&](auto kc) {
+                static_for<RW_ST, KT>([&](auto kc) {
                     constexpr int k = decltype(kc)::value;
                     st_if<O0 + k * PLANE_B>(Z[p].es[0], Z[p].c.x, (float)k, Z[p].cnt.x);
                     st_if<O1 + k * PLANE_B>(Z[p].es[1], Z[p].c.y, (float)k, Z[p].cnt.y);
@@ -586,7 +659,7 @@ __global__ void __launch_bounds__(32, 11) deposit_row(const __grid_constant__ CU
                 return true;
             });
 #if DAXM_ROW_CHECK
-            if (cmax > (float)RW_KT) viol |= 2u;
+            if (cmax > (float)KT) viol |= 2u;
 #endif
         }
 #if DAXM_ROW_CHECK
@@ -677,14 +750,20 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
     const int rr = rt / a.n_rc, rc = rt % a.n_rc;
     const int row0 = a.row_org + rr * RW_ROWS, col0 = rc * RW_COLS;
     const bool empty = ti.k_hi < ti.k_lo;  // no pixel window: the kernel streams zeros
-    const bool eligible = !empty && ti.sep == MODE_SEPARATED && ti.k_hi - ti.k_lo + 1 <= MAX_FAST_NV;
-    unsigned bad = (!eligible && !empty) ? RW_WHY_MODE : 0u;  // reasons (RW_WHY_*)
+    const bool eligible = !empty && ti.sep != MODE_GENERAL && ti.k_hi - ti.k_lo + 1 <= MAX_FAST_NV;
+    unsigned bad = (!eligible && !empty) ? RW_WHY_MODE : 0u;  // reasons both variants share (RW_WHY_*)
+    // reasons only the separated / only the general-span variant has
+    unsigned bad_sep = (!empty && ti.sep != MODE_SEPARATED) ? RW_WHY_MODE : 0u;
+    unsigned bad_gen = a.point_mode ? RW_WHY_MODE : 0u;
     bool back_lo = true, front_lo = true;
     int need = 0, iters = 0;
     if (eligible) {
         const int nvt = ti.k_hi - ti.k_lo + 1;
         const float E0 = (float)(-a.m_ref), EM = (float)(a.M - a.m_ref);
         float cb[2][2][3], cf[2][2][3], En[2][2], ps[2][2];
+        // general-span variant: the walk's last point (lo_v, hi_v), hi_{v-1}, hi_{v-2}, zones done
+        float plo[2][2], phi[2][2], phm[2][2], phmm[2][2];
+        int ndone[2][2];
         RowWalk wk[2][2];
         for (int p = 0; p < 2; ++p)
             for (int r = 0; r < 2; ++r) {
@@ -720,6 +799,10 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
                 point(p, r, vs, lo, hi);
                 En[p][r] = fmaxf(E0, floorf(lo) + 1.f);
                 ps[p][r] = lo + hi;
+                plo[p][r] = lo;
+                phi[p][r] = hi;
+                phm[p][r] = phmm[p][r] = lo;
+                ndone[p][r] = 0;
             }
         const int ngroups = vend / RW_G + 1;
         int g_issue = min(NG, ngroups);
@@ -755,8 +838,30 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
                         point(p, r, v + 1, lo, hi);
                         const float s = lo + hi;
                         if (!(s != ps[p][r])) bad |= RW_WHY_DENSITY;
-                        // finite ramp slope, and a span below two bins (from a zone's third edge on F is linear)
-                        if (!a.point_mode && !(hi - lo >= 1e-6f && hi - lo < 2.f)) bad |= RW_WHY_DENSITY;
+                        if (!a.point_mode) {
+                            // finite ramp slope; separated variant: a span below two bins (from a zone's
+                            // third edge on F is linear)
+                            if (!(hi - lo >= 1e-6f)) bad |= RW_WHY_DENSITY;
+                            if (!(hi - lo < 2.f)) bad_sep |= RW_WHY_DENSITY;
+                            // general-span variant, zone v = [lo_v, lo): nonzero rise width r = min(w_v,
+                            // lo - lo_v) and fall width f1 = hi_v - max(hi_{v-1}, lo_v) (finite reciprocals);
+                            // where the zone can touch the bins, pair v-3 complete (hi_{v-2} <= lo_v) and
+                            // every knot within RW_NQ_GEN bins of lo_v (exact edges 0 .. RW_NQ_GEN - 1)
+                            const float lv = plo[p][r], hv = phi[p][r];
+                            const float rr_ = fminf(hv - lv, lo - lv);
+                            const float f1 = hv - fmaxf(phm[p][r], lv);
+                            if (!(rr_ >= 1e-6f) || !(f1 >= 1e-6f)) bad_gen |= RW_WHY_GEN;
+                            if (lo >= E0 - 1.f && lv <= EM + 1.f) {
+                                if (ndone[p][r] >= 2 && !(phmm[p][r] <= lv)) bad_gen |= RW_WHY_GEN;
+                                const float kn = fmaxf(hv, ndone[p][r] >= 1 ? phm[p][r] : hv) - lv;
+                                if (!(kn <= (float)RW_NQ_GEN)) bad_gen |= RW_WHY_GEN;
+                            }
+                            phmm[p][r] = phm[p][r];
+                            phm[p][r] = hv;
+                            plo[p][r] = lo;
+                            phi[p][r] = hi;
+                            ++ndone[p][r];
+                        }
                         ps[p][r] = s;
                         const float fl = floorf(fminf(lo, EM)) + 1.f;
                         const float cnt = fl - En[p][r];
@@ -770,7 +875,8 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
             ++v;
             kmax = __reduce_max_sync(0xffffffffu, kmax);
             pmax = __reduce_max_sync(0xffffffffu, pmax);
-            if (kmax > RW_KT) bad |= RW_WHY_KT;
+            if (kmax > RW_KT) bad_sep |= RW_WHY_KT;
+            if (kmax > RW_KT_GEN) bad_gen |= RW_WHY_KT;
             zeroed_b = issued_b;  // zero_pending: batches stored at the previous iteration
             if (pmax != INT_MIN) need = max(need, pmax - zeroed_b * RW_PB + 1);
             fr_e = frontier();
@@ -786,15 +892,20 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
                 if (wk[p][r].npts > 0 && !(En[p][r] >= EM + 1.f)) bad |= RW_WHY_TOP;
     }
     bad = __reduce_or_sync(0xffffffffu, bad);
+    bad_sep = __reduce_or_sync(0xffffffffu, bad_sep);
+    bad_gen = __reduce_or_sync(0xffffffffu, bad_gen);
     back_lo = __all_sync(0xffffffffu, back_lo);
     front_lo = __all_sync(0xffffffffu, front_lo);
     if (lane == 0) {
         int cls = 0;
         if (!(back_lo || front_lo)) bad |= RW_WHY_ORDER;
         if (need > RW_RB_LARGE) bad |= RW_WHY_RING;
-        if (!bad) {
+        if (!bad && (!bad_sep || !bad_gen)) {
             cls = need <= RW_RB_SMALL ? RW_RB_SMALL : RW_RB_LARGE;
             if (!back_lo) cls |= RW_CLS_FRONT_LO;
+            if (bad_sep) cls |= RW_CLS_GEN;  // the separated variant does not apply: the general-span one
+        } else {
+            bad |= bad_sep | bad_gen;
         }
         ti.cls = cls;
         ti.why = (int)bad;
@@ -805,63 +916,79 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
     }
 }
 
-template <typename T, bool POINT, int RB>
-cudaError_t set_attr_one(int max_nv) {
-    (void)max_nv;
-    cudaError_t e = cudaFuncSetAttribute(deposit_row<T, POINT, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)RowSmem<T, RB>::bytes(MAX_FAST_NV));
+template <typename T, bool POINT, int RB, bool GEN>
+using RowSmemOf = RowSmem<T, RB, GEN ? RW_KT_GEN : RW_KT>;
+
+template <typename T, bool POINT, int RB, bool GEN>
+cudaError_t set_attr_one() {
+    cudaError_t e = cudaFuncSetAttribute(deposit_row<T, POINT, RB, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)RowSmemOf<T, POINT, RB, GEN>::bytes(MAX_FAST_NV));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(deposit_row<T, POINT, RB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    return cudaFuncSetAttribute(deposit_row<T, POINT, RB, GEN>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                 (int)cudaSharedmemCarveoutMaxShared);
 }
 
-template <typename T, bool POINT, int RB>
+template <typename T, bool POINT, int RB, bool GEN>
 cudaError_t launch_one(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int max_nv,
                        cudaStream_t st) {
-    const size_t sm = RowSmem<T, RB>::bytes(max_nv);
-    deposit_row<T, POINT, RB><<<(unsigned)a.n_list, 32, sm, st>>>(*in_map, *out_map, a);
+    const size_t sm = RowSmemOf<T, POINT, RB, GEN>::bytes(max_nv);
+    deposit_row<T, POINT, RB, GEN><<<(unsigned)a.n_list, 32, sm, st>>>(*in_map, *out_map, a);
     return cudaGetLastError();
 }
 
+template <typename T, int RB>
+cudaError_t launch_rb(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, bool gen, int max_nv,
+                      cudaStream_t st) {
+    if (a.point_mode) return launch_one<T, true, RB, false>(a, in_map, out_map, max_nv, st);
+    return gen ? launch_one<T, false, RB, true>(a, in_map, out_map, max_nv, st)
+               : launch_one<T, false, RB, false>(a, in_map, out_map, max_nv, st);
+}
+
 template <typename T>
-cudaError_t launch_t(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int rb, int max_nv,
-                     cudaStream_t st) {
-    if (rb == RW_RB_SMALL)
-        return a.point_mode ? launch_one<T, true, RW_RB_SMALL>(a, in_map, out_map, max_nv, st)
-                            : launch_one<T, false, RW_RB_SMALL>(a, in_map, out_map, max_nv, st);
-    return a.point_mode ? launch_one<T, true, RW_RB_LARGE>(a, in_map, out_map, max_nv, st)
-                        : launch_one<T, false, RW_RB_LARGE>(a, in_map, out_map, max_nv, st);
+cudaError_t launch_t(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int rb, bool gen,
+                     int max_nv, cudaStream_t st) {
+    return rb == RW_RB_SMALL ? launch_rb<T, RW_RB_SMALL>(a, in_map, out_map, gen, max_nv, st)
+                             : launch_rb<T, RW_RB_LARGE>(a, in_map, out_map, gen, max_nv, st);
+}
+
+template <typename T, int RB>
+cudaError_t set_attr_rb() {
+    cudaError_t e;
+    if ((e = set_attr_one<T, false, RB, false>()) != cudaSuccess) return e;
+    if ((e = set_attr_one<T, true, RB, false>()) != cudaSuccess) return e;
+    return set_attr_one<T, false, RB, true>();
 }
 
 }  // namespace
 
-size_t row_smem_bytes(int dtype, int rb, int max_nv) {
-    if (dtype == DAXM_U16)
-        return rb == RW_RB_SMALL ? RowSmem<uint16_t, RW_RB_SMALL>::bytes(max_nv)
-                                 : RowSmem<uint16_t, RW_RB_LARGE>::bytes(max_nv);
-    return rb == RW_RB_SMALL ? RowSmem<float, RW_RB_SMALL>::bytes(max_nv) : RowSmem<float, RW_RB_LARGE>::bytes(max_nv);
+size_t row_smem_bytes(int dtype, int rb, bool gen, int max_nv) {
+    if (dtype == DAXM_U16) {
+        if (rb == RW_RB_SMALL)
+            return gen ? RowSmem<uint16_t, RW_RB_SMALL, RW_KT_GEN>::bytes(max_nv) : RowSmem<uint16_t, RW_RB_SMALL>::bytes(max_nv);
+        return gen ? RowSmem<uint16_t, RW_RB_LARGE, RW_KT_GEN>::bytes(max_nv) : RowSmem<uint16_t, RW_RB_LARGE>::bytes(max_nv);
+    }
+    if (rb == RW_RB_SMALL)
+        return gen ? RowSmem<float, RW_RB_SMALL, RW_KT_GEN>::bytes(max_nv) : RowSmem<float, RW_RB_SMALL>::bytes(max_nv);
+    return gen ? RowSmem<float, RW_RB_LARGE, RW_KT_GEN>::bytes(max_nv) : RowSmem<float, RW_RB_LARGE>::bytes(max_nv);
 }
 
 // The dynamic shared memory limit is a per-device function attribute: set it on the current
 // device for every instance (daxm_create calls this on the plan's device).
 cudaError_t row_set_attributes(int max_nv) {
+    (void)max_nv;
     cudaError_t e;
-    if ((e = set_attr_one<uint16_t, false, RW_RB_SMALL>(max_nv)) != cudaSuccess) return e;
-    if ((e = set_attr_one<uint16_t, false, RW_RB_LARGE>(max_nv)) != cudaSuccess) return e;
-    if ((e = set_attr_one<uint16_t, true, RW_RB_SMALL>(max_nv)) != cudaSuccess) return e;
-    if ((e = set_attr_one<uint16_t, true, RW_RB_LARGE>(max_nv)) != cudaSuccess) return e;
-    if ((e = set_attr_one<float, false, RW_RB_SMALL>(max_nv)) != cudaSuccess) return e;
-    if ((e = set_attr_one<float, false, RW_RB_LARGE>(max_nv)) != cudaSuccess) return e;
-    if ((e = set_attr_one<float, true, RW_RB_SMALL>(max_nv)) != cudaSuccess) return e;
-    return set_attr_one<float, true, RW_RB_LARGE>(max_nv);
+    if ((e = set_attr_rb<uint16_t, RW_RB_SMALL>()) != cudaSuccess) return e;
+    if ((e = set_attr_rb<uint16_t, RW_RB_LARGE>()) != cudaSuccess) return e;
+    if ((e = set_attr_rb<float, RW_RB_SMALL>()) != cudaSuccess) return e;
+    return set_attr_rb<float, RW_RB_LARGE>();
 }
 
 cudaError_t launch_row(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int dtype, int rb,
-                       cudaStream_t st) {
+                       bool gen, cudaStream_t st) {
     if (a.n_list <= 0) return cudaSuccess;
     const int max_nv = a.max_nv;
-    return dtype == DAXM_U16 ? launch_t<uint16_t>(a, in_map, out_map, rb, max_nv, st)
-                             : launch_t<float>(a, in_map, out_map, rb, max_nv, st);
+    return dtype == DAXM_U16 ? launch_t<uint16_t>(a, in_map, out_map, rb, gen, max_nv, st)
+                             : launch_t<float>(a, in_map, out_map, rb, gen, max_nv, st);
 }
 
 cudaError_t launch_row_admit(const RowArgs& a, RowTile* rt, int n_rt, int* d_stats, cudaStream_t st) {

@@ -88,7 +88,9 @@ struct daxm_plan {
     float* d_rcoef = nullptr;
     int* d_rlist = nullptr;                // class lists [small][large][general], each ascending
     std::vector<int> h_rlist;
-    int n_rcls[3] = {0, 0, 0};
+    // row tiles per class, in h_rlist order: separated RB 16 / 32, general-span RB 16 / 32, not admitted
+    static constexpr int N_RCLS = 5;
+    int n_rcls[N_RCLS] = {0, 0, 0, 0, 0};
     unsigned* d_row_err = nullptr;         // DAXM_ROW_CHECK builds: schedule violations
     CUtensorMap row_in_map{}, row_out_map{};
     daxm_plan_stats stats{};
@@ -798,37 +800,42 @@ daxm_status row_prepass(daxm_plan* p, int) {
     CK(cudaMemcpy(ht.data(), p->d_rt, sizeof(RowTile) * n_rt, cudaMemcpyDeviceToHost));
     // the row path needs the same depth-model tolerance as the deposit tiles' (else: old path)
     if ((flags & (FLAG_FIT_NAN | FLAG_MIXED_DIR)) || !(ferr[1] <= MODEL_ERR_MAX) || !(ferr[0] <= 1e-3)) return DAXM_OK;
-    std::vector<int> lists[3];
+    std::vector<int> lists[daxm_plan::N_RCLS];
     p->stats.row_reject_bits = 0;
     for (size_t q = 0; q < n_rt; ++q) {
         p->stats.row_reject_bits |= ht[q].why;
         for (int b = 0; b < 8; ++b)
             if (ht[q].why & (1 << b)) ++p->stats.row_reject[b];
+        if (ht[q].why & RW_WHY_GEN) ++p->stats.row_reject_more;
         const int rb = ht[q].cls & RW_CLS_RB;
-        lists[rb == RW_RB_SMALL ? 0 : rb == RW_RB_LARGE ? 1 : 2].push_back((int)q);
+        const int g2 = (ht[q].cls & RW_CLS_GEN) ? 2 : 0;
+        lists[rb == RW_RB_SMALL ? g2 : rb == RW_RB_LARGE ? 1 + g2 : 4].push_back((int)q);
     }
     p->h_rlist.clear();
-    for (int c = 0; c < 3; ++c) {
+    for (int c = 0; c < daxm_plan::N_RCLS; ++c) {
         p->n_rcls[c] = (int)lists[c].size();
         p->h_rlist.insert(p->h_rlist.end(), lists[c].begin(), lists[c].end());
     }
     CK(cudaMalloc(&p->d_rlist, sizeof(int) * std::max<size_t>(p->h_rlist.size(), 1)));
     CK(cudaMemcpy(p->d_rlist, p->h_rlist.data(), sizeof(int) * p->h_rlist.size(), cudaMemcpyHostToDevice));
     CK(row_set_attributes(p->max_nv_row));
-    p->stats.row_tiles_small = p->n_rcls[0];
-    p->stats.row_tiles_large = p->n_rcls[1];
-    p->stats.row_tiles_general = p->n_rcls[2];
+    p->stats.row_tiles_small = p->n_rcls[0] + p->n_rcls[2];
+    p->stats.row_tiles_large = p->n_rcls[1] + p->n_rcls[3];
+    p->stats.row_tiles_gen = p->n_rcls[2] + p->n_rcls[3];
+    p->stats.row_tiles_general = p->n_rcls[4];
+    p->stats.row_launches = 0;
+    for (int c = 0; c < daxm_plan::N_RCLS; ++c) p->stats.row_launches += p->n_rcls[c] > 0;
     p->stats.row_ring_need_max = hs[3];
     // one path per plan: the row-segment kernel when it admits every row tile, else the deposit-tile
     // kernels (step-locked, fast, general) of round 1, which cover the overlapping-span regime
-    if (p->n_rcls[2] > 0 && getenv("DAXM_ROW_PARTIAL") == nullptr) return DAXM_OK;
+    if (p->n_rcls[4] > 0 && getenv("DAXM_ROW_PARTIAL") == nullptr) return DAXM_OK;
     p->stats.fit_max_err_bins = std::max(p->stats.fit_max_err_bins, ferr[0]);
     p->stats.fit_model_err_bins = std::max(p->stats.fit_model_err_bins, ferr[1]);
     p->stats.device_bytes += (int64_t)(sizeof(RowTile) * n_rt + sizeof(float) * n_rt * NCOEF * (RW_COLS + 1) * RW_ROWS +
                                        sizeof(int) * p->h_rlist.size());
     p->row_ok = true;
     p->stats.row_path = 1;
-    if (p->n_rcls[1] + p->n_rcls[2] > 0 && !p->st_cls[0]) {  // class launches fork onto two streams
+    if (p->n_rcls[1] + p->n_rcls[2] + p->n_rcls[3] + p->n_rcls[4] > 0 && !p->st_cls[0]) {  // class launches fork
         for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&p->st_cls[i], cudaStreamNonBlocking));
         for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&p->ev_cls[i], cudaEventDisableTiming));
     }
@@ -1324,8 +1331,9 @@ static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_o
         ra = g0 <= p->row_org ? 0 : (g0 - p->row_org) / RW_ROWS;
         rb = g1 >= p->g.row_end ? p->n_rr : std::max(0, (g1 - p->row_org) / RW_ROWS);
     }
-    int seg[3][2], n_launch = 0, off = 0;
-    for (int c = 0; c < 3; ++c) {
+    constexpr int NC = daxm_plan::N_RCLS;
+    int seg[NC][2], n_launch = 0, off = 0;
+    for (int c = 0; c < NC; ++c) {
         const int* b0 = p->h_rlist.data() + off;
         const int* b1 = b0 + p->n_rcls[c];
         seg[c][0] = (int)(std::lower_bound(b0, b1, ra * p->n_rc) - p->h_rlist.data());
@@ -1342,16 +1350,20 @@ static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_o
     }
     RowArgs a = make_row_args(p);
     a.stack = d_stack;
-    for (int c = 0; c < 2 && e == cudaSuccess; ++c) {
+    // launches in class order, spread over the three streams (largest classes first on separate ones)
+    int li = 0;
+    for (int c = 0; c < NC - 1 && e == cudaSuccess; ++c) {
         a.list = p->d_rlist + seg[c][0];
         a.n_list = seg[c][1] - seg[c][0];
-        e = launch_row(a, &p->row_in_map, &p->row_out_map, dt, c == 0 ? RW_RB_SMALL : RW_RB_LARGE, sts[c]);
+        if (a.n_list <= 0) continue;
+        e = launch_row(a, &p->row_in_map, &p->row_out_map, dt, (c & 1) == 0 ? RW_RB_SMALL : RW_RB_LARGE, c >= 2,
+                       sts[li++ % 3]);
     }
-    if (e == cudaSuccess && seg[2][1] > seg[2][0]) {
+    if (e == cudaSuccess && seg[NC - 1][1] > seg[NC - 1][0]) {
         DepositArgs ga = make_args(p, dt);
         ga.stack = d_stack;
-        e = launch_general_rows(ga, p->d_rlist + seg[2][0], seg[2][1] - seg[2][0], p->n_rc, p->row_org, d_stack, dt,
-                                d_out, sts[2]);
+        e = launch_general_rows(ga, p->d_rlist + seg[NC - 1][0], seg[NC - 1][1] - seg[NC - 1][0], p->n_rc, p->row_org,
+                                d_stack, dt, d_out, sts[li++ % 3]);
     }
     if (fork) {  // join even after a failed launch, so a capture or the caller's stream stays consistent
         for (int i = 0; i < 2; ++i) {

@@ -14,6 +14,7 @@ for name in sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"]:
         st = plan.stats()
     rej = {w: n for w, n in zip(WHY, st["row_reject"]) if n}
     print(name, json.dumps({"small": st["row_tiles_small"], "large": st["row_tiles_large"],
-                            "general": st["row_tiles_general"], "need": st["row_ring_need_max"], "reject": rej,
+                            "general": st["row_tiles_general"], "gen": st["row_tiles_gen"], "rej_gen": st["row_reject_more"],
+                            "row_path": st["row_path"], "need": st["row_ring_need_max"], "reject": rej,
                             "model_err": st["fit_model_err_bins"], "max_err": st["fit_max_err_bins"],
                             "prepass_ms": st["prepass_ms"]}), flush=True)

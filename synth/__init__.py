@@ -152,6 +152,20 @@ def geometry(cfg: Config | str, edge: str = "leading", pixel_model: str = "finit
     )
 
 
+def crop_geometry(cfg: Config | str, row0: int, col0: int, n_rows: int, n_cols: int, **kw) -> dict:
+    """The geometry of the detector window rows [row0, row0 + n_rows) x columns [col0, col0 + n_cols)
+    of `cfg`'s detector: the same pixels, in the same lab positions (det_trans shifted in the
+    detector plane by the window centre's offset), so a small test sees the depth spans and
+    step spacings of any region of a full-size configuration."""
+    if isinstance(cfg, str):
+        cfg = get_config(cfg)
+    g = geometry(cfg, n_rows=n_rows, n_cols=n_cols, **kw)
+    dx = (col0 + (n_cols - 1) / 2.0 - (cfg.n - 1) / 2.0) * cfg.pitch
+    dy = (row0 + (n_rows - 1) / 2.0 - (cfg.n - 1) / 2.0) * cfg.pitch
+    g["det_trans"] = (DET_TRANS[0] + dx, DET_TRANS[1] + dy, DET_TRANS[2])
+    return g
+
+
 # ----------------------------------------------------------------------------
 # Integer stack recipe
 # ----------------------------------------------------------------------------

@@ -144,6 +144,28 @@ def test_full_size_sampled(daxm, name, noise, dtype, fraction):
     parity.check(gpu, ref, series.T, f"{name} {cfg.dtype} sampled fraction={fraction}")
 
 
+@pytest.mark.parametrize("col0,expect", [(1344, "wide"), (1856, "overlap"), (1700, "mixed"), (256, "separated")])
+@pytest.mark.parametrize("dtype", ["u16", "f32"])
+def test_c5_regions_element_by_element(daxm, col0, expect, dtype):
+    """64 x 128 windows of the C5 detector (synth.crop_geometry: the same pixel positions, so the
+    same depth spans and step spacings) where the edge spans are 2-3 bins wide ("wide"), where
+    consecutive spans overlap ("overlap", up to 1.5x the step), across the transition ("mixed")
+    and in the separated regime: every row tile runs the row kernel -- the general-span variant
+    in the first three -- and every output element is within tolerance of the
+    oracle's."""
+    g = synth.crop_geometry("C5", 1000, col0, 64, 128)
+    S = g["wire_xyz"].shape[0]
+    rng = np.random.default_rng(col0)
+    host = (20000 + rng.integers(-3000, 3000, (S, 64, 128))).astype(np.uint16 if dtype == "u16" else np.float32)
+    gpu, st = run_gpu(daxm, g, host)
+    assert st["row_path"] == 1, st
+    if expect == "separated":
+        assert st["row_tiles_gen"] == 0
+    else:
+        assert st["row_tiles_gen"] > 0, st
+    parity.check(gpu, oracle.reconstruct(g, host), host, f"C5 window col0={col0} {dtype}")
+
+
 # ------------------------------------------------------------------ edge cases
 
 def test_ragged_detector(daxm):

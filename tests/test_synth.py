@@ -63,3 +63,14 @@ def test_travel_sweeps_bins_at_every_corner_pixel():
                 d0 = oracle.tangent_depth(Q, W[0], axis, g["wire_radius"], s, g["beam_dir"], g["beam_origin"])
                 d1 = oracle.tangent_depth(Q, W[-1], axis, g["wire_radius"], s, g["beam_dir"], g["beam_origin"])
                 assert min(d0, d1) < lo0 - 2 and max(d0, d1) > hi + 2, (name, x, j, edge, d0, d1)
+
+
+def test_crop_geometry_keeps_pixel_positions():
+    """A cropped detector's pixel (j, i) sits where the full detector's (row0 + j, col0 + i) does."""
+    import indep
+    g = synth.geometry("C5")
+    c = synth.crop_geometry("C5", 1000, 1792, 64, 128)
+    for (j, i) in [(0, 0), (63, 127), (10, 77)]:
+        a = indep.detector_xyz(c, i, j)
+        b = indep.detector_xyz(g, 1792 + i, 1000 + j)
+        assert np.allclose(a, b, rtol=0, atol=1e-6)
