@@ -191,6 +191,8 @@ constexpr int RW_RB_SMALL = 16, RW_RB_LARGE = 32;  // output ring planes (+ RW_K
 constexpr int RW_CLS_RB = 0xff;         // RowTile.cls: ring planes (0: not admitted -> general kernel)
 constexpr int RW_CLS_FRONT_LO = 0x100;  //   the front pixel edge is the shallower one over the tile
 constexpr int RW_CLS_GEN = 0x200;       //   general-span variant (overlapping spans, spans up to RW_NQ_GEN bins)
+constexpr int RW_CLS_NB_WIDE = 0x400;   //   general-span variant with the RW_NB_WIDE-slot input ring
+constexpr int RW_NB_WIDE = 64;          // input ring slots for tiles whose visits spread wider than RW_NB
 constexpr int RW_KT_GEN = 6;            // max bin edges per zone and iteration, general-span variant
 constexpr int RW_NQ_GEN = 4;            // general-span variant: zone edges evaluated exactly (then linear)
 static_assert(RW_ROWS * RW_COLS == 128 && RW_COLS % 32 == 0 && (RW_ROWS == 2 || RW_ROWS == 4),
@@ -281,10 +283,9 @@ cudaError_t launch_lock(const DepositArgs& a, const CUtensorMap* in_map, float* 
 cudaError_t launch_lock_prepass(const DepositArgs& a, int n_tiles, int* d_stats, cudaStream_t st);
 // row-segment kernel (deposit_row.cu): pre-pass replay (admission) and the class launches
 cudaError_t launch_row_admit(const RowArgs& a, RowTile* rt, int n_rt, int* d_stats, cudaStream_t st);
-size_t row_smem_bytes(int dtype, int rb, bool gen, int max_nv);
-cudaError_t row_set_attributes(int max_nv);  // per device: dynamic shared memory of every instance
+cudaError_t row_set_attributes();  // per device: dynamic shared memory of every instance
 cudaError_t launch_row(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int dtype, int rb,
-                       bool gen, cudaStream_t st);
+                       int variant, cudaStream_t st);  // variant: 0 separated, 1 general-span, 2 + wide input ring
 cudaError_t launch_general_rows(const DepositArgs& a, const int* rt_list, int n, int n_rc, int row_org,
                                 const void* stack, int dtype, float* out, cudaStream_t st);
 

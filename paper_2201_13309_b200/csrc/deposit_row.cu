@@ -56,14 +56,13 @@ namespace {
 using namespace ptx;
 
 constexpr int PLANE_B = RW_ROWS * RW_COLS * 4;  // one staged output plane (512 B)
-constexpr int NG = RW_NB / RW_G;                // input groups in the ring
-
-template <typename T, int RB, int KT = RW_KT>
+template <typename T, int RB, int KT = RW_KT, int NB = RW_NB>
 struct RowSmem {
+    static constexpr int NG = NB / RW_G;  // input groups in the ring
     static constexpr int OUT_SLOTS = RB + KT - 1;
     static constexpr int IN_SLOT = RW_ROWS * 32 * (int)sizeof(T);  // one step of one column half
     static constexpr int IN_GROUP = RW_G * IN_SLOT;                // one TMA box
-    static constexpr int IN_HALF = RW_NB * IN_SLOT;                // a half's ring
+    static constexpr int IN_HALF = NB * IN_SLOT;                   // a half's ring
     static constexpr int OFF_OUT = 0;
     static constexpr int OFF_IN = OFF_OUT + OUT_SLOTS * PLANE_B;
     static constexpr int OFF_BAR = OFF_IN + RW_H * IN_HALF;
@@ -246,13 +245,14 @@ __device__ __forceinline__ void row_starts(const RowWalk wk[2][2], int lane, int
     vend = __reduce_max_sync(0xffffffffu, ve);
 }
 
-template <typename T, bool POINT, int RB, bool GEN>
+template <typename T, bool POINT, int RB, bool GEN, int NB>
 __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_constant__ CUtensorMap in_map,
                                                             const __grid_constant__ CUtensorMap out_map,
                                                             const RowArgs a) {
     static_assert(!(GEN && POINT), "the general-span variant is for finite pixels");
     constexpr int KT = GEN ? RW_KT_GEN : RW_KT;  // max edges per zone and iteration
-    using L = RowSmem<T, RB, KT>;
+    using L = RowSmem<T, RB, KT, NB>;
+    constexpr int NG = L::NG;
     static_assert(RB % RW_PB == 0 && (RB & (RB - 1)) == 0, "ring");
     extern __shared__ unsigned char smem_raw[];
     const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
     // wire travel and the two pairs' intensities (rows 0, 1) at visit v of the lane's half
     auto fetch = [&](int v, float& t, float2 I[2]) {
         t = lds_f32(tau_l + 4u * (uint32_t)v);
-        const uint32_t ad = in_lane + (uint32_t)((v ^ xr_) & (RW_NB - 1)) * (uint32_t)L::IN_SLOT;
+        const uint32_t ad = in_lane + (uint32_t)((v ^ xr_) & (NB - 1)) * (uint32_t)L::IN_SLOT;
         if constexpr (sizeof(T) == 2) {
             const uint32_t w0 = __byte_perm(lds_u32(ad), 0u, swap), w1 = __byte_perm(lds_u32(ad + 64u), 0u, swap);
             I[0] = make_float2((float)(w0 & 0xffffu), (float)(w1 & 0xffffu));
@@ -477,14 +477,14 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
     // bounds the replay checks with the same formulas (deadlock-free iff the latter's group is loadable).
     int it2 = 2;  // it + 2 of the transition about to run (it reads visit vs + it2)
     // the next it2 at which group g_issue becomes loadable / group g_wait is needed (warp-uniform)
-    int next_issue = g_issue >= ngroups ? INT_MAX : RW_G * g_issue + RW_G - RW_NB;
+    int next_issue = g_issue >= ngroups ? INT_MAX : RW_G * g_issue + RW_G - NB;
     int next_wait = g_wait * RW_G > need_end ? INT_MAX : RW_G * g_wait - need_hi;
     // input rings: refill the slots every lane has read past (group g is loadable from it2 = 4 g + 4 -
     // NB on) and wait for what the next `ahead` + 1 transitions read (visit need_hi + it2 + ahead)
     auto input = [&](int ahead) {
         if (it2 >= next_issue) {
-            issue_upto((int)((unsigned)(it2 + RW_NB - RW_G) / RW_G));
-            next_issue = g_issue >= ngroups ? INT_MAX : RW_G * g_issue + RW_G - RW_NB;
+            issue_upto((int)((unsigned)(it2 + NB - RW_G) / RW_G));
+            next_issue = g_issue >= ngroups ? INT_MAX : RW_G * g_issue + RW_G - NB;
         }
         if (it2 + ahead >= next_wait) {
             const int need = min(need_hi + it2 + ahead, need_end);
@@ -755,6 +755,7 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
     // reasons only the separated / only the general-span variant has
     unsigned bad_sep = (!empty && ti.sep != MODE_SEPARATED) ? RW_WHY_MODE : 0u;
     unsigned bad_gen = a.point_mode ? RW_WHY_MODE : 0u;
+    unsigned bad_in[2] = {0u, 0u};  // input ring of RW_NB / RW_NB_WIDE slots
     bool back_lo = true, front_lo = true;
     int need = 0, iters = 0;
     if (eligible) {
@@ -804,9 +805,13 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
                 phm[p][r] = phmm[p][r] = lo;
                 ndone[p][r] = 0;
             }
+        // input ring of RW_NB (index 0) or RW_NB_WIDE (index 1) slots per half: the same schedule,
+        // loads issued further ahead with the wider ring
         const int ngroups = vend / RW_G + 1;
-        int g_issue = min(NG, ngroups);
-        if (__reduce_max_sync(0xffffffffu, min(vs + 1, ve)) / RW_G >= g_issue) bad |= RW_WHY_INPUT;
+        constexpr int NBs[2] = {RW_NB, RW_NB_WIDE};
+        int g_issue[2] = {min(RW_NB / RW_G, ngroups), min(RW_NB_WIDE / RW_G, ngroups)};
+        for (int b = 0; b < 2; ++b)
+            if (__reduce_max_sync(0xffffffffu, min(vs + 1, ve)) / RW_G >= g_issue[b]) bad_in[b] = RW_WHY_INPUT;
         auto frontier = [&]() {
             return __reduce_min_sync(
                 0xffffffffu, (int)fminf(fminf(En[0][0], En[0][1]), fminf(En[1][0], En[1][1])) + a.m_ref);
@@ -825,9 +830,11 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
             const int n = iters - 1;
             if (n == 0 || (n - 1) % RW_G == 0) {
                 const int it2 = n + 2, ahead = n == 0 ? 0 : RW_G - 1;
-                g_issue = max(g_issue, min((it2 + RW_NB - RW_G) / RW_G, ngroups - 1) + 1);
                 const int nd_ = min(vs_max + it2 + ahead, vend);
-                if (nd_ / RW_G >= g_issue) bad |= RW_WHY_INPUT;  // would wait for a group not yet loadable
+                for (int b = 0; b < 2; ++b) {
+                    g_issue[b] = max(g_issue[b], min((it2 + NBs[b] - RW_G) / RW_G, ngroups - 1) + 1);
+                    if (nd_ / RW_G >= g_issue[b]) bad_in[b] = RW_WHY_INPUT;  // would wait for a group not yet loadable
+                }
             }
             int kmax = 0, pmax = INT_MIN;
             for (int p = 0; p < 2; ++p) {
@@ -894,18 +901,25 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
     bad = __reduce_or_sync(0xffffffffu, bad);
     bad_sep = __reduce_or_sync(0xffffffffu, bad_sep);
     bad_gen = __reduce_or_sync(0xffffffffu, bad_gen);
+    bad_in[0] = __reduce_or_sync(0xffffffffu, bad_in[0]);
+    bad_in[1] = __reduce_or_sync(0xffffffffu, bad_in[1]);
     back_lo = __all_sync(0xffffffffu, back_lo);
     front_lo = __all_sync(0xffffffffu, front_lo);
     if (lane == 0) {
         int cls = 0;
         if (!(back_lo || front_lo)) bad |= RW_WHY_ORDER;
         if (need > RW_RB_LARGE) bad |= RW_WHY_RING;
-        if (!bad && (!bad_sep || !bad_gen)) {
+        // first that applies: separated variant, general-span variant, general-span with the wide
+        // input ring (fewer warps per SM)
+        const int variant = !bad && !bad_sep && !bad_in[0] ? 0 : !bad && !bad_gen && !bad_in[0] ? 1
+                          : !bad && !bad_gen && !bad_in[1] ? 2 : -1;
+        if (variant >= 0) {
             cls = need <= RW_RB_SMALL ? RW_RB_SMALL : RW_RB_LARGE;
             if (!back_lo) cls |= RW_CLS_FRONT_LO;
-            if (bad_sep) cls |= RW_CLS_GEN;  // the separated variant does not apply: the general-span one
+            if (variant >= 1) cls |= RW_CLS_GEN;
+            if (variant == 2) cls |= RW_CLS_NB_WIDE;
         } else {
-            bad |= bad_sep | bad_gen;
+            bad |= bad_sep | bad_gen | bad_in[0] | bad_in[1];
         }
         ti.cls = cls;
         ti.why = (int)bad;
@@ -916,66 +930,57 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
     }
 }
 
-template <typename T, bool POINT, int RB, bool GEN>
-using RowSmemOf = RowSmem<T, RB, GEN ? RW_KT_GEN : RW_KT>;
+// kernel variants: 0 separated, 1 general-span, 2 general-span with the wide input ring
+template <typename T, bool POINT, int RB, int V>
+struct RowVariant {
+    static constexpr bool GEN = V >= 1;
+    static constexpr int NB = V == 2 ? RW_NB_WIDE : RW_NB;
+    using Smem = RowSmem<T, RB, GEN ? RW_KT_GEN : RW_KT, NB>;
+    static constexpr auto kernel = deposit_row<T, POINT, RB, GEN, NB>;
+};
 
-template <typename T, bool POINT, int RB, bool GEN>
+template <typename T, bool POINT, int RB, int V>
 cudaError_t set_attr_one() {
-    cudaError_t e = cudaFuncSetAttribute(deposit_row<T, POINT, RB, GEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)RowSmemOf<T, POINT, RB, GEN>::bytes(MAX_FAST_NV));
+    using K = RowVariant<T, POINT, RB, V>;
+    cudaError_t e = cudaFuncSetAttribute(K::kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)K::Smem::bytes(MAX_FAST_NV));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(deposit_row<T, POINT, RB, GEN>, cudaFuncAttributePreferredSharedMemoryCarveout,
+    return cudaFuncSetAttribute(K::kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                                 (int)cudaSharedmemCarveoutMaxShared);
 }
 
-template <typename T, bool POINT, int RB, bool GEN>
-cudaError_t launch_one(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int max_nv,
-                       cudaStream_t st) {
-    const size_t sm = RowSmemOf<T, POINT, RB, GEN>::bytes(max_nv);
-    deposit_row<T, POINT, RB, GEN><<<(unsigned)a.n_list, 32, sm, st>>>(*in_map, *out_map, a);
+template <typename T, bool POINT, int RB, int V>
+cudaError_t launch_one(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, cudaStream_t st) {
+    using K = RowVariant<T, POINT, RB, V>;
+    K::kernel<<<(unsigned)a.n_list, 32, K::Smem::bytes(a.max_nv), st>>>(*in_map, *out_map, a);
     return cudaGetLastError();
 }
 
 template <typename T, int RB>
-cudaError_t launch_rb(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, bool gen, int max_nv,
+cudaError_t launch_rb(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int variant,
                       cudaStream_t st) {
-    if (a.point_mode) return launch_one<T, true, RB, false>(a, in_map, out_map, max_nv, st);
-    return gen ? launch_one<T, false, RB, true>(a, in_map, out_map, max_nv, st)
-               : launch_one<T, false, RB, false>(a, in_map, out_map, max_nv, st);
-}
-
-template <typename T>
-cudaError_t launch_t(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int rb, bool gen,
-                     int max_nv, cudaStream_t st) {
-    return rb == RW_RB_SMALL ? launch_rb<T, RW_RB_SMALL>(a, in_map, out_map, gen, max_nv, st)
-                             : launch_rb<T, RW_RB_LARGE>(a, in_map, out_map, gen, max_nv, st);
+    if (a.point_mode) return launch_one<T, true, RB, 0>(a, in_map, out_map, st);
+    switch (variant) {
+        case 0: return launch_one<T, false, RB, 0>(a, in_map, out_map, st);
+        case 1: return launch_one<T, false, RB, 1>(a, in_map, out_map, st);
+        default: return launch_one<T, false, RB, 2>(a, in_map, out_map, st);
+    }
 }
 
 template <typename T, int RB>
 cudaError_t set_attr_rb() {
     cudaError_t e;
-    if ((e = set_attr_one<T, false, RB, false>()) != cudaSuccess) return e;
-    if ((e = set_attr_one<T, true, RB, false>()) != cudaSuccess) return e;
-    return set_attr_one<T, false, RB, true>();
+    if ((e = set_attr_one<T, true, RB, 0>()) != cudaSuccess) return e;
+    if ((e = set_attr_one<T, false, RB, 0>()) != cudaSuccess) return e;
+    if ((e = set_attr_one<T, false, RB, 1>()) != cudaSuccess) return e;
+    return set_attr_one<T, false, RB, 2>();
 }
 
 }  // namespace
 
-size_t row_smem_bytes(int dtype, int rb, bool gen, int max_nv) {
-    if (dtype == DAXM_U16) {
-        if (rb == RW_RB_SMALL)
-            return gen ? RowSmem<uint16_t, RW_RB_SMALL, RW_KT_GEN>::bytes(max_nv) : RowSmem<uint16_t, RW_RB_SMALL>::bytes(max_nv);
-        return gen ? RowSmem<uint16_t, RW_RB_LARGE, RW_KT_GEN>::bytes(max_nv) : RowSmem<uint16_t, RW_RB_LARGE>::bytes(max_nv);
-    }
-    if (rb == RW_RB_SMALL)
-        return gen ? RowSmem<float, RW_RB_SMALL, RW_KT_GEN>::bytes(max_nv) : RowSmem<float, RW_RB_SMALL>::bytes(max_nv);
-    return gen ? RowSmem<float, RW_RB_LARGE, RW_KT_GEN>::bytes(max_nv) : RowSmem<float, RW_RB_LARGE>::bytes(max_nv);
-}
-
 // The dynamic shared memory limit is a per-device function attribute: set it on the current
 // device for every instance (daxm_create calls this on the plan's device).
-cudaError_t row_set_attributes(int max_nv) {
-    (void)max_nv;
+cudaError_t row_set_attributes() {
     cudaError_t e;
     if ((e = set_attr_rb<uint16_t, RW_RB_SMALL>()) != cudaSuccess) return e;
     if ((e = set_attr_rb<uint16_t, RW_RB_LARGE>()) != cudaSuccess) return e;
@@ -984,11 +989,13 @@ cudaError_t row_set_attributes(int max_nv) {
 }
 
 cudaError_t launch_row(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int dtype, int rb,
-                       bool gen, cudaStream_t st) {
+                       int variant, cudaStream_t st) {
     if (a.n_list <= 0) return cudaSuccess;
-    const int max_nv = a.max_nv;
-    return dtype == DAXM_U16 ? launch_t<uint16_t>(a, in_map, out_map, rb, gen, max_nv, st)
-                             : launch_t<float>(a, in_map, out_map, rb, gen, max_nv, st);
+    if (dtype == DAXM_U16)
+        return rb == RW_RB_SMALL ? launch_rb<uint16_t, RW_RB_SMALL>(a, in_map, out_map, variant, st)
+                                 : launch_rb<uint16_t, RW_RB_LARGE>(a, in_map, out_map, variant, st);
+    return rb == RW_RB_SMALL ? launch_rb<float, RW_RB_SMALL>(a, in_map, out_map, variant, st)
+                             : launch_rb<float, RW_RB_LARGE>(a, in_map, out_map, variant, st);
 }
 
 cudaError_t launch_row_admit(const RowArgs& a, RowTile* rt, int n_rt, int* d_stats, cudaStream_t st) {

@@ -88,9 +88,10 @@ struct daxm_plan {
     float* d_rcoef = nullptr;
     int* d_rlist = nullptr;                // class lists [small][large][general], each ascending
     std::vector<int> h_rlist;
-    // row tiles per class, in h_rlist order: separated RB 16 / 32, general-span RB 16 / 32, not admitted
-    static constexpr int N_RCLS = 5;
-    int n_rcls[N_RCLS] = {0, 0, 0, 0, 0};
+    // row tiles per class, in h_rlist order: ring 16 / 32 x (separated, general-span, general-span
+    // with the wide input ring) = class 2 variant + (ring 32), then the not admitted ones
+    static constexpr int N_RCLS = 7;
+    int n_rcls[N_RCLS] = {0, 0, 0, 0, 0, 0, 0};
     unsigned* d_row_err = nullptr;         // DAXM_ROW_CHECK builds: schedule violations
     CUtensorMap row_in_map{}, row_out_map{};
     daxm_plan_stats stats{};
@@ -808,8 +809,8 @@ daxm_status row_prepass(daxm_plan* p, int) {
             if (ht[q].why & (1 << b)) ++p->stats.row_reject[b];
         if (ht[q].why & RW_WHY_GEN) ++p->stats.row_reject_more;
         const int rb = ht[q].cls & RW_CLS_RB;
-        const int g2 = (ht[q].cls & RW_CLS_GEN) ? 2 : 0;
-        lists[rb == RW_RB_SMALL ? g2 : rb == RW_RB_LARGE ? 1 + g2 : 4].push_back((int)q);
+        const int var = (ht[q].cls & RW_CLS_NB_WIDE) ? 2 : (ht[q].cls & RW_CLS_GEN) ? 1 : 0;
+        lists[rb == RW_RB_SMALL ? 2 * var : rb == RW_RB_LARGE ? 2 * var + 1 : 6].push_back((int)q);
     }
     p->h_rlist.clear();
     for (int c = 0; c < daxm_plan::N_RCLS; ++c) {
@@ -818,24 +819,24 @@ daxm_status row_prepass(daxm_plan* p, int) {
     }
     CK(cudaMalloc(&p->d_rlist, sizeof(int) * std::max<size_t>(p->h_rlist.size(), 1)));
     CK(cudaMemcpy(p->d_rlist, p->h_rlist.data(), sizeof(int) * p->h_rlist.size(), cudaMemcpyHostToDevice));
-    CK(row_set_attributes(p->max_nv_row));
-    p->stats.row_tiles_small = p->n_rcls[0] + p->n_rcls[2];
-    p->stats.row_tiles_large = p->n_rcls[1] + p->n_rcls[3];
-    p->stats.row_tiles_gen = p->n_rcls[2] + p->n_rcls[3];
-    p->stats.row_tiles_general = p->n_rcls[4];
+    CK(row_set_attributes());
+    p->stats.row_tiles_small = p->n_rcls[0] + p->n_rcls[2] + p->n_rcls[4];
+    p->stats.row_tiles_large = p->n_rcls[1] + p->n_rcls[3] + p->n_rcls[5];
+    p->stats.row_tiles_gen = p->n_rcls[2] + p->n_rcls[3] + p->n_rcls[4] + p->n_rcls[5];
+    p->stats.row_tiles_general = p->n_rcls[6];
     p->stats.row_launches = 0;
     for (int c = 0; c < daxm_plan::N_RCLS; ++c) p->stats.row_launches += p->n_rcls[c] > 0;
     p->stats.row_ring_need_max = hs[3];
     // one path per plan: the row-segment kernel when it admits every row tile, else the deposit-tile
     // kernels (step-locked, fast, general) of round 1, which cover the overlapping-span regime
-    if (p->n_rcls[4] > 0 && getenv("DAXM_ROW_PARTIAL") == nullptr) return DAXM_OK;
+    if (p->n_rcls[6] > 0 && getenv("DAXM_ROW_PARTIAL") == nullptr) return DAXM_OK;
     p->stats.fit_max_err_bins = std::max(p->stats.fit_max_err_bins, ferr[0]);
     p->stats.fit_model_err_bins = std::max(p->stats.fit_model_err_bins, ferr[1]);
     p->stats.device_bytes += (int64_t)(sizeof(RowTile) * n_rt + sizeof(float) * n_rt * NCOEF * (RW_COLS + 1) * RW_ROWS +
                                        sizeof(int) * p->h_rlist.size());
     p->row_ok = true;
     p->stats.row_path = 1;
-    if (p->n_rcls[1] + p->n_rcls[2] + p->n_rcls[3] + p->n_rcls[4] > 0 && !p->st_cls[0]) {  // class launches fork
+    if (p->stats.row_launches > 1 && !p->st_cls[0]) {  // class launches fork
         for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&p->st_cls[i], cudaStreamNonBlocking));
         for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&p->ev_cls[i], cudaEventDisableTiming));
     }
@@ -1356,7 +1357,7 @@ static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_o
         a.list = p->d_rlist + seg[c][0];
         a.n_list = seg[c][1] - seg[c][0];
         if (a.n_list <= 0) continue;
-        e = launch_row(a, &p->row_in_map, &p->row_out_map, dt, (c & 1) == 0 ? RW_RB_SMALL : RW_RB_LARGE, c >= 2,
+        e = launch_row(a, &p->row_in_map, &p->row_out_map, dt, (c & 1) == 0 ? RW_RB_SMALL : RW_RB_LARGE, c / 2,
                        sts[li++ % 3]);
     }
     if (e == cudaSuccess && seg[NC - 1][1] > seg[NC - 1][0]) {
