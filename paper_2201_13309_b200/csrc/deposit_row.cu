@@ -516,7 +516,10 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
             constexpr int p = decltype(pc)::value;
             const float2 lo = poly2(cb[p], f2(S.tq)), hi = POINT ? lo : poly2(cf[p], f2(S.tq));
             const float2 s = add2(lo, hi);
-            const float2 c = mul2(mul2(sdir2, sub2(S.pI[p], S.Iq[p])), rcp2(sub2(s, S.ps[p])));
+            // trapezoid height c = dI / area: twice the area is s - ps for separated spans and
+            // (hi - lo_v) + |hi_v - lo| in general (the sorted corners' two parallel sides)
+            const float2 dn = GEN ? add2(sub2(hi, S.plo[p]), abs2(sub2(S.phi[p], lo))) : sub2(s, S.ps[p]);
+            const float2 c = mul2(mul2(sdir2, sub2(S.pI[p], S.Iq[p])), rcp2(dn));
             // edges of the zone [plo, lo): En .. floor(min(lo, EM))
             const float2 fl = add2(floor2(min2(lo, f2(EM))), f2(1.f));
             const float2 cnt = sub2(fl, add2(S.En[p], gate[p]));
