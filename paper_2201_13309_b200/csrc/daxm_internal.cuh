@@ -241,6 +241,7 @@ struct RowArgs {
     const void* stack;     // band stack (plane 0 read for the intensity cutoff)
     int use_cutoff;
     float cutoff;
+    int zero_skip;         // scan for tiles whose intensities never change (exact zero output)
     unsigned* err;         // DAXM_ROW_CHECK builds: schedule violations (must stay 0)
 };
 

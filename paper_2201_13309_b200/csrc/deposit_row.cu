@@ -311,6 +311,45 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
             }
         }
     }
+    // Exact zero-dI skip: if no active walk's intensity ever changes over the tile's step range, every
+    // dI is 0, so every bin value the walks would store is exactly 0 -- the same output as the
+    // zero path below.  The warp reads the tile's intensities (coalesced, 16 steps per round) until
+    // some active walk differs from its first value; a tile with any change runs in full.
+    if (a.zero_skip && __any_sync(0xffffffffu, any_act)) {
+        const int h = lane >> 4, i2 = 2 * (lane & 15);
+        const int c0 = col0 + 32 * h + i2;  // the lane's two columns (walk pairs 0 / 1 in some order)
+        const T* base = static_cast<const T*>(a.stack);
+        const size_t plane = (size_t)(a.row_end - a.row_begin) * a.C;
+        bool rok[2];
+        size_t roff[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int j = row0 + r;
+            rok[r] = j >= a.row_begin && j < a.row_end;
+            roff[r] = rok[r] ? (size_t)(j - a.row_begin) * a.C + c0 : 0;
+        }
+        const bool col2 = c0 + 1 < a.C;  // second column inside the detector
+        using U = std::conditional_t<sizeof(T) == 2, unsigned short, unsigned int>;
+        auto word = [&](int k, int r) -> uint64_t {  // both columns' bits at step k, row r
+            if (!rok[r] || c0 >= a.C) return 0;
+            const U* q = reinterpret_cast<const U*>(base + (size_t)k * plane + roff[r]);
+            const uint64_t lo = __ldg(q), hi = col2 ? (uint64_t)__ldg(q + 1) : 0;
+            return lo | (hi << 32);
+        };
+        const uint64_t w0 = word(ti.k_lo, 0), w1 = word(ti.k_lo, 1);
+        bool var = false;
+        for (int k0 = ti.k_lo + 1; k0 <= ti.k_hi; k0 += 16) {
+            uint64_t x = 0;
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+                const int k = min(k0 + u, ti.k_hi);
+                x |= (word(k, 0) ^ w0) | (word(k, 1) ^ w1);
+            }
+            var = x != 0;
+            if (__any_sync(0xffffffffu, var)) break;
+        }
+        if (!__any_sync(0xffffffffu, var)) any_act = false;
+    }
     if (!__any_sync(0xffffffffu, any_act)) {  // no active walk: the tile's output is zero
         fence_proxy_async_smem();
         __syncwarp();

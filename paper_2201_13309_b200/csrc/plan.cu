@@ -1226,6 +1226,7 @@ static RowArgs make_row_args(const daxm_plan* p) {
     a.stack = nullptr;
     a.use_cutoff = p->use_cutoff;
     a.cutoff = p->cutoff;
+    a.zero_skip = getenv("DAXM_NO_ZERO_SKIP") == nullptr;
     a.err = p->d_row_err;
     return a;
 }

@@ -166,6 +166,23 @@ def test_c5_regions_element_by_element(daxm, col0, expect, dtype):
     parity.check(gpu, oracle.reconstruct(g, host), host, f"C5 window col0={col0} {dtype}")
 
 
+@pytest.mark.parametrize("name,dtype", [("C3", "u16"), ("C2", "f32")])
+def test_zero_skip_equals_full_run(daxm, name, dtype, monkeypatch):
+    """The row kernel's exact zero-dI skip (tiles whose intensities never change write zeros
+    without running the deposit) gives the same values as running every tile in full, and the
+    oracle's exact zeros on the constant pixels (noise-free stacks: most tiles constant)."""
+    g = synth.geometry(name)
+    host = synth.stack_numpy(synth.make_maps(name), dtype, noise=False)
+    skip, st = run_gpu(daxm, g, host)
+    assert st["row_path"] == 1
+    monkeypatch.setenv("DAXM_NO_ZERO_SKIP", "1")
+    full, _ = run_gpu(daxm, g, host)
+    assert np.array_equal(skip, full)
+    flat = parity.abs_dI(host) == 0
+    assert flat.mean() > 0.5 and (skip[:, flat] == 0).all()
+    parity.check(skip, oracle.reconstruct(g, host), host, f"{name} zero skip")
+
+
 # ------------------------------------------------------------------ edge cases
 
 def test_ragged_detector(daxm):
