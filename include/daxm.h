@@ -119,8 +119,9 @@ typedef struct {
     int64_t row_tiles_gen;     /* of row_tiles_small + row_tiles_large: tiles the general-span variant    */
                                /* runs (overlapping edge spans or spans of 2-4 bins)      */
     int64_t row_reject_more;   /* row tiles not admitted for RW_WHY_GEN (bit 8)                          */
-    int64_t row_launches;      /* kernel launches of one daxm_reconstruct on the row path (one per       */
-                               /* non-empty class: separated / general-span x ring 16 / 32, general)    */
+    int64_t row_launches;      /* kernel launches of one daxm_reconstruct on the row path: the zero-dI  */
+                               /* scan, then one per non-empty class (separated / general-span / wide   */
+                               /* input ring x ring 16 / 32, general)                                    */
 } daxm_plan_stats;
 
 /* daxm_create -- validate `g`, run the fp64 geometry pre-pass on `cuda_device`,

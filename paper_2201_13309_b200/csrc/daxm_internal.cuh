@@ -241,7 +241,7 @@ struct RowArgs {
     const void* stack;     // band stack (plane 0 read for the intensity cutoff)
     int use_cutoff;
     float cutoff;
-    int zero_skip;         // scan for tiles whose intensities never change (exact zero output)
+    const unsigned char* live;  // [n_rt] per-call row_live_kernel flags (0: zeros written), or NULL
     unsigned* err;         // DAXM_ROW_CHECK builds: schedule violations (must stay 0)
 };
 
@@ -284,7 +284,9 @@ cudaError_t launch_lock(const DepositArgs& a, const CUtensorMap* in_map, float* 
 cudaError_t launch_lock_prepass(const DepositArgs& a, int n_tiles, int* d_stats, cudaStream_t st);
 // row-segment kernel (deposit_row.cu): pre-pass replay (admission) and the class launches
 cudaError_t launch_row_admit(const RowArgs& a, RowTile* rt, int n_rt, int* d_stats, cudaStream_t st);
-cudaError_t row_set_attributes();  // per device: dynamic shared memory of every instance
+cudaError_t row_set_attributes();
+cudaError_t launch_row_live(const RowArgs& a, int rt0, int n, unsigned char* live, float* out, int dtype,
+                            cudaStream_t st);  // exact zero-dI skip over row tiles [rt0, rt0 + n)  // per device: dynamic shared memory of every instance
 cudaError_t launch_row(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int dtype, int rb,
                        int variant, cudaStream_t st);  // variant: 0 separated, 1 general-span, 2 + wide input ring
 cudaError_t launch_general_rows(const DepositArgs& a, const int* rt_list, int n, int n_rc, int row_org,

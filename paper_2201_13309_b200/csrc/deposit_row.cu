@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
     unsigned char* smem = smem_raw + (sbase - smem_u32(smem_raw));
     const int lane = threadIdx.x;
     const int rt = a.list[blockIdx.x];
+    if (a.live && !a.live[rt]) return;  // constant intensities: row_live_kernel wrote the zeros
     const RowTile ti = a.rt[rt];
     const int rr = rt / a.n_rc, rc = rt % a.n_rc;
     const int row0 = a.row_org + rr * RW_ROWS;  // global row of the tile's first row
@@ -310,45 +311,6 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
                 (r ? cf[p][m].y : cf[p][m].x) = ch[m];
             }
         }
-    }
-    // Exact zero-dI skip: if no active walk's intensity ever changes over the tile's step range, every
-    // dI is 0, so every bin value the walks would store is exactly 0 -- the same output as the
-    // zero path below.  The warp reads the tile's intensities (coalesced, 16 steps per round) until
-    // some active walk differs from its first value; a tile with any change runs in full.
-    if (a.zero_skip && __any_sync(0xffffffffu, any_act)) {
-        const int h = lane >> 4, i2 = 2 * (lane & 15);
-        const int c0 = col0 + 32 * h + i2;  // the lane's two columns (walk pairs 0 / 1 in some order)
-        const T* base = static_cast<const T*>(a.stack);
-        const size_t plane = (size_t)(a.row_end - a.row_begin) * a.C;
-        bool rok[2];
-        size_t roff[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const int j = row0 + r;
-            rok[r] = j >= a.row_begin && j < a.row_end;
-            roff[r] = rok[r] ? (size_t)(j - a.row_begin) * a.C + c0 : 0;
-        }
-        const bool col2 = c0 + 1 < a.C;  // second column inside the detector
-        using U = std::conditional_t<sizeof(T) == 2, unsigned short, unsigned int>;
-        auto word = [&](int k, int r) -> uint64_t {  // both columns' bits at step k, row r
-            if (!rok[r] || c0 >= a.C) return 0;
-            const U* q = reinterpret_cast<const U*>(base + (size_t)k * plane + roff[r]);
-            const uint64_t lo = __ldg(q), hi = col2 ? (uint64_t)__ldg(q + 1) : 0;
-            return lo | (hi << 32);
-        };
-        const uint64_t w0 = word(ti.k_lo, 0), w1 = word(ti.k_lo, 1);
-        bool var = false;
-        for (int k0 = ti.k_lo + 1; k0 <= ti.k_hi; k0 += 16) {
-            uint64_t x = 0;
-#pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const int k = min(k0 + u, ti.k_hi);
-                x |= (word(k, 0) ^ w0) | (word(k, 1) ^ w1);
-            }
-            var = x != 0;
-            if (__any_sync(0xffffffffu, var)) break;
-        }
-        if (!__any_sync(0xffffffffu, var)) any_act = false;
     }
     if (!__any_sync(0xffffffffu, any_act)) {  // no active walk: the tile's output is zero
         fence_proxy_async_smem();
@@ -769,6 +731,60 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
 #endif
 }
 
+// ------------------------------------------------------------------ exact zero-dI skip
+// One CTA per row tile of rows [tr0, tr1) x all row-tile columns.  A tile whose intensities are the
+// same at every step of its range [k_lo, k_hi] has every dI = 0, so every bin value the row kernel
+// would store is exactly 0: this kernel writes those zeros (coalesced 256-byte row segments) and
+// clears the tile's live flag, and the row kernel's CTA for the tile returns at once.  The scan
+// reads 16-byte chunks, all threads on distinct (step, row, chunk), and stops at the first round
+// with a change, so a live tile costs one round.  Tiles at the detector's edges, with misaligned
+// rows, or not admitted to the row kernel stay live (no scan).
+template <typename T>
+__global__ void __launch_bounds__(256) row_live_kernel(const RowArgs a, int rt0, int n, unsigned char* __restrict__ live,
+                                                       float* __restrict__ out) {
+    const int rt = rt0 + blockIdx.x;
+    const RowTile ti = a.rt[rt];
+    const int rr = rt / a.n_rc, rc = rt % a.n_rc;
+    const int row0 = a.row_org + rr * RW_ROWS, col0 = rc * RW_COLS;
+    const bool can = (ti.cls & RW_CLS_RB) != 0 && ti.k_hi >= ti.k_lo && row0 >= a.row_begin &&
+                     row0 + RW_ROWS <= a.row_end && col0 + RW_COLS <= a.C && (a.C * (int)sizeof(T)) % 16 == 0;
+    if (!can) {
+        if (threadIdx.x == 0) live[rt] = 1;
+        return;
+    }
+    constexpr int CPR = RW_COLS * (int)sizeof(T) / 16;  // 16-byte chunks per row segment
+    constexpr int CPS = CPR * RW_ROWS;                  // ... per step
+    constexpr int SPI = 256 / CPS;                      // steps per round
+    const int tid = threadIdx.x, ch = tid % CPS, sub = tid / CPS;
+    const int r = ch / CPR, cc = ch % CPR;
+    const size_t plane = (size_t)(a.row_end - a.row_begin) * a.C;
+    const char* base = static_cast<const char*>(a.stack) +
+                       ((size_t)(row0 + r - a.row_begin) * a.C + col0) * sizeof(T) + (size_t)cc * 16;
+    auto ld = [&](int k) { return __ldg(reinterpret_cast<const uint4*>(base + (size_t)k * plane * sizeof(T))); };
+    const uint4 ref = ld(ti.k_lo);
+    int var = 0;
+    for (int k0 = ti.k_lo + 1; k0 <= ti.k_hi; k0 += 4 * SPI) {
+        uint4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = ld(min(k0 + u * SPI + sub, ti.k_hi));
+#pragma unroll
+        for (int u = 0; u < 4; ++u) var |= (x[u].x ^ ref.x) | (x[u].y ^ ref.y) | (x[u].z ^ ref.z) | (x[u].w ^ ref.w);
+        if (__syncthreads_or(var)) break;
+    }
+    if (__syncthreads_or(var)) {
+        if (tid == 0) live[rt] = 1;
+        return;
+    }
+    // dead: zeros for planes [0, M) of the tile's 2 x 64 pixels (16 threads per 256-byte row segment)
+    const int rows = a.row_end - a.row_begin;
+    const int zr = (tid >> 4) & 1, zc = tid & 15;
+    for (int m = tid >> 5; m < a.M; m += 8) {
+        float4* q = reinterpret_cast<float4*>(out + ((size_t)m * rows + (row0 + zr - a.row_begin)) * a.C + col0) + zc;
+        *q = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (tid == 0) live[rt] = 0;
+}
+
 // ------------------------------------------------------------------ admission replay
 // One warp per row tile replays the kernel's schedule (lanes, pauses, frontier, drains) with the
 // kernel's own fp32 arithmetic for the geometry (the intensities do not enter the schedule) and
@@ -1038,6 +1054,16 @@ cudaError_t launch_row(const RowArgs& a, const CUtensorMap* in_map, const CUtens
                                  : launch_rb<uint16_t, RW_RB_LARGE>(a, in_map, out_map, variant, st);
     return rb == RW_RB_SMALL ? launch_rb<float, RW_RB_SMALL>(a, in_map, out_map, variant, st)
                              : launch_rb<float, RW_RB_LARGE>(a, in_map, out_map, variant, st);
+}
+
+cudaError_t launch_row_live(const RowArgs& a, int rt0, int n, unsigned char* live, float* out, int dtype,
+                            cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    if (dtype == DAXM_U16)
+        row_live_kernel<uint16_t><<<(unsigned)n, 256, 0, st>>>(a, rt0, n, live, out);
+    else
+        row_live_kernel<float><<<(unsigned)n, 256, 0, st>>>(a, rt0, n, live, out);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_row_admit(const RowArgs& a, RowTile* rt, int n_rt, int* d_stats, cudaStream_t st) {

@@ -85,6 +85,7 @@ struct daxm_plan {
     int row_org = 0, n_rr = 0, n_rc = 0;   // global row of row-tile row 0 (= row_begin), rows, columns
     int max_nv_row = 0;                    // largest row-tile step range
     RowTile* d_rt = nullptr;
+    unsigned char* d_rlive = nullptr;  // row tiles' live flags of the last call (exact zero-dI skip)
     float* d_rcoef = nullptr;
     int* d_rlist = nullptr;                // class lists [small][large][general], each ascending
     std::vector<int> h_rlist;
@@ -641,10 +642,12 @@ void free_plan_memory(daxm_plan* p) {
     cudaFree(p->d_lock_err);
     p->d_lock_err = nullptr;
     cudaFree(p->d_rt);
+    cudaFree(p->d_rlive);
     cudaFree(p->d_rcoef);
     cudaFree(p->d_rlist);
     cudaFree(p->d_row_err);
     p->d_rt = nullptr;
+    p->d_rlive = nullptr;
     p->d_rcoef = nullptr;
     p->d_rlist = nullptr;
     p->d_row_err = nullptr;
@@ -767,6 +770,7 @@ daxm_status row_prepass(daxm_plan* p, int) {
     p->n_rc = (g.n_cols + RW_COLS - 1) / RW_COLS;
     const size_t n_rt = (size_t)p->n_rr * p->n_rc;
     CK(cudaMalloc(&p->d_rt, sizeof(RowTile) * n_rt));
+    CK(cudaMalloc(&p->d_rlive, n_rt));
     CK(cudaMalloc(&p->d_rcoef, sizeof(float) * n_rt * NCOEF * (RW_COLS + 1) * RW_ROWS));
     CK(cudaMalloc(&p->d_row_err, 64));
     CK(cudaMemset(p->d_row_err, 0, 64));
@@ -826,13 +830,14 @@ daxm_status row_prepass(daxm_plan* p, int) {
     p->stats.row_tiles_general = p->n_rcls[6];
     p->stats.row_launches = 0;
     for (int c = 0; c < daxm_plan::N_RCLS; ++c) p->stats.row_launches += p->n_rcls[c] > 0;
+    p->stats.row_launches += 1;  // row_live_kernel (exact zero-dI skip)
     p->stats.row_ring_need_max = hs[3];
     // one path per plan: the row-segment kernel when it admits every row tile, else the deposit-tile
     // kernels (step-locked, fast, general) of round 1, which cover the overlapping-span regime
     if (p->n_rcls[6] > 0 && getenv("DAXM_ROW_PARTIAL") == nullptr) return DAXM_OK;
     p->stats.fit_max_err_bins = std::max(p->stats.fit_max_err_bins, ferr[0]);
     p->stats.fit_model_err_bins = std::max(p->stats.fit_model_err_bins, ferr[1]);
-    p->stats.device_bytes += (int64_t)(sizeof(RowTile) * n_rt + sizeof(float) * n_rt * NCOEF * (RW_COLS + 1) * RW_ROWS +
+    p->stats.device_bytes += (int64_t)(sizeof(RowTile) * n_rt + n_rt + sizeof(float) * n_rt * NCOEF * (RW_COLS + 1) * RW_ROWS +
                                        sizeof(int) * p->h_rlist.size());
     p->row_ok = true;
     p->stats.row_path = 1;
@@ -1226,7 +1231,7 @@ static RowArgs make_row_args(const daxm_plan* p) {
     a.stack = nullptr;
     a.use_cutoff = p->use_cutoff;
     a.cutoff = p->cutoff;
-    a.zero_skip = getenv("DAXM_NO_ZERO_SKIP") == nullptr;
+    a.live = nullptr;
     a.err = p->d_row_err;
     return a;
 }
@@ -1343,6 +1348,16 @@ static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_o
         n_launch += seg[c][1] > seg[c][0];
         off += p->n_rcls[c];
     }
+    RowArgs a = make_row_args(p);
+    a.stack = d_stack;
+    if (getenv("DAXM_NO_ZERO_SKIP") == nullptr) {  // exact zero-dI skip, before the class launches fork
+        cudaError_t z = launch_row_live(a, ra * p->n_rc, (rb - ra) * p->n_rc, p->d_rlive, d_out, dt, st);
+        if (z != cudaSuccess) {
+            cudaGetLastError();
+            return fail(p, DAXM_ERR_CUDA, "row live launch: %s", cudaGetErrorString(z));
+        }
+        a.live = p->d_rlive;
+    }
     const bool fork = n_launch >= 2 && p->st_cls[0] != nullptr && getenv("DAXM_NO_FORK") == nullptr;
     cudaStream_t sts[3] = {st, fork ? p->st_cls[0] : st, fork ? p->st_cls[1] : st};
     cudaError_t e = cudaSuccess;
@@ -1350,8 +1365,6 @@ static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_o
         e = cudaEventRecord(p->ev_cls[0], st);
         for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(p->st_cls[i], p->ev_cls[0], 0);
     }
-    RowArgs a = make_row_args(p);
-    a.stack = d_stack;
     // launches in class order, spread over the three streams (largest classes first on separate ones)
     int li = 0;
     for (int c = 0; c < NC - 1 && e == cudaSuccess; ++c) {
