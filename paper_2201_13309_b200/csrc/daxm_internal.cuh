@@ -285,8 +285,8 @@ cudaError_t launch_lock_prepass(const DepositArgs& a, int n_tiles, int* d_stats,
 // row-segment kernel (deposit_row.cu): pre-pass replay (admission) and the class launches
 cudaError_t launch_row_admit(const RowArgs& a, RowTile* rt, int n_rt, int* d_stats, cudaStream_t st);
 cudaError_t row_set_attributes();
-cudaError_t launch_row_live(const RowArgs& a, int rt0, int n, unsigned char* live, float* out, int dtype,
-                            cudaStream_t st);  // exact zero-dI skip over row tiles [rt0, rt0 + n)  // per device: dynamic shared memory of every instance
+cudaError_t launch_row_live(const RowArgs& a, int rt0, int n, unsigned char* live, int dtype,
+                            cudaStream_t st);  // exact zero-dI skip flags of row tiles [rt0, rt0 + n)  // per device: dynamic shared memory of every instance
 cudaError_t launch_row(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int dtype, int rb,
                        int variant, cudaStream_t st);  // variant: 0 separated, 1 general-span, 2 + wide input ring
 cudaError_t launch_general_rows(const DepositArgs& a, const int* rt_list, int n, int n_rc, int row_org,

@@ -259,7 +259,6 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
     unsigned char* smem = smem_raw + (sbase - smem_u32(smem_raw));
     const int lane = threadIdx.x;
     const int rt = a.list[blockIdx.x];
-    if (a.live && !a.live[rt]) return;  // constant intensities: row_live_kernel wrote the zeros
     const RowTile ti = a.rt[rt];
     const int rr = rt / a.n_rc, rc = rt % a.n_rc;
     const int row0 = a.row_org + rr * RW_ROWS;  // global row of the tile's first row
@@ -300,7 +299,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
                 const T* s0 = static_cast<const T*>(a.stack) + (size_t)(j - a.row_begin) * a.C + c;
                 on = (float)s0[0] >= a.cutoff;
             }
-            any_act |= on;
+            any_act |= on;  // (a tile with constant intensities, row_live_kernel: none, zeros below)
             (r ? gate[p].y : gate[p].x) = on ? 0.f : 1.0e9f;  // inactive: edge counts below zero
             float cl[3], ch[3];
             row_coef(a, rt, r, (ti.cls & RW_CLS_FRONT_LO) && !POINT ? e + 1 : e, cl);
@@ -312,6 +311,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
             }
         }
     }
+    if (a.live && !a.live[rt]) any_act = false;  // every dI is 0 (exact zero-dI skip)
     if (!__any_sync(0xffffffffu, any_act)) {  // no active walk: the tile's output is zero
         fence_proxy_async_smem();
         __syncwarp();
@@ -732,57 +732,49 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
 }
 
 // ------------------------------------------------------------------ exact zero-dI skip
-// One CTA per row tile of rows [tr0, tr1) x all row-tile columns.  A tile whose intensities are the
-// same at every step of its range [k_lo, k_hi] has every dI = 0, so every bin value the row kernel
-// would store is exactly 0: this kernel writes those zeros (coalesced 256-byte row segments) and
-// clears the tile's live flag, and the row kernel's CTA for the tile returns at once.  The scan
-// reads 16-byte chunks, all threads on distinct (step, row, chunk), and stops at the first round
-// with a change, so a live tile costs one round.  Tiles at the detector's edges, with misaligned
-// rows, or not admitted to the row kernel stay live (no scan).
+// One warp per row tile of [rt0, rt0 + n).  A tile whose intensities are the same at every step of
+// its range [k_lo, k_hi] has every dI = 0, so every bin value the row kernel would store is exactly 0:
+// the warp clears the tile's live flag and the row kernel's CTA writes the zeros (its zero path,
+// TMA stores interleaved with the live tiles' deposits) without running the deposit.  The scan reads
+// 16-byte chunks, lanes on distinct (step, row, chunk), 8 loads in flight per lane, and stops at the
+// first round with a change, so a live tile costs one round.  Tiles at the detector's edges, with
+// misaligned rows, or not admitted to the row kernel stay live (no scan).
 template <typename T>
-__global__ void __launch_bounds__(256) row_live_kernel(const RowArgs a, int rt0, int n, unsigned char* __restrict__ live,
-                                                       float* __restrict__ out) {
-    const int rt = rt0 + blockIdx.x;
+__global__ void __launch_bounds__(256) row_live_kernel(const RowArgs a, int rt0, int n, unsigned char* __restrict__ live) {
+    const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (w >= n) return;
+    const int rt = rt0 + w;
     const RowTile ti = a.rt[rt];
     const int rr = rt / a.n_rc, rc = rt % a.n_rc;
     const int row0 = a.row_org + rr * RW_ROWS, col0 = rc * RW_COLS;
     const bool can = (ti.cls & RW_CLS_RB) != 0 && ti.k_hi >= ti.k_lo && row0 >= a.row_begin &&
                      row0 + RW_ROWS <= a.row_end && col0 + RW_COLS <= a.C && (a.C * (int)sizeof(T)) % 16 == 0;
     if (!can) {
-        if (threadIdx.x == 0) live[rt] = 1;
+        if (lane == 0) live[rt] = 1;
         return;
     }
     constexpr int CPR = RW_COLS * (int)sizeof(T) / 16;  // 16-byte chunks per row segment
-    constexpr int CPS = CPR * RW_ROWS;                  // ... per step
-    constexpr int SPI = 256 / CPS;                      // steps per round
-    const int tid = threadIdx.x, ch = tid % CPS, sub = tid / CPS;
+    constexpr int CPS = CPR * RW_ROWS;                  // ... per step (16 or 32)
+    constexpr int SPL = 32 / CPS;                       // steps per load instruction
+    constexpr int U = 8;                                // loads in flight per lane
+    const int ch = lane % CPS, sub = lane / CPS;
     const int r = ch / CPR, cc = ch % CPR;
-    const size_t plane = (size_t)(a.row_end - a.row_begin) * a.C;
+    const size_t plane = (size_t)(a.row_end - a.row_begin) * a.C * sizeof(T);
     const char* base = static_cast<const char*>(a.stack) +
                        ((size_t)(row0 + r - a.row_begin) * a.C + col0) * sizeof(T) + (size_t)cc * 16;
-    auto ld = [&](int k) { return __ldg(reinterpret_cast<const uint4*>(base + (size_t)k * plane * sizeof(T))); };
+    auto ld = [&](int k) { return __ldg(reinterpret_cast<const uint4*>(base + (size_t)k * plane)); };
     const uint4 ref = ld(ti.k_lo);
-    int var = 0;
-    for (int k0 = ti.k_lo + 1; k0 <= ti.k_hi; k0 += 4 * SPI) {
-        uint4 x[4];
+    unsigned var = 0;
+    for (int k0 = ti.k_lo + 1; k0 <= ti.k_hi; k0 += U * SPL) {
+        uint4 x[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) x[u] = ld(min(k0 + u * SPI + sub, ti.k_hi));
+        for (int u = 0; u < U; ++u) x[u] = ld(min(k0 + u * SPL + sub, ti.k_hi));
 #pragma unroll
-        for (int u = 0; u < 4; ++u) var |= (x[u].x ^ ref.x) | (x[u].y ^ ref.y) | (x[u].z ^ ref.z) | (x[u].w ^ ref.w);
-        if (__syncthreads_or(var)) break;
+        for (int u = 0; u < U; ++u) var |= (x[u].x ^ ref.x) | (x[u].y ^ ref.y) | (x[u].z ^ ref.z) | (x[u].w ^ ref.w);
+        if (__any_sync(0xffffffffu, var != 0)) break;
     }
-    if (__syncthreads_or(var)) {
-        if (tid == 0) live[rt] = 1;
-        return;
-    }
-    // dead: zeros for planes [0, M) of the tile's 2 x 64 pixels (16 threads per 256-byte row segment)
-    const int rows = a.row_end - a.row_begin;
-    const int zr = (tid >> 4) & 1, zc = tid & 15;
-    for (int m = tid >> 5; m < a.M; m += 8) {
-        float4* q = reinterpret_cast<float4*>(out + ((size_t)m * rows + (row0 + zr - a.row_begin)) * a.C + col0) + zc;
-        *q = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    if (tid == 0) live[rt] = 0;
+    const bool changed = __any_sync(0xffffffffu, var != 0);
+    if (lane == 0) live[rt] = changed ? 1 : 0;
 }
 
 // ------------------------------------------------------------------ admission replay
@@ -1056,13 +1048,13 @@ cudaError_t launch_row(const RowArgs& a, const CUtensorMap* in_map, const CUtens
                              : launch_rb<float, RW_RB_LARGE>(a, in_map, out_map, variant, st);
 }
 
-cudaError_t launch_row_live(const RowArgs& a, int rt0, int n, unsigned char* live, float* out, int dtype,
-                            cudaStream_t st) {
+cudaError_t launch_row_live(const RowArgs& a, int rt0, int n, unsigned char* live, int dtype, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((n + 7) / 8);
     if (dtype == DAXM_U16)
-        row_live_kernel<uint16_t><<<(unsigned)n, 256, 0, st>>>(a, rt0, n, live, out);
+        row_live_kernel<uint16_t><<<grid, 256, 0, st>>>(a, rt0, n, live);
     else
-        row_live_kernel<float><<<(unsigned)n, 256, 0, st>>>(a, rt0, n, live, out);
+        row_live_kernel<float><<<grid, 256, 0, st>>>(a, rt0, n, live);
     return cudaGetLastError();
 }
 

@@ -1351,7 +1351,7 @@ static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_o
     RowArgs a = make_row_args(p);
     a.stack = d_stack;
     if (getenv("DAXM_NO_ZERO_SKIP") == nullptr) {  // exact zero-dI skip, before the class launches fork
-        cudaError_t z = launch_row_live(a, ra * p->n_rc, (rb - ra) * p->n_rc, p->d_rlive, d_out, dt, st);
+        cudaError_t z = launch_row_live(a, ra * p->n_rc, (rb - ra) * p->n_rc, p->d_rlive, dt, st);
         if (z != cudaSuccess) {
             cudaGetLastError();
             return fail(p, DAXM_ERR_CUDA, "row live launch: %s", cudaGetErrorString(z));

@@ -1,4 +1,4 @@
-export T=${TAG:-r02zc}
+export T=${TAG:-r02zd}
 timeout 900 python -m pytest tests/test_parity_gpu.py -x -q -k "zero_skip or peaks_only or c5_regions or full_size_sampled or cutoff" > gpurun_out/${T}_pytest.log 2>&1; tail -3 gpurun_out/${T}_pytest.log
 for c in C4 C5; do
 timeout 300 python bench.py --config $c --steps 10 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/${T}_bench_$c.json 2> gpurun_out/${T}_bench_$c.err
@@ -11,7 +11,7 @@ python -c "import json; d=json.load(open('gpurun_out/${T}_bench_C5_cut.json')); 
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches.csv python bench.py --config C5 --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
 python - <<'PY'
 import csv
-rows=[r for r in csv.reader(open('gpurun_out/'+__import__('os').environ.get('T','r02zc')+'_launches.csv')) if len(r)>10]
+rows=[r for r in csv.reader(open('gpurun_out/'+__import__('os').environ.get('T','r02zd')+'_launches.csv')) if len(r)>10]
 hdr=rows[0]; ki=hdr.index('Kernel Name'); vi=hdr.index('Metric Value')
 from collections import defaultdict
 d=defaultdict(list)
