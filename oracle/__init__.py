@@ -12,6 +12,9 @@ Parity status of each exported function:
   oracle_reconstruct[_pixels]                  pinned (conservation, background, linearity,
                                                reversal identity, forward-model round trip)
   select_cutoff, active_pixels (python)        pinned (order-statistic definition, tests/test_oracle_cutoff.py)
+  edge "both" (reading R16)                    pinned (tests/test_oracle_both.py: split identity
+                                               both(I) = lead(D) + trail(U) through the pinned single-edge
+                                               oracle, monotone stacks, forward-model point scatterer)
   depth_profile (python)                       pinned (conservation: the profile's total = sum_p s (I_0 - I_{S-1})
                                                when every trapezoid lies inside the bins; a single non-constant
                                                pixel's profile = its oracle_reconstruct_pixels column;
@@ -94,7 +97,7 @@ class Geometry:
 
     def __init__(self, g: dict, raw_sign: bool = False):
         self.wire = np.ascontiguousarray(np.asarray(g["wire_xyz"], dtype=np.float64).reshape(-1, 3))
-        edge = {"leading": 0, "trailing": 1}[g.get("edge", "leading")]
+        edge = {"leading": 0, "trailing": 1, "both": 2}[g.get("edge", "leading")]
         pm = {"finite": 0, "point": 1}[g.get("pixel_model", "finite")]
         self.s = OracleGeometry(
             int(g["n_rows"]), int(g["n_cols"]), float(g["pitch_col"]), float(g["pitch_row"]),

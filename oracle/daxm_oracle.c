@@ -48,7 +48,7 @@ typedef struct {
     int32_t n_steps;               /* S                                                      */
     const double *wire_xyz;        /* [S][3] wire-centre positions W_k                       */
     double depth_start, depth_end, depth_res;
-    int32_t edge;                  /* 0 leading, 1 trailing                                  */
+    int32_t edge;                  /* 0 leading, 1 trailing, 2 both (reading R16)            */
     int32_t pixel_model;           /* 0 finite (trapezoid), 1 point (box)                    */
     int32_t raw_sign;              /* 1: s = +1 even for trailing (used by identity tests)   */
 } oracle_geometry;
@@ -182,6 +182,7 @@ void oracle_deposit_pair(double dI, const double c[4], double start, double dz, 
 
 static int geometry_ok(const oracle_geometry *g) {
     if (!g || g->n_rows < 1 || g->n_cols < 1 || g->n_steps < 2 || !g->wire_xyz) return 0;
+    if (g->edge < 0 || g->edge > 2) return 0;
     if (!(g->depth_res > 0.0) || !(g->depth_end >= g->depth_start) || !(g->wire_radius > 0.0)) return 0;
     return 1;
 }
@@ -200,7 +201,9 @@ int oracle_reconstruct_pixels(const oracle_geometry *g, int n_pix, const int32_t
     unit3(g->wire_axis, axis);
     unit3(g->beam_dir, beam);
     const double *W0 = g->wire_xyz, *Wl = g->wire_xyz + 3 * (S - 1);
-    const double s = (g->edge == 1 && !g->raw_sign) ? -1.0 : 1.0; /* reading R2 */
+    /* edges run: the plan's one, or both (reading R16: leading takes the intensity decreases,
+     * trailing the sign-normalised increases, and the two reconstructions add) */
+    const int e_first = g->edge == 2 ? 0 : g->edge, e_last = g->edge == 2 ? 1 : g->edge;
 #ifdef _OPENMP
     if (n_threads > 0) omp_set_num_threads(n_threads);
 #pragma omp parallel for schedule(dynamic, 16)
@@ -218,10 +221,13 @@ int oracle_reconstruct_pixels(const oracle_geometry *g, int n_pix, const int32_t
             oracle_detector_point(g, cols[p] - 0.5, rows[p], back);
             oracle_detector_point(g, cols[p] + 0.5, rows[p], front);
         }
-        double sb = oracle_edge_sigma(back, W0, Wl, axis, g->edge);
-        double sf = oracle_edge_sigma(front, W0, Wl, axis, g->edge);
+        for (int e = e_first; e <= e_last; ++e) {
+        const double s = (e == 1 && !g->raw_sign) ? -1.0 : 1.0; /* reading R2 */
+        double sb = oracle_edge_sigma(back, W0, Wl, axis, e);
+        double sf = oracle_edge_sigma(front, W0, Wl, axis, e);
         for (int k = 0; k + 1 < S; ++k) {
             double dI = s * (I[k] - I[k + 1]);
+            if (g->edge == 2 && dI < 0.0) dI = 0.0; /* reading R16: each edge its own sign of change */
             if (dI == 0.0) continue;
             const double *Wa = g->wire_xyz + 3 * k, *Wb = g->wire_xyz + 3 * (k + 1);
             /* Fig. 7: full_start, partial_start, partial_end, full_end */
@@ -231,6 +237,7 @@ int oracle_reconstruct_pixels(const oracle_geometry *g, int n_pix, const int32_t
                            oracle_tangent_depth(front, Wb, axis, g->wire_radius, sf, beam, g->beam_origin)};
             if (isnan(c[0]) || isnan(c[1]) || isnan(c[2]) || isnan(c[3])) continue; /* reading R8 */
             oracle_deposit_pair(dI, c, g->depth_start, g->depth_res, M, o, 1);
+        }
         }
     }
     return ORC_OK;
