@@ -87,11 +87,11 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def workload_config(cfg, noise, world, parallelism_rows):
+def workload_config(cfg, noise, world, parallelism_rows, edge="leading"):
     return {
         "workload": f"{cfg.name}: {cfg.description}",
         "detector": f"{cfg.n}x{cfg.n}", "n_steps": cfg.n_steps, "n_bins": cfg.n_bins,
-        "depth_res_um": cfg.depth_res, "input_dtype": cfg.dtype, "edge": "leading", "pixel_model": "finite",
+        "depth_res_um": cfg.depth_res, "input_dtype": cfg.dtype, "edge": edge, "pixel_model": "finite",
         "stack_noise": noise, "geometry": "34-ID-E-like synthetic (SURVEY.md §8(d))",
         "parallelism": f"row-sharded x{world} (no collective)", "rows_per_gpu": parallelism_rows,
         "l2": "inputs larger than L2 (stack + output per step >> 126 MB); no flush",
@@ -156,7 +156,7 @@ def run_reference(args):
     oracle.build()
     cfg = synth.get_config(args.config)
     noise = not cfg.sparse if args.noise is None else args.noise
-    g = synth.geometry(cfg)
+    g = synth.geometry(cfg, edge=args.edge)
     maps = synth.make_maps(cfg)
     rng = np.random.default_rng(99)
     threads = oracle.max_threads()
@@ -188,7 +188,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": workload_config(cfg, noise, 1, cfg.n),
+        "config": workload_config(cfg, noise, 1, cfg.n, args.edge),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
@@ -217,6 +217,8 @@ def main():
                     help="torch.distributed backend for N>1 (gloo lets several ranks share one GPU)")
     ap.add_argument("--dtype", choices=["u16", "f32"], default=None,
                     help="override the config's stack dtype (e.g. C5 in fp32, SURVEY §8(d))")
+    ap.add_argument("--edge", choices=["leading", "trailing", "both"], default="leading",
+                    help="wire edge(s): both = leading on the decreases + trailing on the increases (R16)")
     ap.add_argument("--fraction", type=float, default=1.0,
                     help="pixel percentage (P:L299-303): reconstruct only this fraction of the pixels, the "
                          "brightest by first-step intensity (daxm_select_cutoff + daxm_set_cutoff)")
@@ -255,7 +257,7 @@ def main():
         import dataclasses
         cfg = dataclasses.replace(cfg, dtype=args.dtype)
     noise = (not cfg.sparse) if args.noise is None else args.noise
-    g = synth.geometry(cfg)
+    g = synth.geometry(cfg, edge=args.edge)
     R = cfg.n
     from paper_2201_13309_b200 import multi
     r0, r1 = multi.my_band(rank, world, R)  # tile-aligned row band
@@ -302,7 +304,11 @@ def main():
     kern_median = sorted(kern_ms)[len(kern_ms) // 2]
     # with a cutoff the input term is scaled by the active-pixel fraction (an estimate: the
     # active pixels' windows are not counted individually)
-    alg_bytes = active * (st["contrib_pairs"] + st["contrib_pixels"]) * b_in + st["rows"] * st["cols"] * st["n_bins"] * 4
+    # both edges: each edge's pass reads its windows (the stats sum the two plans'); the output is
+    # stored by the first pass and read + written by the second's reduce-add
+    out_passes = 3 if args.edge == "both" else 1
+    alg_bytes = (active * (st["contrib_pairs"] + st["contrib_pixels"]) * b_in +
+                 out_passes * st["rows"] * st["cols"] * st["n_bins"] * 4)
     achieved = alg_bytes / (kern_avg * 1e-3) / 1e9
     ms_step = total_ms / K
     ms_step_max, kern_max, achieved_min = multi.max_over_ranks([ms_step, kern_avg, -achieved], device=dev)
@@ -465,12 +471,14 @@ def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_ma
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_step_max, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": workload_config(cfg, noise, world, r1 - r0),
+            "config": workload_config(cfg, noise, world, r1 - r0, args.edge),
             "roofline": {"bound": "hbm", "achieved": achieved_min, "peak": peak, "unit": "GB/s",
                          "frac": achieved_min / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "deposit (daxm_reconstruct)", "kernel_ms": kern_max,
                          "algorithmic_bytes_per_launch": alg_bytes,
-                         "bytes_rule": "sum_p (S_c(p)+1)*b_in + rows*C*M*4 (SURVEY.md §8(d))"},
+                         "bytes_rule": "sum_p (S_c(p)+1)*b_in + rows*C*M*4 (SURVEY.md §8(d))" +
+                                       (" per edge, output x3 (store, then reduce-add read + write)"
+                                        if args.edge == "both" else "")},
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": K * world * launches_per_step(st, cfg.dtype, cut[0] is not None),

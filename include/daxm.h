@@ -49,7 +49,12 @@ typedef enum {
     DAXM_ERR_CUDA = 5              /* any CUDA runtime error; detail in daxm_last_error()            */
 } daxm_status;
 
-typedef enum { DAXM_EDGE_LEADING = 0, DAXM_EDGE_TRAILING = 1 } daxm_edge;
+/* DAXM_EDGE_BOTH (reading R16): both wire edges in one reconstruction -- the leading
+ * edge's geometry takes every step's intensity decrease max(I_k - I_{k+1}, 0), the trailing edge's
+ * the increase max(I_{k+1} - I_k, 0) (its sign-normalised dI, reading R2), and the two add.  The
+ * paper's wire_edge selector runs one edge per call; with BOTH a plan holds
+ * one pre-pass per edge (twice the plan memory and pre-pass time) and a call runs both. */
+typedef enum { DAXM_EDGE_LEADING = 0, DAXM_EDGE_TRAILING = 1, DAXM_EDGE_BOTH = 2 } daxm_edge;
 typedef enum {
     DAXM_PIXEL_FINITE = 0, /* pixel of finite width along the column axis: trapezoid (the paper)   */
     DAXM_PIXEL_POINT = 1   /* pixel centre only: box response                                       */

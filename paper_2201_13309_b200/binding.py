@@ -15,7 +15,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 # DAXM_LIBRARY selects an alternative build of the same library (kernel-variant experiments)
 _LIB_PATH = os.environ.get("DAXM_LIBRARY") or os.path.join(_PKG, "libdaxm.so")
 
-EDGE = {"leading": 0, "trailing": 1}
+EDGE = {"leading": 0, "trailing": 1, "both": 2}
 PIXEL_MODEL = {"finite": 0, "point": 1}
 DTYPE = {"u16": 0, "f32": 1}
 

@@ -121,6 +121,8 @@ struct DepositArgs {
     const int* vneed;         // [n_tiles][n_states + 1][8 warps] furthest visit index loaded by each state
     int n_states;             // (M + MC - 1) / MC + 1
     float sign;               // s: +1 leading, -1 trailing (reading R2)
+    float dI_floor;           // s dI -> max(s dI, dI_floor): -inf, or 0 in the both-edges mode (R16)
+    int acc;                  // 1: add into the output (both-edges mode, second edge) instead of storing
     const void* stack;        // band stack [S][rows][C] (plane 0 read for the intensity cutoff)
     const float* table;       // exact depth table (general kernel) or nullptr: per tile at toff[tile],
     const long long* toff;    //   [k - k_lo][TILE_E][TILE_R] fp32 bins relative to m_ref
@@ -238,6 +240,8 @@ struct RowArgs {
     int max_nv;            // largest tile step range (tau table size)
     int point_mode;
     float sign;            // s: +1 leading, -1 trailing (reading R2)
+    float dI_floor;        // s dI -> max(s dI, dI_floor): -inf, or 0 in the both-edges mode (R16)
+    int acc;               // 1: TMA reduce-add into the output (both-edges mode, second edge)
     const void* stack;     // band stack (plane 0 read for the intensity cutoff)
     int use_cutoff;
     float cutoff;

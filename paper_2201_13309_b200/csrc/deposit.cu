@@ -671,7 +671,8 @@ __device__ void general_pixel(const DepositArgs& a, int tile, int r, int c, int 
     const T* px = stack + (size_t)jl * a.C + i;
     const float sgn = a.sign * (float)dir;
     auto dI = [&](int q) -> float {
-        return sgn * ((float)px[(size_t)step_of(q) * plane] - (float)px[(size_t)step_of(q + 1) * plane]);
+        return fmaxf(sgn * ((float)px[(size_t)step_of(q) * plane] - (float)px[(size_t)step_of(q + 1) * plane]),
+                     a.dI_floor);  // both-edges mode: this edge's sign of change only (R16)
     };
     int qc = 0, qo = 0;
     float P = 0.f, F_prev = 0.f;
@@ -706,7 +707,10 @@ __device__ void general_pixel(const DepositArgs& a, int tile, int r, int c, int 
             const float d = dI(q);
             if (d != 0.f) F += d * trapezoid_fraction(lo1, hi1, lo2, hi2, E);
         }
-        if (e > 0) o[(size_t)(e - 1) * plane] = F - F_prev;
+        if (e > 0) {
+            float* q = o + (size_t)(e - 1) * plane;
+            *q = a.acc ? *q + (F - F_prev) : F - F_prev;
+        }
         F_prev = F;
     }
 }

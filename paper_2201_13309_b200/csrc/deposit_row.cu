@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
     if (!__any_sync(0xffffffffu, any_act)) {  // no active walk: the tile's output is zero
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) {
+        if (lane == 0 && !a.acc) {  // (adding zeros: nothing to do)
             for (int P = 0; P < a.M; P += RW_PB) tma_store_3d(&out_map, col0, rowl, P, smem + L::OFF_OUT);
             bulk_commit();
             bulk_wait<0>();
@@ -370,7 +370,8 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
     const uint32_t ob = sbase + L::OFF_OUT + (uint32_t)(32 * hh + 2 * (lane & 15)) * 4u;  // column 2i of a plane
     const uint32_t ob0 = opaque(ob + 4u * (uint32_t)hh), ob1 = opaque(ob + 4u * (uint32_t)(hh ^ 1));  // pair 0 / 1
     const uint32_t swap = hh ? 0x1032u : 0x3210u;  // pair p's column is the (p ^ h)-th of the lane's two
-    const float2 sdir2 = f2(opaque(2.f * a.sign * (float)dir));  // c = 2 s dir dI / (sum_{q+1} - sum_q)
+    const float2 sdir2 = f2(opaque(2.f * a.sign * (float)dir));
+    const float2 dfl2 = f2(opaque(a.dI_floor));  // c = 2 s dir dI / (sum_{q+1} - sum_q)
     const float EM = opaque((float)(a.M - a.m_ref));
     const int m_ref = a.m_ref;
     // bits(E + fbias) = 0x4B000000 + e - 1 + RB for edge index e = E + m_ref: its plane's slot in the low bits
@@ -459,8 +460,13 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
         __syncwarp();
         if (lane == 0) {
 #pragma unroll 1
-            for (int b = b0; b < nb; ++b)
-                tma_store_3d(&out_map, col0, rowl, b * RW_PB, smem + L::OFF_OUT + ((b * RW_PB) & (RB - 1)) * PLANE_B);
+            for (int b = b0; b < nb; ++b) {
+                const unsigned char* src = smem + L::OFF_OUT + ((b * RW_PB) & (RB - 1)) * PLANE_B;
+                if (a.acc)
+                    tma_reduce_add_3d(&out_map, col0, rowl, b * RW_PB, src);
+                else
+                    tma_store_3d(&out_map, col0, rowl, b * RW_PB, src);
+            }
             bulk_commit();
         }
     };
@@ -520,7 +526,8 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
             // trapezoid height c = dI / area: twice the area is s - ps for separated spans and
             // (hi - lo_v) + |hi_v - lo| in general (the sorted corners' two parallel sides)
             const float2 dn = GEN ? add2(sub2(hi, S.plo[p]), abs2(sub2(S.phi[p], lo))) : sub2(s, S.ps[p]);
-            const float2 c = mul2(mul2(sdir2, sub2(S.pI[p], S.Iq[p])), rcp2(dn));
+            // (both-edges mode: the clamp keeps this edge's sign of change, reading R16; -inf otherwise)
+            const float2 c = mul2(max2(mul2(sdir2, sub2(S.pI[p], S.Iq[p])), dfl2), rcp2(dn));
             // edges of the zone [plo, lo): En .. floor(min(lo, EM))
             const float2 fl = add2(floor2(min2(lo, f2(EM))), f2(1.f));
             const float2 cnt = sub2(fl, add2(S.En[p], gate[p]));

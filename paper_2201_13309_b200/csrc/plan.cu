@@ -35,6 +35,11 @@ using namespace daxm;
 
 struct daxm_plan {
     int device = 0;
+    // both-edges mode (reading R16): the parent holds one plan per edge and runs both per call
+    daxm_plan* child[2] = {nullptr, nullptr};
+    bool is_child = false;
+    float dI_floor = -INFINITY;  // children: 0 (each edge takes its own sign of change)
+    int acc = 0;                 // children: 0 for the leading edge (stores), 1 for the trailing (adds)
     daxm_geometry g{};
     std::vector<double> wire;
     std::vector<double> t;        // wire travel t_k
@@ -834,7 +839,9 @@ daxm_status row_prepass(daxm_plan* p, int) {
     p->stats.row_ring_need_max = hs[3];
     // one path per plan: the row-segment kernel when it admits every row tile, else the deposit-tile
     // kernels (step-locked, fast, general) of round 1, which cover the overlapping-span regime
-    if (p->n_rcls[6] > 0 && getenv("DAXM_ROW_PARTIAL") == nullptr) return DAXM_OK;
+    // (both-edges children take the row path with the general kernel for the rest: the deposit-tile
+    // kernels neither clamp nor accumulate)
+    if (p->n_rcls[6] > 0 && getenv("DAXM_ROW_PARTIAL") == nullptr && !p->is_child) return DAXM_OK;
     p->stats.fit_max_err_bins = std::max(p->stats.fit_max_err_bins, ferr[0]);
     p->stats.fit_model_err_bins = std::max(p->stats.fit_model_err_bins, ferr[1]);
     p->stats.device_bytes += (int64_t)(sizeof(RowTile) * n_rt + n_rt + sizeof(float) * n_rt * NCOEF * (RW_COLS + 1) * RW_ROWS +
@@ -1054,6 +1061,9 @@ const char* daxm_create_error(void) { return g_create_err.c_str(); }
 
 const char* daxm_last_error(const daxm_plan* p) { return p ? p->err.c_str() : ""; }
 
+static daxm_status create_one(const daxm_geometry* g, int cuda_device, bool child, daxm_plan** out);
+static daxm_status create_both(const daxm_geometry* g, int cuda_device, daxm_plan** out);
+
 daxm_status daxm_create(const daxm_geometry* g, int cuda_device, daxm_plan** out) {
     g_create_err.clear();
     if (!out) return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "out is NULL");
@@ -1082,7 +1092,7 @@ daxm_status daxm_create(const daxm_geometry* g, int cuda_device, daxm_plan** out
     if (fabs(nb - nearbyint(nb)) > 1e-6 || nb > 1e7)
         return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "(depth_end - depth_start)/depth_res = %.9g is not an integer",
                     nb);
-    if (g->edge != DAXM_EDGE_LEADING && g->edge != DAXM_EDGE_TRAILING)
+    if (g->edge != DAXM_EDGE_LEADING && g->edge != DAXM_EDGE_TRAILING && g->edge != DAXM_EDGE_BOTH)
         return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "unknown edge %d", g->edge);
     if (g->pixel_model != DAXM_PIXEL_FINITE && g->pixel_model != DAXM_PIXEL_POINT)
         return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "unknown pixel model %d", g->pixel_model);
@@ -1095,13 +1105,20 @@ daxm_status daxm_create(const daxm_geometry* g, int cuda_device, daxm_plan** out
         if (norm3(c) < 1e-9 * norm3(a) * norm3(b))
             return fail(nullptr, DAXM_ERR_INVALID_ARGUMENT, "beam is parallel to the wire axis");
     }
+    if (g->edge == DAXM_EDGE_BOTH) return create_both(g, cuda_device, out);
+    return create_one(g, cuda_device, false, out);
+}
+
+// After daxm_create's validation: one plan (one edge).
+static daxm_status create_one(const daxm_geometry* g, int cuda_device, bool child, daxm_plan** out) {
     daxm_plan* p = new (std::nothrow) daxm_plan();
     if (!p) return fail(nullptr, DAXM_ERR_OUT_OF_MEMORY, "host allocation failed");
+    p->is_child = child;
     p->device = cuda_device;
     p->g = *g;
     p->wire.assign(g->wire_xyz, g->wire_xyz + 3 * (size_t)g->n_steps);
     p->g.wire_xyz = nullptr;
-    p->M = (int)nearbyint(nb) + 1;
+    p->M = (int)nearbyint((g->depth_end - g->depth_start) / g->depth_res) + 1;
     p->rows = g->row_end - g->row_begin;
     p->C = g->n_cols;
     p->S = g->n_steps;
@@ -1125,6 +1142,37 @@ daxm_status daxm_create(const daxm_geometry* g, int cuda_device, daxm_plan** out
     return DAXM_OK;
 }
 
+// Both-edges mode (reading R16): one child plan per edge, same geometry; the leading child stores
+// the reconstruction of the intensity decreases, the trailing child adds that of the increases.
+static daxm_status create_both(const daxm_geometry* g, int cuda_device, daxm_plan** out) {
+    daxm_plan* p = new (std::nothrow) daxm_plan();
+    if (!p) return fail(nullptr, DAXM_ERR_OUT_OF_MEMORY, "host allocation failed");
+    p->device = cuda_device;
+    p->g = *g;
+    p->g.wire_xyz = nullptr;
+    for (int e = 0; e < 2; ++e) {
+        daxm_geometry ge = *g;
+        ge.edge = e == 0 ? DAXM_EDGE_LEADING : DAXM_EDGE_TRAILING;
+        daxm_status s = create_one(&ge, cuda_device, true, &p->child[e]);
+        if (s != DAXM_OK) {
+            daxm_destroy(p);
+            return s;
+        }
+        p->child[e]->dI_floor = 0.f;
+        p->child[e]->acc = e;
+    }
+    const daxm_plan* c = p->child[0];
+    p->M = c->M;
+    p->rows = c->rows;
+    p->C = c->C;
+    p->S = c->S;
+    p->tr0 = c->tr0;
+    p->n_tr = c->n_tr;
+    p->n_tc = c->n_tc;
+    *out = p;
+    return DAXM_OK;
+}
+
 daxm_status daxm_plan_info(const daxm_plan* p, int64_t* n_bins, int64_t* rows, int64_t* cols) {
     if (!p) return DAXM_ERR_INVALID_ARGUMENT;
     if (n_bins) *n_bins = p->M;
@@ -1135,6 +1183,29 @@ daxm_status daxm_plan_info(const daxm_plan* p, int64_t* n_bins, int64_t* rows, i
 
 daxm_status daxm_plan_stats_get(const daxm_plan* p, daxm_plan_stats* st) {
     if (!p || !st) return DAXM_ERR_INVALID_ARGUMENT;
+    if (p->child[0]) {  // both-edges mode: the leading child's numbers, sums of the per-plan counts
+        daxm_plan_stats b;
+        daxm_status s = daxm_plan_stats_get(p->child[0], st);
+        if (s == DAXM_OK) s = daxm_plan_stats_get(p->child[1], &b);
+        if (s != DAXM_OK) return s;
+        st->contrib_pairs += b.contrib_pairs;
+        st->contrib_pixels += b.contrib_pixels;
+        st->window_pairs += b.window_pairs;
+        st->general_tiles_u16 += b.general_tiles_u16;
+        st->general_tiles_f32 += b.general_tiles_f32;
+        st->prepass_ms += b.prepass_ms;
+        st->device_bytes += b.device_bytes;
+        st->lock_ring_violations += b.lock_ring_violations;
+        st->row_tiles_small += b.row_tiles_small;
+        st->row_tiles_large += b.row_tiles_large;
+        st->row_tiles_general += b.row_tiles_general;
+        st->row_tiles_gen += b.row_tiles_gen;
+        st->row_launches += b.row_launches;
+        st->row_path = st->row_path && b.row_path;
+        st->fit_max_err_bins = std::max(st->fit_max_err_bins, b.fit_max_err_bins);
+        st->fit_model_err_bins = std::max(st->fit_model_err_bins, b.fit_model_err_bins);
+        return DAXM_OK;
+    }
     *st = p->stats;
     st->row_path = p->row_ok && getenv("DAXM_NO_ROW") == nullptr ? 1 : 0;
     if (p->d_lock_err) {  // synchronous read of the step-locked kernel's violation counter
@@ -1188,6 +1259,8 @@ static DepositArgs make_args(const daxm_plan* p, int dtype) {
     a.m_ref = p->gc.m_ref;
     a.point_mode = p->gc.point_mode;
     a.sign = p->g.edge == DAXM_EDGE_TRAILING ? -1.f : 1.f;
+    a.dI_floor = p->dI_floor;
+    a.acc = p->acc;
     a.stack = nullptr;
     a.table = p->d_table;
     a.toff = p->d_toff;
@@ -1228,6 +1301,8 @@ static RowArgs make_row_args(const daxm_plan* p) {
     a.max_nv = p->max_nv_row;
     a.point_mode = p->gc.point_mode;
     a.sign = p->g.edge == DAXM_EDGE_TRAILING ? -1.f : 1.f;
+    a.dI_floor = p->dI_floor;
+    a.acc = p->acc;
     a.stack = nullptr;
     a.use_cutoff = p->use_cutoff;
     a.cutoff = p->cutoff;
@@ -1396,9 +1471,21 @@ static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_o
 
 static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float* d_out, cudaStream_t st,
                                int tr_begin = 0, int tr_end = -1) {
-    const bool fast = fast_possible(p, dt);
+    if (p->child[0]) {  // both-edges mode: the leading child stores, the trailing child adds
+        for (int e = 0; e < 2; ++e) {
+            daxm_status s = run_deposit(p->child[e], d_stack, dt, d_out, st, tr_begin, tr_end);
+            if (s != DAXM_OK) {
+                p->err = p->child[e]->err;
+                return s;
+            }
+        }
+        return DAXM_OK;
+    }
+    bool fast = fast_possible(p, dt);
     if (fast && p->row_ok && getenv("DAXM_NO_ROW") == nullptr)
         return run_row(p, d_stack, dt, d_out, st, tr_begin, tr_end < 0 ? -1 : tr_end);
+    // both-edges children off the row path: the general kernel alone clamps and accumulates
+    if (p->is_child) fast = false;
     if (fast) {
         daxm_status s = encode_maps(p, d_stack, dt, d_out);
         if (s != DAXM_OK) return s;
@@ -1408,7 +1495,7 @@ static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float*
     a.tr_end = tr_end < 0 ? p->n_tr : tr_end;
     a.stack = d_stack;
     cudaError_t e = cudaSuccess;
-    const bool live = a.use_cutoff && getenv("DAXM_NO_TILE_LIVE") == nullptr;
+    const bool live = a.use_cutoff && !p->is_child && getenv("DAXM_NO_TILE_LIVE") == nullptr;
     if (live) {  // dead tiles: flags here; their zero fill after the fork, beside the class launches
         e = launch_cutoff_tiles(a, d_stack, dt, d_out, p->d_live, 0, st);
         if (e != cudaSuccess) {
@@ -1555,6 +1642,11 @@ daxm_status daxm_set_cutoff(daxm_plan* p, int enable, double cutoff) {
     if (enable && !(cutoff == cutoff)) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "cutoff is NaN");
     p->use_cutoff = enable ? 1 : 0;
     p->cutoff = (float)cutoff;
+    for (daxm_plan* c : p->child)
+        if (c) {
+            c->use_cutoff = p->use_cutoff;
+            c->cutoff = p->cutoff;
+        }
     return DAXM_OK;
 }
 
@@ -1620,6 +1712,10 @@ daxm_status daxm_depth_profile(daxm_plan* p, const float* d_out, double* d_profi
 
 void daxm_destroy(daxm_plan* p) {
     if (!p) return;
+    for (daxm_plan*& c : p->child) {
+        daxm_destroy(c);
+        c = nullptr;
+    }
     {
         DeviceGuard guard(p->device);
         cudaDeviceSynchronize();

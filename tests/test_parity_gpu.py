@@ -183,6 +183,39 @@ def test_zero_skip_equals_full_run(daxm, name, dtype, monkeypatch):
     parity.check(skip, oracle.reconstruct(g, host), host, f"{name} zero skip")
 
 
+@pytest.mark.parametrize("name,dtype,pixel_model", [("C1", "f32", "finite"), ("C1", "u16", "point"),
+                                                    ("C2", "f32", "finite"), ("C3", "u16", "finite")])
+def test_both_edges_mode(daxm, name, dtype, pixel_model):
+    """edge = "both" (reading R16): the leading child plan stores the reconstruction of the
+    intensity decreases, the trailing child adds (TMA reduce-add) that of the increases; element
+    by element against the oracle's both-edges mode, whose pins are tests/test_oracle_both.py."""
+    g = synth.geometry(name, edge="both", pixel_model=pixel_model)
+    host = synth.stack_numpy(synth.make_maps(name), dtype, noise=True)
+    gpu, st = run_gpu(daxm, g, host)
+    assert st["row_path"] == 1, st
+    ref = oracle.reconstruct(g, host)
+    parity.check(gpu, ref, host, f"{name} both edges")
+    # the mode is really both: not the leading reconstruction
+    lead = oracle.reconstruct(synth.geometry(name, pixel_model=pixel_model), host)
+    assert np.abs(ref - lead).max() > 10 * np.abs(gpu - ref).max()
+
+
+def test_both_edges_host_path_and_cutoff(daxm):
+    """The both-edges mode through daxm_reconstruct_host (band pipeline) and with a cutoff."""
+    import torch
+    g = synth.geometry("C3", edge="both")
+    host = synth.stack_numpy(synth.make_maps("C3"), "u16", noise=True)
+    ref = oracle.reconstruct(g, host)
+    cut = oracle.select_cutoff(host[0], 0.3)
+    with daxm.create(g, device=0) as plan:
+        out = np.asarray(plan.reconstruct_host(host))
+        parity.check(out, ref, host, "C3 both host")
+        plan.set_cutoff(cut)
+        dev = plan.reconstruct(torch.from_numpy(host).cuda()).cpu().numpy()
+    ref[:, ~oracle.active_pixels(host[0], cut)] = 0
+    parity.check(dev, ref, host, "C3 both cutoff")
+
+
 # ------------------------------------------------------------------ edge cases
 
 def test_ragged_detector(daxm):
