@@ -226,6 +226,18 @@ daxm_status daxm_select_cutoff_sharded(daxm_plan *p, const void *d_stack, daxm_d
  * Errors: INVALID_ARGUMENT (NULL pointers), CUDA. */
 daxm_status daxm_depth_profile(daxm_plan *p, const float *d_out, double *d_profile, void *cuda_stream);
 
+/* daxm_reconstruct_profile -- daxm_reconstruct plus the depth profile of its output (as
+ * daxm_depth_profile: d_profile[m] = sum over the plan's pixels of d_out[m][row][col], fp64),
+ * fused: when every row tile runs the row-segment kernel (stats.row_path = 1, no general tiles,
+ * one edge), the kernel sums each final plane of its tile while the plane is staged in shared
+ * memory (an fp32 sum of the tile's 128 values) and one short kernel adds the tiles' sums in
+ * fixed order, so the output is not read back.  Otherwise it runs daxm_reconstruct and then
+ * daxm_depth_profile.  The first fused call allocates rows/2 * C/64 * M floats of plan memory.
+ * Arguments, layouts and errors as daxm_reconstruct plus d_profile: device double[M],
+ * overwritten (NULL: INVALID_ARGUMENT). */
+daxm_status daxm_reconstruct_profile(daxm_plan *p, const void *d_stack, daxm_dtype dtype, float *d_out,
+                                     double *d_profile, void *cuda_stream);
+
 /* Detail text for the last failing call on this plan ("" if none).  Valid until
  * the next call on the plan. */
 const char *daxm_last_error(const daxm_plan *p);

@@ -95,6 +95,8 @@ def lib():
         L.daxm_select_cutoff_sharded.restype = C.c_int
         L.daxm_depth_profile.argtypes = [P, P, P, P]
         L.daxm_depth_profile.restype = C.c_int
+        L.daxm_reconstruct_profile.argtypes = [P, P, C.c_int, P, P, P]
+        L.daxm_reconstruct_profile.restype = C.c_int
         L.daxm_last_error.argtypes = [P]
         L.daxm_last_error.restype = C.c_char_p
         L.daxm_create_error.restype = C.c_char_p
@@ -233,6 +235,29 @@ class Plan:
             raise errors[0]
         self._check(st)
         return val.value
+
+    def reconstruct_profile(self, stack, out=None, profile=None, stream=None):
+        """daxm_reconstruct_profile: reconstruction and its depth profile (fused on the row path)
+        -> (out [M][rows][C] float32 CUDA, profile [M] float64 CUDA)."""
+        import torch
+        dt = self._dtype_of(stack)
+        if out is None:
+            out = torch.empty(self.output_shape(), dtype=torch.float32, device=stack.device)
+        if not (out.is_cuda and out.is_contiguous() and out.dtype == torch.float32 and
+                tuple(out.shape) == self.output_shape() and out.device == stack.device):
+            raise ValueError("out must be a contiguous float32 CUDA tensor of shape [M][rows][C] on the "
+                             "stack's device")
+        if profile is None:
+            profile = torch.empty(self.n_bins, dtype=torch.float64, device=stack.device)
+        if not (profile.is_cuda and profile.is_contiguous() and profile.dtype == torch.float64 and
+                tuple(profile.shape) == (self.n_bins,) and profile.device == stack.device):
+            raise ValueError("profile must be a contiguous float64 CUDA tensor [M] on the stack's device")
+        if stream is None:
+            stream = torch.cuda.current_stream(stack.device)
+        self._check(lib().daxm_reconstruct_profile(self._h, C.c_void_p(stack.data_ptr()), dt,
+                                                   C.c_void_p(out.data_ptr()), C.c_void_p(profile.data_ptr()),
+                                                   C.c_void_p(stream.cuda_stream)))
+        return out, profile
 
     def depth_profile(self, out, profile=None, stream=None):
         """Per-depth-bin total intensity of `out` ([M][rows][C] float32 CUDA) -> float64 CUDA [M]."""

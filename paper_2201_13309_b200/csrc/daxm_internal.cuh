@@ -246,6 +246,7 @@ struct RowArgs {
     int use_cutoff;
     float cutoff;
     const unsigned char* live;  // [n_rt] per-call row_live_kernel flags (0: zeros written), or NULL
+    float* prof_part;      // [n_rt][M] per-tile plane sums (fused depth-profile epilogue), or NULL
     unsigned* err;         // DAXM_ROW_CHECK builds: schedule violations (must stay 0)
 };
 
@@ -278,6 +279,8 @@ cudaError_t select_cutoff(const void* plane0, int dtype, size_t n, unsigned long
 cudaError_t launch_cutoff_tiles(const DepositArgs& a, const void* plane0, int dtype, float* out, unsigned char* live,
                                 int phase, cudaStream_t st);  // phase 0: tile flags; 1: zero fill of dead tiles
 cudaError_t launch_depth_profile(const float* out, int M, size_t plane, double* profile, cudaStream_t st);
+// profile[m] = sum over row tiles [rt0, rt0 + n) of part[rt][m] (fp64, fixed order)
+cudaError_t launch_profile_reduce(const float* part, int rt0, int n, int M, double* profile, cudaStream_t st);
 size_t fast_smem_bytes(int dtype, int max_nv);
 cudaError_t launch_deposit(const DepositArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
                            const void* stack, int dtype, float* out, bool fast_enabled, cudaStream_t st,

@@ -315,6 +315,8 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
     if (!__any_sync(0xffffffffu, any_act)) {  // no active walk: the tile's output is zero
         fence_proxy_async_smem();
         __syncwarp();
+        if (a.prof_part)  // fused depth profile: this tile adds nothing to any plane
+            for (int m = lane; m < a.M; m += 32) a.prof_part[(size_t)rt * a.M + m] = 0.f;
         if (lane == 0 && !a.acc) {  // (adding zeros: nothing to do)
             for (int P = 0; P < a.M; P += RW_PB) tma_store_3d(&out_map, col0, rowl, P, smem + L::OFF_OUT);
             bulk_commit();
@@ -452,6 +454,29 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
                     sts128u(s_copy + s * PLANE_B, make_uint4(y.x == SENT ? x.x : y.x, y.y == SENT ? x.y : y.y,
                                                              y.z == SENT ? x.z : y.z, y.w == SENT ? x.w : y.w));
                     sts128u(s_copy + (RB + s) * PLANE_B, make_uint4(SENT, SENT, SENT, SENT));
+                }
+            }
+        }
+        if (a.prof_part) {  // fused depth-profile epilogue: the tile's sum of each final plane
+            __syncwarp();    // every lane's edge stores (and the fold) before the sums read them
+#pragma unroll 1
+            for (int b = b0; b < nb; ++b) {
+                const int s0 = (b * RW_PB) & (RB - 1);
+                float v[RW_PB];
+#pragma unroll
+                for (int q = 0; q < RW_PB; ++q) {
+                    const float4 x = lds128(s_copy + (s0 + q) * PLANE_B);
+                    v[q] = (x.x + x.y) + (x.z + x.w);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int q = 0; q < RW_PB; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
+                if (lane < RW_PB && b * RW_PB + lane < a.M) {
+                    float w = v[0];
+#pragma unroll
+                    for (int q = 1; q < RW_PB; ++q) w = lane == q ? v[q] : w;
+                    a.prof_part[(size_t)rt * a.M + b * RW_PB + lane] = w;
                 }
             }
         }

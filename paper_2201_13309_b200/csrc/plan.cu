@@ -91,6 +91,7 @@ struct daxm_plan {
     int max_nv_row = 0;                    // largest row-tile step range
     RowTile* d_rt = nullptr;
     unsigned char* d_rlive = nullptr;  // row tiles' live flags of the last call (exact zero-dI skip)
+    float* d_prof_part = nullptr;      // [n_rt][M] fused depth-profile partial sums (allocated on use)
     float* d_rcoef = nullptr;
     int* d_rlist = nullptr;                // class lists [small][large][general], each ascending
     std::vector<int> h_rlist;
@@ -648,11 +649,13 @@ void free_plan_memory(daxm_plan* p) {
     p->d_lock_err = nullptr;
     cudaFree(p->d_rt);
     cudaFree(p->d_rlive);
+    cudaFree(p->d_prof_part);
     cudaFree(p->d_rcoef);
     cudaFree(p->d_rlist);
     cudaFree(p->d_row_err);
     p->d_rt = nullptr;
     p->d_rlive = nullptr;
+    p->d_prof_part = nullptr;
     p->d_rcoef = nullptr;
     p->d_rlist = nullptr;
     p->d_row_err = nullptr;
@@ -1307,6 +1310,7 @@ static RowArgs make_row_args(const daxm_plan* p) {
     a.use_cutoff = p->use_cutoff;
     a.cutoff = p->cutoff;
     a.live = nullptr;
+    a.prof_part = nullptr;
     a.err = p->d_row_err;
     return a;
 }
@@ -1402,7 +1406,7 @@ static daxm_status encode_maps(daxm_plan* p, const void* d_stack, int dt, float*
 // for the row tiles not admitted, forked onto the plan's class streams and joined back into st.
 // tr_begin / tr_end (deposit-tile rows, host pipeline) select the row tiles of those rows.
 static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_out, cudaStream_t st, int tr_begin,
-                           int tr_end) {
+                           int tr_end, double* d_profile = nullptr) {
     daxm_status s = encode_maps(p, d_stack, dt, d_out);
     if (s != DAXM_OK) return s;
     int ra = 0, rb = p->n_rr;
@@ -1425,6 +1429,7 @@ static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_o
     }
     RowArgs a = make_row_args(p);
     a.stack = d_stack;
+    a.prof_part = d_profile ? p->d_prof_part : nullptr;
     if (getenv("DAXM_NO_ZERO_SKIP") == nullptr) {  // exact zero-dI skip, before the class launches fork
         cudaError_t z = launch_row_live(a, ra * p->n_rc, (rb - ra) * p->n_rc, p->d_rlive, dt, st);
         if (z != cudaSuccess) {
@@ -1462,6 +1467,8 @@ static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_o
             if (e == cudaSuccess) e = j;
         }
     }
+    if (e == cudaSuccess && d_profile) e = launch_profile_reduce(p->d_prof_part, ra * p->n_rc, (rb - ra) * p->n_rc, p->M,
+                                                                d_profile, st);
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(p, DAXM_ERR_CUDA, "row deposit launch: %s", cudaGetErrorString(e));
@@ -1539,6 +1546,41 @@ daxm_status daxm_reconstruct(daxm_plan* p, const void* d_stack, daxm_dtype dt, f
         return fail(p, DAXM_ERR_INVALID_ARGUMENT, "stack and output must be 16-byte aligned");
     DeviceGuard guard(p->device);
     return run_deposit(p, d_stack, (int)dt, d_out, (cudaStream_t)cuda_stream);
+}
+
+daxm_status daxm_reconstruct_profile(daxm_plan* p, const void* d_stack, daxm_dtype dt, float* d_out, double* d_profile,
+                                     void* cuda_stream) {
+    if (!p) return DAXM_ERR_INVALID_ARGUMENT;
+    p->err.clear();
+    if (!d_stack || !d_out || !d_profile) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "NULL stack, output or profile");
+    if (dt != DAXM_U16 && dt != DAXM_F32) return fail(p, DAXM_ERR_INVALID_ARGUMENT, "unknown dtype %d", (int)dt);
+    if ((reinterpret_cast<uintptr_t>(d_stack) | reinterpret_cast<uintptr_t>(d_out)) & 15)
+        return fail(p, DAXM_ERR_INVALID_ARGUMENT, "stack and output must be 16-byte aligned");
+    DeviceGuard guard(p->device);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    // fused: every row tile in the row kernel (its epilogue sums each final plane per tile)
+    const bool fused = !p->child[0] && p->row_ok && p->n_rcls[daxm_plan::N_RCLS - 1] == 0 &&
+                       fast_possible(p, (int)dt) && getenv("DAXM_NO_ROW") == nullptr &&
+                       getenv("DAXM_NO_FUSED_PROFILE") == nullptr;
+    if (fused) {
+        if (!p->d_prof_part) {
+            const size_t n = (size_t)p->n_rr * p->n_rc * p->M;
+            if (cudaMalloc(&p->d_prof_part, n * sizeof(float)) != cudaSuccess) {
+                cudaGetLastError();
+                return fail(p, DAXM_ERR_OUT_OF_MEMORY, "profile partial sums (%zu floats)", n);
+            }
+            p->stats.device_bytes += (int64_t)(n * sizeof(float));
+        }
+        return run_row(p, d_stack, (int)dt, d_out, st, 0, -1, d_profile);
+    }
+    daxm_status s = run_deposit(p, d_stack, (int)dt, d_out, st);
+    if (s != DAXM_OK) return s;
+    cudaError_t e = launch_depth_profile(d_out, p->M, (size_t)p->rows * p->C, d_profile, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(p, DAXM_ERR_CUDA, "depth profile launch: %s", cudaGetErrorString(e));
+    }
+    return DAXM_OK;
 }
 
 daxm_status daxm_reconstruct_host(daxm_plan* p, const void* h_stack, daxm_dtype dt, float* h_out, void* cuda_stream) {

@@ -33,7 +33,25 @@ __global__ void __launch_bounds__(512) depth_profile_kernel(const float* __restr
     }
 }
 
+// The fused epilogue's second half: the row kernel leaves each row tile's per-plane sum in
+// part[rt][m]; one thread per plane adds the tiles' sums in tile order (coalesced over m).
+__global__ void __launch_bounds__(256) profile_reduce_kernel(const float* __restrict__ part, int rt0, int n, int M,
+                                                             double* __restrict__ profile) {
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= M) return;
+    double acc = 0.0;
+    const float* p = part + (size_t)rt0 * M + m;
+    for (int t = 0; t < n; ++t) acc += (double)__ldcs(p + (size_t)t * M);
+    profile[m] = acc;
+}
+
 }  // namespace
+
+cudaError_t launch_profile_reduce(const float* part, int rt0, int n, int M, double* profile, cudaStream_t st) {
+    if (M <= 0) return cudaSuccess;
+    profile_reduce_kernel<<<(M + 255) / 256, 256, 0, st>>>(part, rt0, n, M, profile);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_depth_profile(const float* out, int M, size_t plane, double* profile, cudaStream_t st) {
     if (M <= 0) return cudaSuccess;

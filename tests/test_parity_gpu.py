@@ -435,6 +435,36 @@ def test_depth_profile(daxm, name, dtype):
     assert np.abs(prof - ref).max() <= 1e-5 * scale
 
 
+@pytest.mark.parametrize("name,dtype,fraction", [("C1", "f32", None), ("C2", "f32", None), ("C3", "u16", None),
+                                                 ("C3", "u16", 0.2), ("C2", "u16", "noise-free")])
+def test_fused_profile(daxm, name, dtype, fraction, monkeypatch):
+    """daxm_reconstruct_profile: the row kernel's fused per-tile plane sums + tile reduction give
+    the oracle's depth profile (oracle.depth_profile, pinned by conservation), the same output as
+    daxm_reconstruct, and the unfused profile of that output; also with a cutoff and with the
+    zero-dI skip's dead tiles (noise-free stack)."""
+    import torch
+    g = synth.geometry(name)
+    host = synth.stack_numpy(synth.make_maps(name), dtype, noise=fraction != "noise-free")
+    ref_out = oracle.reconstruct(g, host)
+    with daxm.create(g, device=0) as plan:
+        assert plan.stats()["row_path"] == 1
+        st = torch.from_numpy(host).cuda()
+        if isinstance(fraction, float):
+            cut = oracle.select_cutoff(host[0], fraction)
+            plan.set_cutoff(cut)
+            ref_out[:, ~oracle.active_pixels(host[0], cut)] = 0
+        out, prof = plan.reconstruct_profile(st)
+        plain = plan.reconstruct(st)
+        unfused = plan.depth_profile(plain)
+        assert torch.equal(out, plain)
+        prof, unfused = prof.cpu().numpy(), unfused.cpu().numpy()
+    scale = parity.abs_dI(host).sum()
+    ref = oracle.depth_profile(ref_out)
+    assert np.abs(prof - ref).max() <= 1e-5 * scale
+    assert np.allclose(prof, unfused, rtol=1e-6, atol=1e-7 * scale)
+    parity.check(out.cpu().numpy(), ref_out, host, f"{name} fused profile output")
+
+
 @pytest.mark.parametrize("name,dtype", [("C2", "f32"), ("C3", "u16")])
 @pytest.mark.parametrize("fraction", [0.003, 0.25, 1.0])
 def test_select_cutoff_matches_oracle(daxm, name, dtype, fraction):
