@@ -22,7 +22,9 @@
  *   daxm_reconstruct   device stack [S][rows][C] -> device output [M][rows][C]
  *                      (stream-ordered, asynchronous, allocates nothing,
  *                      CUDA-graph capturable)
- *   daxm_reconstruct_host  the same from/to HOST buffers (copies included)
+ *   daxm_reconstruct_host  the same from/to HOST buffers (copies included;
+ *                      out of core under a device-memory budget,
+ *                      daxm_set_host_budget / daxm_host_ring_info)
  *   daxm_plan_info / daxm_plan_stats / daxm_last_error / daxm_status_string
  *   daxm_destroy
  */
@@ -175,9 +177,28 @@ daxm_status daxm_reconstruct(daxm_plan *p, const void *d_stack, daxm_dtype dt, f
  * ([S][rows][C] of dt) to device buffers owned by the plan (allocated on first
  * use), reconstructs, copies the result to h_out ([M][rows][C] float32) and
  * synchronises `cuda_stream`.  Pinned host buffers give full PCIe/C2C speed;
- * pageable buffers work too. */
+ * pageable buffers work too.
+ * Device memory: with no budget set (daxm_set_host_budget) or a budget that holds the whole stack
+ * and output, the plan keeps one device copy of both and overlaps band copies with the deposit.
+ * Otherwise the call runs OUT OF CORE (the paper's row chunking, Fig. 2, and its
+ * transfer stage): the rows are cut into bands of B rows (B a multiple of 128, the
+ * largest whose two ring slots fit the budget), each band has its own plan (built on the first
+ * such call, cached), and band b goes H2D into ring slot b mod 2, is reconstructed there and
+ * returns D2H while band b + 1 arrives -- device memory O(band), not O(stack).  Output of
+ * 128-aligned bands equals the whole-plan output bit for bit (same tiles, same kernels).
+ * Errors: as daxm_reconstruct; OUT_OF_MEMORY when the budget cannot hold two 128-row slots. */
 daxm_status daxm_reconstruct_host(daxm_plan *p, const void *h_stack, daxm_dtype dt, float *h_out,
                                   void *cuda_stream);
+
+/* daxm_set_host_budget -- cap, in bytes, on the device memory daxm_reconstruct_host may hold for
+ * stack and output buffers (0 = no cap, the default).  Takes effect at the next host call; band
+ * plans already built for another band height are rebuilt.  Errors: INVALID_ARGUMENT (NULL plan). */
+daxm_status daxm_set_host_budget(daxm_plan *p, uint64_t device_bytes);
+
+/* daxm_host_ring_info -- the out-of-core layout of the last daxm_reconstruct_host call: band rows
+ * B and band count (both 0 when the call ran in core) and the device bytes of the two ring slots.
+ * Any output pointer may be NULL. */
+daxm_status daxm_host_ring_info(const daxm_plan *p, int64_t *band_rows, int64_t *n_bands, int64_t *ring_bytes);
 
 /* daxm_set_cutoff -- intensity cutoff ("d_cutoff", kernel setTwo argument; the
  * pixel-percentage experiment).  Reading R14: with enable != 0 a

@@ -86,6 +86,10 @@ def lib():
         L.daxm_reconstruct.restype = C.c_int
         L.daxm_reconstruct_host.argtypes = [P, P, C.c_int, P, P]
         L.daxm_reconstruct_host.restype = C.c_int
+        L.daxm_set_host_budget.argtypes = [P, C.c_uint64]
+        L.daxm_set_host_budget.restype = C.c_int
+        L.daxm_host_ring_info.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+        L.daxm_host_ring_info.restype = C.c_int
         L.daxm_set_cutoff.argtypes = [P, C.c_int, C.c_double]
         L.daxm_set_cutoff.restype = C.c_int
         L.daxm_select_cutoff.argtypes = [P, P, C.c_int, C.c_double, C.POINTER(C.c_double), P]
@@ -296,6 +300,19 @@ class Plan:
         self._check(lib().daxm_reconstruct_host(self._h, C.c_void_p(stack.data_ptr()), dt,
                                                 C.c_void_p(out.data_ptr()), C.c_void_p(st)))
         return out
+
+    def set_host_budget(self, device_bytes: int):
+        """Cap the device memory reconstruct_host may hold (0 = no cap): above it the host path runs
+        out of core through a two-slot ring of 128-aligned row bands (daxm_set_host_budget)."""
+        if device_bytes < 0:
+            raise ValueError("device_bytes must be >= 0")
+        self._check(lib().daxm_set_host_budget(self._h, C.c_uint64(int(device_bytes))))
+
+    def host_ring_info(self) -> dict:
+        """Layout of the last reconstruct_host call (band_rows = n_bands = 0: it ran in core)."""
+        v = [C.c_int64() for _ in range(3)]
+        self._check(lib().daxm_host_ring_info(self._h, *[C.byref(x) for x in v]))
+        return {"band_rows": v[0].value, "n_bands": v[1].value, "ring_bytes": v[2].value}
 
     def close(self):
         if self._h is not None and self._h.value:

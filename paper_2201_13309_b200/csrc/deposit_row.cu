@@ -45,6 +45,9 @@
 #include "fp2.cuh"
 #include "ptx.cuh"
 
+#ifndef DAXM_RW_TAU_GLOBAL
+#define DAXM_RW_TAU_GLOBAL 0  // 1: wire travel tau read from the plan's fp64 t (L1) instead of a shared table
+#endif
 #define DAXM_PRAGMA_(x) _Pragma(#x)
 #define DAXM_PRAGMA_UNROLL(n) DAXM_PRAGMA_(unroll n)
 #ifndef DAXM_ROW_CHECK
@@ -67,7 +70,7 @@ struct RowSmem {
     static constexpr int OFF_IN = OFF_OUT + OUT_SLOTS * PLANE_B;
     static constexpr int OFF_BAR = OFF_IN + RW_H * IN_HALF;
     static constexpr int OFF_TAU = OFF_BAR + NG * 8;
-    static size_t bytes(int max_nv) { return (size_t)OFF_TAU + 4 * (size_t)(max_nv + 4) + 128; }
+    static size_t bytes(int max_nv) { return (size_t)OFF_TAU + (DAXM_RW_TAU_GLOBAL ? 0 : 4 * (size_t)(max_nv + 4)) + 128; }
 };
 
 __device__ __forceinline__ void sts_zero4(uint32_t addr) {
@@ -245,8 +248,11 @@ __device__ __forceinline__ void row_starts(const RowWalk wk[2][2], int lane, int
     vend = __reduce_max_sync(0xffffffffu, ve);
 }
 
+#ifndef DAXM_RW_MINB
+#define DAXM_RW_MINB 11  // resident CTAs (= warps) per SM the separated variant's registers allow
+#endif
 template <typename T, bool POINT, int RB, bool GEN, int NB>
-__global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_constant__ CUtensorMap in_map,
+__global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const __grid_constant__ CUtensorMap in_map,
                                                             const __grid_constant__ CUtensorMap out_map,
                                                             const RowArgs a) {
     static_assert(!(GEN && POINT), "the general-span variant is for finite pixels");
@@ -269,7 +275,8 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
     float* tau = reinterpret_cast<float*>(smem + L::OFF_TAU);
 
-    for (int q = lane; q < nvt; q += 32) tau[q] = (float)(a.t[dir > 0 ? ti.k_lo + q : ti.k_hi - q] - ti.t_ref);
+    if (!DAXM_RW_TAU_GLOBAL)
+        for (int q = lane; q < nvt; q += 32) tau[q] = (float)(a.t[dir > 0 ? ti.k_lo + q : ti.k_hi - q] - ti.t_ref);
     if (lane == 0) {
         for (int g = 0; g < NG; ++g) mbar_init(&bars[g], 1);
         fence_mbar_init();
@@ -369,6 +376,9 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
     const uint32_t in_lane =
         opaque(sbase + L::OFF_IN + (uint32_t)(hh * L::IN_HALF) + (uint32_t)(2 * (lane & 15)) * (uint32_t)sizeof(T));
     const uint32_t tau_l = opaque(sbase + L::OFF_TAU + 4u * (uint32_t)vmin_h);
+    // (DAXM_RW_TAU_GLOBAL) visit v of the lane's half is step tg[dir v]; tau = (float)(t - t_ref) as the table
+    const double* tg = a.t + (dir > 0 ? ti.k_lo + vmin_h : ti.k_hi - vmin_h);
+    const double t_ref = ti.t_ref;
     const uint32_t ob = sbase + L::OFF_OUT + (uint32_t)(32 * hh + 2 * (lane & 15)) * 4u;  // column 2i of a plane
     const uint32_t ob0 = opaque(ob + 4u * (uint32_t)hh), ob1 = opaque(ob + 4u * (uint32_t)(hh ^ 1));  // pair 0 / 1
     const uint32_t swap = hh ? 0x1032u : 0x3210u;  // pair p's column is the (p ^ h)-th of the lane's two
@@ -384,7 +394,10 @@ __global__ void __launch_bounds__(32, GEN ? 8 : 11) deposit_row(const __grid_con
 
     // wire travel and the two pairs' intensities (rows 0, 1) at visit v of the lane's half
     auto fetch = [&](int v, float& t, float2 I[2]) {
-        t = lds_f32(tau_l + 4u * (uint32_t)v);
+        if (DAXM_RW_TAU_GLOBAL)
+            t = (float)(__ldg(tg + (dir > 0 ? v : -v)) - t_ref);
+        else
+            t = lds_f32(tau_l + 4u * (uint32_t)v);
         const uint32_t ad = in_lane + (uint32_t)((v ^ xr_) & (NB - 1)) * (uint32_t)L::IN_SLOT;
         if constexpr (sizeof(T) == 2) {
             const uint32_t w0 = __byte_perm(lds_u32(ad), 0u, swap), w1 = __byte_perm(lds_u32(ad + 64u), 0u, swap);

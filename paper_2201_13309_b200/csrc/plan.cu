@@ -78,6 +78,17 @@ struct daxm_plan {
     float* d_out_buf = nullptr;
     size_t out_buf_bytes = 0;
     cudaStream_t st_in = nullptr, st_out = nullptr;  // host-path pipeline streams
+    // out-of-core host path (daxm_set_host_budget): band plans of ring_rows rows and a two-slot
+    // device ring of [S][B][C] stacks and [M][B][C] outputs
+    uint64_t host_budget = 0;
+    int ring_rows = 0;                 // band rows the band plans were built for (0: none)
+    std::vector<daxm_plan*> bands;     // band b: plan-local rows [band_r0[b], band_r0[b + 1])
+    std::vector<int> band_r0;
+    void* d_ring_in[2] = {nullptr, nullptr};
+    float* d_ring_out[2] = {nullptr, nullptr};
+    size_t ring_in_bytes = 0, ring_out_bytes = 0;
+    cudaEvent_t ev_ring[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    int last_ring_rows = 0, last_ring_bands = 0;  // layout of the last host call (0: in core)
     cudaStream_t st_cls[2] = {nullptr, nullptr};     // concurrent step-locked class launches (fork/join)
     cudaEvent_t ev_cls[3] = {nullptr, nullptr, nullptr};
     std::vector<cudaEvent_t> ev;
@@ -628,6 +639,25 @@ void rodrigues(const double R[3], double rho[9]) {
         }
 }
 
+// out-of-core ring: band plans and slots
+void free_ring(daxm_plan* p) {
+    for (daxm_plan* b : p->bands) daxm_destroy(b);
+    p->bands.clear();
+    p->band_r0.clear();
+    p->ring_rows = 0;
+    for (int i = 0; i < 2; ++i) {
+        cudaFree(p->d_ring_in[i]);
+        cudaFree(p->d_ring_out[i]);
+        p->d_ring_in[i] = nullptr;
+        p->d_ring_out[i] = nullptr;
+    }
+    p->ring_in_bytes = p->ring_out_bytes = 0;
+    for (cudaEvent_t& e : p->ev_ring) {
+        if (e) cudaEventDestroy(e);
+        e = nullptr;
+    }
+}
+
 void free_plan_memory(daxm_plan* p) {
     cudaFree(p->d_t);
     cudaFree(p->d_wire);
@@ -641,6 +671,10 @@ void free_plan_memory(daxm_plan* p) {
     cudaFree(p->d_list_f32);
     cudaFree(p->d_stack_buf);
     cudaFree(p->d_out_buf);
+    p->d_stack_buf = nullptr;
+    p->d_out_buf = nullptr;
+    p->stack_buf_bytes = p->out_buf_bytes = 0;
+    free_ring(p);
     cudaFree(p->d_hist);
     cudaFree(p->d_live);
     cudaFree(p->d_table);
@@ -1583,6 +1617,139 @@ daxm_status daxm_reconstruct_profile(daxm_plan* p, const void* d_stack, daxm_dty
     return DAXM_OK;
 }
 
+// Out-of-core host path (the paper's row chunking, P:L182-215 / Fig. 2, and
+// its host<->device transfer stage): bands of B rows (B a multiple of TILE_R, band edges
+// at global multiples of B, so every band plan's tiles are the whole plan's), one plan per band
+// (built on first use), a two-slot device ring.  Band b (slot s = b & 1):
+//   st_in : [wait: band b-2's deposit released in[s]]  H2D rows -> in[s]        record in-done
+//   st    : [wait: in-done, band b-2's D2H released out[s]]  deposit in[s] -> out[s]  record dep-done
+//   st_out: [wait: dep-done]  D2H out[s] -> host rows                          record out-done
+// so H2D of band b + 1, the deposit of band b and the D2H of band b - 1 overlap.
+static daxm_status host_ring(daxm_plan* p, const void* h_stack, daxm_dtype dt, float* h_out, cudaStream_t st) {
+    const size_t es = dt == DAXM_U16 ? 2 : 4;
+    const size_t row_in = (size_t)p->C * es, row_out = (size_t)p->C * sizeof(float);
+    const size_t per_row = row_in * p->S + row_out * p->M;  // one detector row of one slot
+    const uint64_t rows_fit = p->host_budget / (2 * per_row);
+    const int B = (int)std::min<uint64_t>(rows_fit / TILE_R, (uint64_t)(p->g.n_rows / TILE_R + 1)) * TILE_R;
+    if (B < TILE_R)
+        return fail(p, DAXM_ERR_OUT_OF_MEMORY,
+                    "host budget %llu bytes holds no two %d-row ring slots (%zu bytes per row and slot)",
+                    (unsigned long long)p->host_budget, TILE_R, per_row);
+    cudaError_t e = cudaSuccess;
+    if (p->ring_rows != B) {  // (re)build the band plans and the ring for this band height
+        free_ring(p);
+        const daxm_plan* src = p->child[0] ? p->child[0] : p;
+        daxm_geometry ge = p->g;
+        ge.wire_xyz = src->wire.data();
+        for (int r = p->g.row_begin; r < p->g.row_end;) {
+            const int r1 = std::min(p->g.row_end, (r / B + 1) * B);
+            ge.row_begin = r;
+            ge.row_end = r1;
+            daxm_plan* bp = nullptr;
+            daxm_status s = ge.edge == DAXM_EDGE_BOTH ? create_both(&ge, p->device, &bp)
+                                                      : create_one(&ge, p->device, false, &bp);
+            if (s != DAXM_OK) {
+                free_ring(p);
+                return fail(p, s, "band plan [%d, %d): %s", r, r1, g_create_err.c_str());
+            }
+            p->bands.push_back(bp);
+            p->band_r0.push_back(r - p->g.row_begin);
+            r = r1;
+        }
+        p->band_r0.push_back(p->rows);
+        for (cudaEvent_t& ev : p->ev_ring)
+            if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) break;
+        p->ring_rows = B;
+    }
+    int bmax = 0;
+    for (size_t b = 0; b + 1 < p->band_r0.size(); ++b) bmax = std::max(bmax, p->band_r0[b + 1] - p->band_r0[b]);
+    const size_t in_b = row_in * p->S * bmax, out_b = row_out * p->M * bmax;
+    if (e == cudaSuccess && (p->ring_in_bytes < in_b || p->ring_out_bytes < out_b)) {
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(p->d_ring_in[i]);
+            cudaFree(p->d_ring_out[i]);
+            p->d_ring_in[i] = nullptr;
+            p->d_ring_out[i] = nullptr;
+        }
+        p->ring_in_bytes = p->ring_out_bytes = 0;
+        for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+            e = cudaMalloc(&p->d_ring_in[i], in_b);
+            if (e == cudaSuccess) e = cudaMalloc(reinterpret_cast<void**>(&p->d_ring_out[i]), out_b);
+        }
+        if (e == cudaSuccess) {
+            p->ring_in_bytes = in_b;
+            p->ring_out_bytes = out_b;
+        }
+    }
+    if (e == cudaSuccess && !p->st_in) {
+        e = cudaStreamCreateWithFlags(&p->st_in, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->st_out, cudaStreamNonBlocking);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(p, e == cudaErrorMemoryAllocation ? DAXM_ERR_OUT_OF_MEMORY : DAXM_ERR_CUDA, "host ring: %s",
+                    cudaGetErrorString(e));
+    }
+    cudaEvent_t* ev_in = p->ev_ring;       // [slot] band's stack landed
+    cudaEvent_t* ev_dep = p->ev_ring + 2;  // [slot] band's deposit done (in[s] free, out[s] ready)
+    cudaEvent_t* ev_out = p->ev_ring + 4;  // [slot] band's output copied out (out[s] free)
+    // the caller's stream must reach this point before the first copy
+    e = cudaEventRecord(ev_dep[0], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->st_in, ev_dep[0], 0);
+    const int nb = (int)p->bands.size();
+    for (int b = 0; b < nb && e == cudaSuccess; ++b) {
+        const int s = b & 1, r0 = p->band_r0[b], nr = p->band_r0[b + 1] - r0;
+        daxm_plan* bp = p->bands[b];
+        if (b >= 2) e = cudaStreamWaitEvent(p->st_in, ev_dep[s], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(p->d_ring_in[s], nr * row_in, static_cast<const char*>(h_stack) + r0 * row_in,
+                                  p->rows * row_in, nr * row_in, p->S, cudaMemcpyHostToDevice, p->st_in);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_in[s], p->st_in);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_in[s], 0);
+        if (e == cudaSuccess && b >= 2) e = cudaStreamWaitEvent(st, ev_out[s], 0);
+        if (e != cudaSuccess) break;
+        daxm_set_cutoff(bp, p->use_cutoff, p->cutoff);
+        daxm_status ds = run_deposit(bp, p->d_ring_in[s], (int)dt, p->d_ring_out[s], st);
+        if (ds != DAXM_OK) {
+            p->err = bp->err;
+            cudaStreamSynchronize(st);
+            return ds;
+        }
+        e = cudaEventRecord(ev_dep[s], st);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(p->st_out, ev_dep[s], 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(reinterpret_cast<char*>(h_out) + r0 * row_out, p->rows * row_out, p->d_ring_out[s],
+                                  nr * row_out, nr * row_out, p->M, cudaMemcpyDeviceToHost, p->st_out);
+        if (e == cudaSuccess) e = cudaEventRecord(ev_out[s], p->st_out);
+    }
+    // join: the caller's stream sees the last copy out, then completes
+    if (e == cudaSuccess) e = cudaEventRecord(ev_out[0], p->st_out);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, ev_out[0], 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(p, DAXM_ERR_CUDA, "host ring: %s", cudaGetErrorString(e));
+    }
+    p->last_ring_rows = B;
+    p->last_ring_bands = nb;
+    return DAXM_OK;
+}
+
+daxm_status daxm_set_host_budget(daxm_plan* p, uint64_t device_bytes) {
+    if (!p) return DAXM_ERR_INVALID_ARGUMENT;
+    p->err.clear();
+    p->host_budget = device_bytes;
+    return DAXM_OK;
+}
+
+daxm_status daxm_host_ring_info(const daxm_plan* p, int64_t* band_rows, int64_t* n_bands, int64_t* ring_bytes) {
+    if (!p) return DAXM_ERR_INVALID_ARGUMENT;
+    if (band_rows) *band_rows = p->last_ring_rows;
+    if (n_bands) *n_bands = p->last_ring_bands;
+    if (ring_bytes) *ring_bytes = p->last_ring_rows ? (int64_t)(2 * (p->ring_in_bytes + p->ring_out_bytes)) : 0;
+    return DAXM_OK;
+}
+
 daxm_status daxm_reconstruct_host(daxm_plan* p, const void* h_stack, daxm_dtype dt, float* h_out, void* cuda_stream) {
     if (!p) return DAXM_ERR_INVALID_ARGUMENT;
     p->err.clear();
@@ -1594,6 +1761,18 @@ daxm_status daxm_reconstruct_host(daxm_plan* p, const void* h_stack, daxm_dtype 
     const size_t out_bytes = plane * p->M * sizeof(float);
     cudaStream_t st = (cudaStream_t)cuda_stream;
     cudaError_t e = cudaSuccess;
+    if (p->host_budget > 0 && in_bytes + out_bytes > p->host_budget) {  // out of core
+        if (p->d_stack_buf || p->d_out_buf) {  // the in-core buffers would break the budget
+            cudaStreamSynchronize(st);
+            cudaFree(p->d_stack_buf);
+            cudaFree(p->d_out_buf);
+            p->d_stack_buf = nullptr;
+            p->d_out_buf = nullptr;
+            p->stack_buf_bytes = p->out_buf_bytes = 0;
+        }
+        return host_ring(p, h_stack, dt, h_out, st);
+    }
+    p->last_ring_rows = p->last_ring_bands = 0;
     if (p->stack_buf_bytes < in_bytes) {
         cudaFree(p->d_stack_buf);
         p->d_stack_buf = nullptr;

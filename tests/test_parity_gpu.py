@@ -418,6 +418,48 @@ def test_host_path_pipelined_bands(daxm):
             assert torch.equal(dev.cpu(), hp) and torch.equal(hp, hp2)
 
 
+def test_host_path_out_of_core(daxm):
+    """Out-of-core host path (the paper's row chunking P:L182-215): under a
+    device budget smaller than stack + output the call streams 128-row bands through a two-slot
+    ring (device memory O(band)) and returns the whole-plan device-path output bit for bit --
+    also for a plan that starts inside a band, under a cutoff, and in both-edges mode; a budget
+    that cannot hold two 128-row slots is OUT_OF_MEMORY."""
+    import torch
+    g = synth.geometry("C3")
+    host = synth.stack_numpy(synth.make_maps("C3"), "u16", noise=True)
+    in_b, out_b = host.nbytes, 201 * 1024 * 1024 * 4
+    for rows in [(0, 1024), (70, 901)]:
+        band = np.ascontiguousarray(host[:, rows[0]:rows[1]])
+        with daxm.create(g, device=0, rows=rows) as plan:
+            dev = plan.reconstruct(torch.from_numpy(band).cuda()).cpu()
+            budget = (in_b + out_b) // 3  # the whole stack + output does not fit
+            plan.set_host_budget(budget)
+            hp = plan.reconstruct_host(torch.from_numpy(band).pin_memory())
+            info = plan.host_ring_info()
+            assert info["band_rows"] >= 128 and info["band_rows"] % 128 == 0, info
+            assert info["n_bands"] >= 2 and 0 < info["ring_bytes"] <= budget, info
+            assert torch.equal(dev, hp), rows
+            # cutoff through the ring = cutoff on the device path
+            c = float(np.quantile(band[0], 0.7))
+            plan.set_cutoff(c)
+            hc = plan.reconstruct_host(band)
+            dc = plan.reconstruct(torch.from_numpy(band).cuda()).cpu()
+            assert torch.equal(dc, hc) and not torch.equal(hc, hp)
+            plan.set_cutoff(None)
+            plan.set_host_budget(0)  # back in core
+            assert torch.equal(plan.reconstruct_host(band), dev) and plan.host_ring_info()["n_bands"] == 0
+            plan.set_host_budget(1 << 20)
+            with pytest.raises(daxm.DaxmError, match="OUT_OF_MEMORY|budget"):
+                plan.reconstruct_host(band)
+    gb = synth.geometry("C2", edge="both")
+    hb = synth.stack_numpy(synth.make_maps("C2"), "f32", noise=True)
+    with daxm.create(gb, device=0) as plan:
+        dev = plan.reconstruct(torch.from_numpy(hb).cuda()).cpu()
+        plan.set_host_budget((hb.nbytes + dev.numel() * 4) // 2)
+        hp = plan.reconstruct_host(hb)
+        assert plan.host_ring_info()["n_bands"] >= 2 and torch.equal(dev, hp)
+
+
 @pytest.mark.parametrize("name,dtype", [("C2", "f32"), ("C3", "u16")])
 def test_depth_profile(daxm, name, dtype):
     """daxm_depth_profile = the paper's image_set.depth_intensity: per-bin totals of the
