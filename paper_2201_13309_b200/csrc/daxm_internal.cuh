@@ -241,8 +241,9 @@ struct RowArgs {
     int point_mode;
     float sign;            // s: +1 leading, -1 trailing (reading R2)
     float dI_floor;        // s dI -> max(s dI, dI_floor): -inf, or 0 in the both-edges mode (R16)
-    int acc;               // 1: TMA reduce-add into the output (both-edges mode, second edge)
+    int acc;               // 1: add into the output (both-edges mode, second edge)
     const void* stack;     // band stack (plane 0 read for the intensity cutoff)
+    float* out;            // band output [M][rows][C] (the row kernel's plane copy-out)
     int use_cutoff;
     float cutoff;
     const unsigned char* live;  // [n_rt] per-call row_live_kernel flags (0: zeros written), or NULL

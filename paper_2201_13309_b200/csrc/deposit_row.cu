@@ -106,6 +106,14 @@ __device__ __forceinline__ void edge_st(uint32_t addr, float o, float F, float k
         : "r"(addr), "f"(o), "f"(kf), "f"(cnt), "f"(F), "n"(OFF)
         : "memory");
 }
+__device__ __forceinline__ void stg_cs_v4(float* g, float4 v) {  // streaming store (evict first)
+    asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(g), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void red_add_v4(float* g, float4 v) {  // one add per element (sm_90+)
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(g), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
@@ -434,79 +442,58 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
     auto frontier = [&](const RowState& S) {  // slowest walk's next edge index (no window: EM + 1)
         return warp_min((int)fminf(fminf(S.En[0].x, S.En[0].y), fminf(S.En[1].x, S.En[1].y)) + m_ref);
     };
-    // Output batches: once the slowest walk has passed a batch of RW_PB planes, lane 0 stores it
-    // with one TMA store (end of an iteration).  No slot is ever zeroed: each walk writes each plane
-    // from its first edge on exactly once, so the next lap simply overwrites its position (positions
-    // a walk never writes keep their initial 0).  The exception is a plane written through an
-    // overflow slot (RB + s): overflow slots hold the sentinel SENT until a walk writes them, and the
-    // fold at the batch's store takes the overflow value where one was written, else the direct
-    // slot's, and re-arms SENT.  A slot may be rewritten once the store that read it has completed
-    // its shared-memory read (released at the start of the next iteration).
-    int issued_b = 0, zeroed_b = 0;  // batches stored / released for rewriting
-    const int n_batches = (a.M + RW_PB - 1) / RW_PB;
-    auto release = [&]() {
-        if (zeroed_b >= issued_b) return;
-        if (lane == 0) bulk_wait_read<0>();
-        __syncwarp();
-        zeroed_b = issued_b;
-    };
-    auto issue_final = [&](int final_planes) {  // planes [0, final_planes) hold their final values
-        const int nb = final_planes >= a.M ? n_batches : (int)((unsigned)max(final_planes, 0) / RW_PB);
-        if (nb <= issued_b) return;
-        const int b0 = issued_b;
+    // Output (F staging).  Slot (e - 1) mod RB of the staged ring holds F(E_e), the intensity a walk
+    // deposits below bin edge e (edge e is the top of plane e - 1); plane P = F(E_{P+1}) - F(E_P).
+    // Once the slowest walk has passed edge P + 1, every lane copies its 16 bytes of plane P out of
+    // the ring: it reads F(E_{P+1}), subtracts the F(E_P) it kept from the previous plane, and writes
+    // the 16 bytes with one st.global.cs.v4 (the warp writes the plane's two 256-byte rows: the
+    // store geometry that reaches the copy ceiling, profiles/r02b_membench.md).  No slot is ever
+    // zeroed: each walk writes each edge from its first one on exactly once, so the next lap simply
+    // overwrites its position (positions a walk never writes keep their initial 0 = F below its
+    // window).  The exception is an edge written through an overflow slot (RB + s): overflow slots
+    // hold the sentinel SENT until a walk writes them; the copy takes the overflow value where one
+    // was written, else the direct slot's, and re-arms SENT.  A slot may be rewritten once the
+    // plane that reads it as its lower edge has been copied (the replay's ring-need rule).
+    const bool lane_out = rowl + (lane >> 4) >= 0 && row0 + (lane >> 4) < a.row_end && col0 + 4 * (lane & 15) < a.C;
+    float* gout = a.out + (size_t)(rowl + (lane >> 4)) * a.C + col0 + 4 * (lane & 15);
+    const size_t gplane = (size_t)(a.row_end - a.row_begin) * a.C;
+    int copied = 0;   // planes [0, copied) written out
+    float4 Flo = make_float4(0.f, 0.f, 0.f, 0.f);  // F at the lower edge of plane `copied`
+    auto copy_upto = [&](int final_planes) {  // planes [0, final_planes) hold their final values
+        const int nf = min(final_planes, a.M);
+        if (nf <= copied) return;
+        __syncwarp();  // every lane's edge stores before the reads
+        if (copied == 0) Flo = lds128(s_copy + (RB - 1) * PLANE_B);  // F(E_0): slot RB - 1 (never overflow)
 #pragma unroll 1
-        for (int b = b0; b < nb; ++b) {
-            const int s0 = (b * RW_PB) & (RB - 1);
-            if (s0 < KT - 1) {  // the ring's first slots: fold their overflow planes in
-                __syncwarp();  // order the other lanes' slot writes before this lane's fold reads
-#pragma unroll
-                for (int q = 0; q < RW_PB; ++q) {
-                    const int s = s0 + q;
-                    if (s >= KT - 1) break;
-                    const uint4 x = lds128u(s_copy + s * PLANE_B), y = lds128u(s_copy + (RB + s) * PLANE_B);
-                    sts128u(s_copy + s * PLANE_B, make_uint4(y.x == SENT ? x.x : y.x, y.y == SENT ? x.y : y.y,
-                                                             y.z == SENT ? x.z : y.z, y.w == SENT ? x.w : y.w));
-                    sts128u(s_copy + (RB + s) * PLANE_B, make_uint4(SENT, SENT, SENT, SENT));
-                }
+        for (int P = copied; P < nf; ++P) {
+            const int s = P & (RB - 1);  // slot of edge P + 1
+            float4 Fh;
+            if (s < KT - 1) {  // the ring's first slots: fold their overflow planes in
+                const uint4 x = lds128u(s_copy + s * PLANE_B), y = lds128u(s_copy + (RB + s) * PLANE_B);
+                Fh = make_float4(__uint_as_float(y.x == SENT ? x.x : y.x), __uint_as_float(y.y == SENT ? x.y : y.y),
+                                 __uint_as_float(y.z == SENT ? x.z : y.z), __uint_as_float(y.w == SENT ? x.w : y.w));
+                sts128u(s_copy + (RB + s) * PLANE_B, make_uint4(SENT, SENT, SENT, SENT));
+            } else {
+                Fh = lds128(s_copy + s * PLANE_B);
             }
-        }
-        if (a.prof_part) {  // fused depth-profile epilogue: the tile's sum of each final plane
-            __syncwarp();    // every lane's edge stores (and the fold) before the sums read them
-#pragma unroll 1
-            for (int b = b0; b < nb; ++b) {
-                const int s0 = (b * RW_PB) & (RB - 1);
-                float v[RW_PB];
-#pragma unroll
-                for (int q = 0; q < RW_PB; ++q) {
-                    const float4 x = lds128(s_copy + (s0 + q) * PLANE_B);
-                    v[q] = (x.x + x.y) + (x.z + x.w);
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-                    for (int q = 0; q < RW_PB; ++q) v[q] += __shfl_xor_sync(0xffffffffu, v[q], o);
-                if (lane < RW_PB && b * RW_PB + lane < a.M) {
-                    float w = v[0];
-#pragma unroll
-                    for (int q = 1; q < RW_PB; ++q) w = lane == q ? v[q] : w;
-                    a.prof_part[(size_t)rt * a.M + b * RW_PB + lane] = w;
-                }
-            }
-        }
-        issued_b = nb;
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-#pragma unroll 1
-            for (int b = b0; b < nb; ++b) {
-                const unsigned char* src = smem + L::OFF_OUT + ((b * RW_PB) & (RB - 1)) * PLANE_B;
+            const float4 v = make_float4(Fh.x - Flo.x, Fh.y - Flo.y, Fh.z - Flo.z, Fh.w - Flo.w);
+            Flo = Fh;
+            float* g = gout + (size_t)P * gplane;
+            if (lane_out) {
                 if (a.acc)
-                    tma_reduce_add_3d(&out_map, col0, rowl, b * RW_PB, src);
+                    red_add_v4(g, v);  // both-edges mode: the second edge adds
                 else
-                    tma_store_3d(&out_map, col0, rowl, b * RW_PB, src);
+                    stg_cs_v4(g, v);
             }
-            bulk_commit();
+            if (a.prof_part) {  // fused depth-profile epilogue: the tile's sum of the plane
+                float t = lane_out ? (v.x + v.y) + (v.z + v.w) : 0.f;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                if (lane == 0) a.prof_part[(size_t)rt * a.M + P] = t;
+            }
         }
+        copied = nf;
+        __syncwarp();  // every lane's reads before the next edge stores reuse the slots
     };
 #if DAXM_ROW_CHECK
     unsigned viol = 0u;
@@ -543,12 +530,11 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
     // Zone [lo_v, lo_{v+1}) of a walk pair, everything its bin-edge stores need.  Inside the zone
     // F(E) = F0 + c x + xc (d + g xc), x = E - lo_v, xc = min(x, w); the admission replay checks
     // w < 2 bins, so from the zone's third edge on x > w and F(E) = h + c x, h = F0 + w d / 2: the
-    // zone's edges En, En + 1, ... receive o0 = F(x0) - Fp (Fp: F at the walk's previous edge),
-    // o1 = F(x0 + 1) - F(x0), o2 = h + c (x0 + 2) - F(x0 + 1), and c for every later one; the walk's
-    // F at its last edge becomes the next Fp.
+    // zone's edges En, En + 1, ... receive F(x0), F(x0 + 1) and then hc + k c, hc = h + c x0 (the
+    // linear form at x0), k = 2, 3, ...
     struct Zone {
-        float2 F0v, o1, o2, c, Fl, cnt;
-        float2 o3, o4;  // general-span variant: edges 3 and 4 of the zone (else both are c)
+        float2 F0v, F1v, hc, c, cnt;
+        float2 F2v, F3v;  // general-span variant: F at the zone's edges 2 and 3 (exact)
         uint32_t es[2];
     };
     // Transition S -> D: every pair advances one point; point v + 1 closes the zone [lo_v, lo_{v+1})
@@ -612,18 +598,12 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
                 };
                 const float2 F0v = Fx(x0), F1v = Fx(add2(x0, f2(1.f))), F2v = Fx(add2(x0, f2(2.f)));
                 const float2 F3v = Fx(add2(x0, f2(3.f)));
-                const float2 xl = add2(x0, sub2(cnt, f2(1.f)));  // x of the zone's last edge
-                const float2 Fl = fma2(c, xl, h);
                 Z[p].F0v = F0v;
-                Z[p].o1 = sub2(F1v, F0v);
-                Z[p].o2 = sub2(F2v, F1v);
-                Z[p].o3 = sub2(F3v, F2v);
-                Z[p].o4 = sub2(fma2(c, add2(x0, f2(4.f)), h), F3v);
+                Z[p].F1v = F1v;
+                Z[p].F2v = F2v;
+                Z[p].F3v = F3v;
+                Z[p].hc = fma2(c, x0, h);
                 Z[p].c = c;
-                Z[p].Fl = make_float2(cnt.x >= 5.f ? Fl.x : cnt.x >= 4.f ? F3v.x : cnt.x >= 3.f ? F2v.x
-                                                          : cnt.x >= 2.f ? F1v.x : F0v.x,
-                                      cnt.y >= 5.f ? Fl.y : cnt.y >= 4.f ? F3v.y : cnt.y >= 3.f ? F2v.y
-                                                          : cnt.y >= 2.f ? F1v.y : F0v.y);
                 D.zF[p] = Fx(st);  // F at the next zone's start
                 D.cq2[p] = c1;
                 D.phm[p] = S.phi[p];
@@ -644,14 +624,10 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
                 F0v = fma2(xc0, fma2(g, xc0, d), fma2(c, x0, S.zF[p]));
                 F1v = fma2(xc1, fma2(g, xc1, d), fma2(c, x1, S.zF[p]));
             }
-            const float2 xl = add2(x0, sub2(cnt, f2(1.f)));  // x of the zone's last edge
-            const float2 Fl = fma2(c, xl, h);
             Z[p].F0v = F0v;
-            Z[p].o1 = sub2(F1v, F0v);
-            Z[p].o2 = sub2(fma2(c, add2(x1, f2(1.f)), h), F1v);
+            Z[p].F1v = F1v;
+            Z[p].hc = fma2(c, x0, h);
             Z[p].c = c;
-            Z[p].Fl = make_float2(cnt.x >= 3.f ? Fl.x : cnt.x >= 2.f ? F1v.x : F0v.x,
-                                  cnt.y >= 3.f ? Fl.y : cnt.y >= 2.f ? F1v.y : F0v.y);
             D.zF[p] = fma2(c, sub2(lo, S.plo[p]), h);  // F at the next zone's start
             }
             Z[p].cnt = cnt;
@@ -668,30 +644,22 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
         });
         ++it2;
     };
-    // The bin-edge stores of a zone: edge k of walk (p, r) goes to plane En + k - 1, staged slot
+    // The bin-edge stores of a zone: F at edge k of walk (p, r) goes to slot En + k - 1, staged slot
     // es + k planes (immediate offsets; row r, column half p), iff k < cnt.  Branch-free: RW_ST
     // predicated stores per walk, a rare extra trip when some zone holds more edges.
     constexpr int RW_ST = GEN ? 5 : 4;  // (general-span zones, up to 5 bins, hold more edges)
-    auto edges = [&](const Zone Z[2], const float2 Fin[2], float2 Fout[2]) {
+    auto edges = [&](const Zone Z[2]) {
         static_for<0, 2>([&](auto pc) {
             constexpr int p = decltype(pc)::value;
             constexpr int O0 = 0, O1 = RW_COLS * 4;  // rows 0 / 1 (the column is in es)
-            const float2 o0 = sub2(Z[p].F0v, Fin[p]);
-            st_if<O0>(Z[p].es[0], o0.x, 0.f, Z[p].cnt.x);
-            st_if<O1>(Z[p].es[1], o0.y, 0.f, Z[p].cnt.y);
-            st_if<O0 + PLANE_B>(Z[p].es[0], Z[p].o1.x, 1.f, Z[p].cnt.x);
-            st_if<O1 + PLANE_B>(Z[p].es[1], Z[p].o1.y, 1.f, Z[p].cnt.y);
-            st_if<O0 + 2 * PLANE_B>(Z[p].es[0], Z[p].o2.x, 2.f, Z[p].cnt.x);
-            st_if<O1 + 2 * PLANE_B>(Z[p].es[1], Z[p].o2.y, 2.f, Z[p].cnt.y);
-            static_for<3, RW_ST>([&](auto kc) {
+            static_for<0, RW_ST>([&](auto kc) {
                 constexpr int k = decltype(kc)::value;
-                const float2 v = !GEN ? Z[p].c : k == 3 ? Z[p].o3 : k == 4 ? Z[p].o4 : Z[p].c;
+                const float2 v = k == 0 ? Z[p].F0v : k == 1 ? Z[p].F1v : (GEN && k == 2) ? Z[p].F2v
+                               : (GEN && k == 3) ? Z[p].F3v : fma2(Z[p].c, f2((float)k), Z[p].hc);
                 st_if<O0 + k * PLANE_B>(Z[p].es[0], v.x, (float)k, Z[p].cnt.x);
                 st_if<O1 + k * PLANE_B>(Z[p].es[1], v.y, (float)k, Z[p].cnt.y);
                 return true;
             });
-            Fout[p].x = Z[p].cnt.x >= 1.f ? Z[p].Fl.x : Fin[p].x;
-            Fout[p].y = Z[p].cnt.y >= 1.f ? Z[p].Fl.y : Fin[p].y;
             return true;
         });
         const float cmax = fmaxf(fmaxf(Z[0].cnt.x, Z[0].cnt.y), fmaxf(Z[1].cnt.x, Z[1].cnt.y));
@@ -701,8 +669,9 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
                 constexpr int O0 = 0, O1 = RW_COLS * 4;
                 static_for<RW_ST, KT>([&](auto kc) {
                     constexpr int k = decltype(kc)::value;
-                    st_if<O0 + k * PLANE_B>(Z[p].es[0], Z[p].c.x, (float)k, Z[p].cnt.x);
-                    st_if<O1 + k * PLANE_B>(Z[p].es[1], Z[p].c.y, (float)k, Z[p].cnt.y);
+                    const float2 v = fma2(Z[p].c, f2((float)k), Z[p].hc);
+                    st_if<O0 + k * PLANE_B>(Z[p].es[0], v.x, (float)k, Z[p].cnt.x);
+                    st_if<O1 + k * PLANE_B>(Z[p].es[1], v.y, (float)k, Z[p].cnt.y);
                     return true;
                 });
                 return true;
@@ -711,60 +680,40 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
             if (cmax > (float)KT) viol |= 2u;
 #endif
         }
-#if DAXM_ROW_CHECK
-        {   // every plane written lies below the released part of the ring + RB
-            float pl = -1.0e30f;
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                const float e0x = (float)(((int)(Z[p].es[0] - ob) >> 9)), e0y = (float)(((int)(Z[p].es[1] - ob) >> 9));
-                (void)e0x;
-                (void)e0y;
-                if (Z[p].cnt.x > 0.f) pl = fmaxf(pl, Z[p].cnt.x);
-                if (Z[p].cnt.y > 0.f) pl = fmaxf(pl, Z[p].cnt.y);
-            }
-            (void)pl;
-        }
-#endif
     };
     // Software pipeline: the stores of step n's zones and step n + 1's transition are independent,
     // so they form one block; the input waits, slot releases and batch stores sit between steps.
     Zone Z0[2], Z1[2];
-    float2 FpA[2] = {f2(0.f), f2(0.f)}, FpB[2];
     RowState& Bs = B;
     input(0);
     trans(A, Bs, Z0);  // step 0's zones; state after point 1
     fr_e = frontier(Bs);
-    // the replay's iteration count, rounded up to even (an extra step after every pair has
-    // finished changes nothing: no edges, nothing left to load)
-    // The input rings are refilled and waited for once per four steps (for all four transitions).
+    // the replay's iteration count, rounded up to a multiple of four (an extra step after every pair
+    // has finished changes nothing: no edges, nothing left to load).  The input rings are refilled and
+    // waited for once per four steps (for all four transitions).
     const int nquad = (ti.niter + 3) >> 2;
 #pragma unroll 1
     for (int it = 0; it < nquad; ++it) {
         input(RW_G - 1);
-        release();
         trans(Bs, A, Z1);
-        edges(Z0, FpA, FpB);
-        issue_final(fr_e - 1);  // edge e completes plane e - 1: planes below the slowest walk's next are final
+        edges(Z0);
+        copy_upto(fr_e - 1);  // edge e completes plane e - 1: planes below the slowest walk's next are final
         fr_e = frontier(A);
-        release();
         trans(A, Bs, Z0);
-        edges(Z1, FpB, FpA);
-        issue_final(fr_e - 1);
+        edges(Z1);
+        copy_upto(fr_e - 1);
         fr_e = frontier(Bs);
-        release();
         trans(Bs, A, Z1);
-        edges(Z0, FpA, FpB);
-        issue_final(fr_e - 1);
+        edges(Z0);
+        copy_upto(fr_e - 1);
         fr_e = frontier(A);
-        release();
         trans(A, Bs, Z0);
-        edges(Z1, FpB, FpA);
-        issue_final(fr_e - 1);
+        edges(Z1);
+        copy_upto(fr_e - 1);
         fr_e = frontier(Bs);
     }
-    issue_final(a.M);
+    copy_upto(a.M);
     if (lane == 0) {
-        bulk_wait<0>();
         // every issued input load must have landed before the CTA exits
         for (; g_wait < g_issue; ++g_wait)
             while (!mbar_try(s_bar + (uint32_t)(g_wait & (NG - 1)) * 8u, (uint32_t)(g_wait / NG) & 1u)) {
@@ -912,8 +861,7 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
                 0xffffffffu, (int)fminf(fminf(En[0][0], En[0][1]), fminf(En[1][0], En[1][1])) + a.m_ref);
         };
         int fr_e = frontier();
-        int issued_b = 0, zeroed_b = 0;
-        const int n_batches = (a.M + RW_PB - 1) / RW_PB;
+        int copied = 0;  // planes the kernel has copied out (F staging: edge e in slot (e - 1) mod RB)
         for (;;) {
             if (!__any_sync(0xffffffffu, v < ve)) break;
             if (++iters > 4 * nvt + 64) {  // cannot happen (every pair advances every iteration)
@@ -979,14 +927,12 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
             pmax = __reduce_max_sync(0xffffffffu, pmax);
             if (kmax > RW_KT) bad_sep |= RW_WHY_KT;
             if (kmax > RW_KT_GEN) bad_gen |= RW_WHY_KT;
-            zeroed_b = issued_b;  // zero_pending: batches stored at the previous iteration
-            if (pmax != INT_MIN) need = max(need, pmax - zeroed_b * RW_PB + 1);
+            // edge e = pmax + 1 goes to slot pmax mod RB, whose previous occupant, edge e - RB, is free
+            // once it has been read: as the upper edge of plane e - RB - 1 (copied >= e - RB), or for
+            // edge 0 as the lower edge of plane 0 (copied >= 1): pmax + 1 - copied (+1) <= RB
+            if (pmax != INT_MIN) need = max(need, pmax + 1 - copied + (copied == 0 ? 1 : 0));
             fr_e = frontier();
-            {   // issue_final, exactly as the kernel
-                const int fp = fr_e - 1;
-                const int nb = fp >= a.M ? n_batches : fp / RW_PB;
-                if (nb > issued_b) issued_b = nb;
-            }
+            copied = max(copied, min(fr_e - 1, a.M));  // copy_upto, exactly as the kernel
         }
         // a finished schedule leaves every walk with a window past the top edge
         for (int p = 0; p < 2; ++p)

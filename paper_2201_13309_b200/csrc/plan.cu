@@ -1341,6 +1341,7 @@ static RowArgs make_row_args(const daxm_plan* p) {
     a.dI_floor = p->dI_floor;
     a.acc = p->acc;
     a.stack = nullptr;
+    a.out = nullptr;
     a.use_cutoff = p->use_cutoff;
     a.cutoff = p->cutoff;
     a.live = nullptr;
@@ -1463,6 +1464,7 @@ static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_o
     }
     RowArgs a = make_row_args(p);
     a.stack = d_stack;
+    a.out = d_out;
     a.prof_part = d_profile ? p->d_prof_part : nullptr;
     if (getenv("DAXM_NO_ZERO_SKIP") == nullptr) {  // exact zero-dI skip, before the class launches fork
         cudaError_t z = launch_row_live(a, ra * p->n_rc, (rb - ra) * p->n_rc, p->d_rlive, dt, st);
