@@ -110,6 +110,11 @@ __device__ __forceinline__ void stg_cs_v4(float* g, float4 v) {  // streaming st
     asm volatile("st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(g), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                  : "memory");
 }
+__device__ __forceinline__ void stg_cs_v4_if(float* g, float2 a, float2 b, bool pred) {  // iff pred
+    asm volatile("{\n .reg .pred q;\n setp.ne.u32 q, %5, 0;\n @q st.global.cs.v4.f32 [%0], {%1, %2, %3, %4};\n}\n" ::"l"(g),
+                 "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "r"((unsigned)pred)
+                 : "memory");
+}
 __device__ __forceinline__ void red_add_v4(float* g, float4 v) {  // one add per element (sm_90+)
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(g), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                  : "memory");
@@ -455,42 +460,77 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
     // was written, else the direct slot's, and re-arms SENT.  A slot may be rewritten once the
     // plane that reads it as its lower edge has been copied (the replay's ring-need rule).
     const bool lane_out = rowl + (lane >> 4) >= 0 && row0 + (lane >> 4) < a.row_end && col0 + 4 * (lane & 15) < a.C;
-    float* gout = a.out + (size_t)(rowl + (lane >> 4)) * a.C + col0 + 4 * (lane & 15);
     const size_t gplane = (size_t)(a.row_end - a.row_begin) * a.C;
-    int copied = 0;   // planes [0, copied) written out
-    float4 Flo = make_float4(0.f, 0.f, 0.f, 0.f);  // F at the lower edge of plane `copied`
+    // the lane's 16 bytes of plane `copied` (advanced by one plane per copy)
+    float* gnext = a.out + (ptrdiff_t)(rowl + (lane >> 4)) * a.C + col0 + 4 * (lane & 15);
+    const bool plain = !a.acc && !a.prof_part;  // store only (the both-edges add and the fused profile: else)
+    int copied = 0;  // planes [0, copied) written out
+    float2 Flo[2] = {f2(0.f), f2(0.f)};  // F at the lower edge of plane `copied` (the lane's 4 values)
     auto copy_upto = [&](int final_planes) {  // planes [0, final_planes) hold their final values
         const int nf = min(final_planes, a.M);
         if (nf <= copied) return;
         __syncwarp();  // every lane's edge stores before the reads
-        if (copied == 0) Flo = lds128(s_copy + (RB - 1) * PLANE_B);  // F(E_0): slot RB - 1 (never overflow)
+        if (copied == 0) {  // F(E_0): slot RB - 1 (never an overflow slot)
+            const float4 f = lds128(s_copy + (RB - 1) * PLANE_B);
+            Flo[0] = make_float2(f.x, f.y);
+            Flo[1] = make_float2(f.z, f.w);
+        }
+        // F(E_{P+1}) of plane P, with the overflow fold (its slot's overflow plane, re-armed)
+        auto f_hi = [&](int P, float2 h[2]) {
+            const uint32_t s = (uint32_t)P & (RB - 1);  // slot of edge P + 1
+            const uint32_t ad = s_copy + s * PLANE_B;
+            uint4 x = lds128u(ad);
+            if (s < (uint32_t)(KT - 1)) {  // the ring's first slots: fold their overflow planes in
+                const uint4 y = lds128u(ad + RB * PLANE_B);
+                x = make_uint4(y.x == SENT ? x.x : y.x, y.y == SENT ? x.y : y.y, y.z == SENT ? x.z : y.z,
+                               y.w == SENT ? x.w : y.w);
+                sts128u(ad + RB * PLANE_B, make_uint4(SENT, SENT, SENT, SENT));
+            }
+            h[0] = make_float2(__uint_as_float(x.x), __uint_as_float(x.y));
+            h[1] = make_float2(__uint_as_float(x.z), __uint_as_float(x.w));
+        };
+        int P = copied;
+        if (plain) {
+            // two planes per trip (F of one plane's upper edge is the next one's lower edge: no copies)
+            float2 Fh[2];
 #pragma unroll 1
-        for (int P = copied; P < nf; ++P) {
-            const int s = P & (RB - 1);  // slot of edge P + 1
-            float4 Fh;
-            if (s < KT - 1) {  // the ring's first slots: fold their overflow planes in
-                const uint4 x = lds128u(s_copy + s * PLANE_B), y = lds128u(s_copy + (RB + s) * PLANE_B);
-                Fh = make_float4(__uint_as_float(y.x == SENT ? x.x : y.x), __uint_as_float(y.y == SENT ? x.y : y.y),
-                                 __uint_as_float(y.z == SENT ? x.z : y.z), __uint_as_float(y.w == SENT ? x.w : y.w));
-                sts128u(s_copy + (RB + s) * PLANE_B, make_uint4(SENT, SENT, SENT, SENT));
-            } else {
-                Fh = lds128(s_copy + s * PLANE_B);
+            for (;;) {
+                f_hi(P, Fh);
+                stg_cs_v4_if(gnext, sub2(Fh[0], Flo[0]), sub2(Fh[1], Flo[1]), lane_out);
+                gnext += gplane;
+                if (++P == nf) {
+                    Flo[0] = Fh[0];
+                    Flo[1] = Fh[1];
+                    break;
+                }
+                f_hi(P, Flo);
+                stg_cs_v4_if(gnext, sub2(Flo[0], Fh[0]), sub2(Flo[1], Fh[1]), lane_out);
+                gnext += gplane;
+                if (++P == nf) break;
             }
-            const float4 v = make_float4(Fh.x - Flo.x, Fh.y - Flo.y, Fh.z - Flo.z, Fh.w - Flo.w);
-            Flo = Fh;
-            float* g = gout + (size_t)P * gplane;
-            if (lane_out) {
-                if (a.acc)
-                    red_add_v4(g, v);  // both-edges mode: the second edge adds
-                else
-                    stg_cs_v4(g, v);
-            }
-            if (a.prof_part) {  // fused depth-profile epilogue: the tile's sum of the plane
-                float t = lane_out ? (v.x + v.y) + (v.z + v.w) : 0.f;
+        } else {
+#pragma unroll 1
+            do {
+                float2 h[2];
+                f_hi(P, h);
+                const float2 v0 = sub2(h[0], Flo[0]), v1 = sub2(h[1], Flo[1]);
+                Flo[0] = h[0];
+                Flo[1] = h[1];
+                const float4 v = make_float4(v0.x, v0.y, v1.x, v1.y);
+                if (lane_out) {
+                    if (a.acc)
+                        red_add_v4(gnext, v);  // both-edges mode: the second edge adds
+                    else
+                        stg_cs_v4(gnext, v);
+                }
+                if (a.prof_part) {  // fused depth-profile epilogue: the tile's sum of the plane
+                    float t = lane_out ? (v.x + v.y) + (v.z + v.w) : 0.f;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-                if (lane == 0) a.prof_part[(size_t)rt * a.M + P] = t;
-            }
+                    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                    if (lane == 0) a.prof_part[(size_t)rt * a.M + P] = t;
+                }
+                gnext += gplane;
+            } while (++P < nf);
         }
         copied = nf;
         __syncwarp();  // every lane's reads before the next edge stores reuse the slots
