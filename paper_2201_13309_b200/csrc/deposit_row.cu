@@ -149,6 +149,18 @@ __device__ __forceinline__ float lds_in(uint32_t addr) {
     }
 }
 
+// Overflow fold of a staged slot at `ad` holding x: the value a walk wrote through the overflow slot
+// (ad + RB planes) where one was written (not SENT), else x; written back to the direct slot (a later
+// plane reads it as its lower edge) and the overflow slot re-armed.
+template <int RB>
+__device__ __forceinline__ uint4 fold_slot(uint32_t ad, uint4 x) {
+    const uint4 y = lds128u(ad + RB * PLANE_B);
+    x = make_uint4(y.x == SENT ? x.x : y.x, y.y == SENT ? x.y : y.y, y.z == SENT ? x.z : y.z, y.w == SENT ? x.w : y.w);
+    sts128u(ad, x);
+    sts128u(ad + RB * PLANE_B, make_uint4(SENT, SENT, SENT, SENT));
+    return x;
+}
+
 // compile-time loop: f(integral_constant<int, k>) for k = K0 .. KN - 1 while f returns true
 template <int K0, int KN, typename F>
 __device__ __forceinline__ void static_for(F&& f) {
@@ -362,7 +374,8 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
         lim = min(lim, ngroups - 1);
         if (lim < g_issue) return;
         if (lane == 0)
-            for (int g = g_issue; g <= lim; ++g) {
+#pragma unroll 1
+            for (int g = g_issue; g <= lim; ++g) {  // (in the loop: one group per four steps)
                 const int b = g & (NG - 1);
                 const int dk = dir > 0 ? g * RW_G : -g * RW_G;
                 mbar_arrive_expect_tx(&bars[b], 2 * L::IN_GROUP);
@@ -375,6 +388,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
     auto wait_for = [&](int v) {  // every group up to visit v's has landed (v warp-uniform, >= 0)
         const int gn = (int)((unsigned)v / RW_G);
         if (gn < g_wait) return;
+#pragma unroll 1
         for (; g_wait <= gn; ++g_wait)
             while (!mbar_try(s_bar + (uint32_t)(g_wait & (NG - 1)) * 8u, (uint32_t)(g_wait / NG) & 1u)) {
             }
@@ -450,78 +464,59 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
     // Output (F staging).  Slot (e - 1) mod RB of the staged ring holds F(E_e), the intensity a walk
     // deposits below bin edge e (edge e is the top of plane e - 1); plane P = F(E_{P+1}) - F(E_P).
     // Once the slowest walk has passed edge P + 1, every lane copies its 16 bytes of plane P out of
-    // the ring: it reads F(E_{P+1}), subtracts the F(E_P) it kept from the previous plane, and writes
-    // the 16 bytes with one st.global.cs.v4 (the warp writes the plane's two 256-byte rows: the
+    // the ring: it reads F(E_{P+1}) and F(E_P) (both still staged) and writes their difference with
+    // one st.global.cs.v4 (the warp writes the plane's two 256-byte rows: the
     // store geometry that reaches the copy ceiling, profiles/r02b_membench.md).  No slot is ever
     // zeroed: each walk writes each edge from its first one on exactly once, so the next lap simply
     // overwrites its position (positions a walk never writes keep their initial 0 = F below its
     // window).  The exception is an edge written through an overflow slot (RB + s): overflow slots
     // hold the sentinel SENT until a walk writes them; the copy takes the overflow value where one
-    // was written, else the direct slot's, and re-arms SENT.  A slot may be rewritten once the
-    // plane that reads it as its lower edge has been copied (the replay's ring-need rule).
+    // was written, else the direct slot's, writes it back to the direct slot and re-arms SENT.  A
+    // slot may be rewritten once the plane that reads it as its lower edge has been copied (the
+    // replay's ring-need rule).
     const bool lane_out = rowl + (lane >> 4) >= 0 && row0 + (lane >> 4) < a.row_end && col0 + 4 * (lane & 15) < a.C;
     const size_t gplane = (size_t)(a.row_end - a.row_begin) * a.C;
     // the lane's 16 bytes of plane `copied` (advanced by one plane per copy)
     float* gnext = a.out + (ptrdiff_t)(rowl + (lane >> 4)) * a.C + col0 + 4 * (lane & 15);
     const bool plain = !a.acc && !a.prof_part;  // store only (the both-edges add and the fused profile: else)
     int copied = 0;  // planes [0, copied) written out
-    float2 Flo[2] = {f2(0.f), f2(0.f)};  // F at the lower edge of plane `copied` (the lane's 4 values)
     auto copy_upto = [&](int final_planes) {  // planes [0, final_planes) hold their final values
         const int nf = min(final_planes, a.M);
         if (nf <= copied) return;
         __syncwarp();  // every lane's edge stores before the reads
-        if (copied == 0) {  // F(E_0): slot RB - 1 (never an overflow slot)
-            const float4 f = lds128(s_copy + (RB - 1) * PLANE_B);
-            Flo[0] = make_float2(f.x, f.y);
-            Flo[1] = make_float2(f.z, f.w);
-        }
-        // F(E_{P+1}) of plane P, with the overflow fold (its slot's overflow plane, re-armed)
-        auto f_hi = [&](int P, float2 h[2]) {
-            const uint32_t s = (uint32_t)P & (RB - 1);  // slot of edge P + 1
-            const uint32_t ad = s_copy + s * PLANE_B;
-            uint4 x = lds128u(ad);
-            if (s < (uint32_t)(KT - 1)) {  // the ring's first slots: fold their overflow planes in
-                const uint4 y = lds128u(ad + RB * PLANE_B);
-                x = make_uint4(y.x == SENT ? x.x : y.x, y.y == SENT ? x.y : y.y, y.z == SENT ? x.z : y.z,
-                               y.w == SENT ? x.w : y.w);
-                sts128u(ad + RB * PLANE_B, make_uint4(SENT, SENT, SENT, SENT));
-            }
-            h[0] = make_float2(__uint_as_float(x.x), __uint_as_float(x.y));
-            h[1] = make_float2(__uint_as_float(x.z), __uint_as_float(x.w));
-        };
         int P = copied;
+        float* g = gnext;
         if (plain) {
-            // two planes per trip (F of one plane's upper edge is the next one's lower edge: no copies)
-            float2 Fh[2];
 #pragma unroll 1
-            for (;;) {
-                f_hi(P, Fh);
-                stg_cs_v4_if(gnext, sub2(Fh[0], Flo[0]), sub2(Fh[1], Flo[1]), lane_out);
-                gnext += gplane;
-                if (++P == nf) {
-                    Flo[0] = Fh[0];
-                    Flo[1] = Fh[1];
-                    break;
-                }
-                f_hi(P, Flo);
-                stg_cs_v4_if(gnext, sub2(Flo[0], Fh[0]), sub2(Flo[1], Fh[1]), lane_out);
-                gnext += gplane;
-                if (++P == nf) break;
-            }
+            do {
+                // plane P = F(E_{P+1}) (slot P mod RB) - F(E_P) (slot (P - 1) mod RB; E_0: slot RB - 1)
+                const uint32_t ad = s_copy + ((uint32_t)P & (RB - 1)) * PLANE_B;
+                uint4 x = lds128u(ad);
+                if (((uint32_t)P & (RB - 1)) < (uint32_t)(KT - 1)) x = fold_slot<RB>(ad, x);
+                const uint4 y = lds128u(s_copy + ((uint32_t)(P - 1) & (RB - 1)) * PLANE_B);
+                stg_cs_v4_if(g, sub2(make_float2(__uint_as_float(x.x), __uint_as_float(x.y)),
+                                     make_float2(__uint_as_float(y.x), __uint_as_float(y.y))),
+                             sub2(make_float2(__uint_as_float(x.z), __uint_as_float(x.w)),
+                                  make_float2(__uint_as_float(y.z), __uint_as_float(y.w))),
+                             lane_out);
+                g += gplane;
+            } while (++P < nf);
         } else {
 #pragma unroll 1
             do {
-                float2 h[2];
-                f_hi(P, h);
-                const float2 v0 = sub2(h[0], Flo[0]), v1 = sub2(h[1], Flo[1]);
-                Flo[0] = h[0];
-                Flo[1] = h[1];
-                const float4 v = make_float4(v0.x, v0.y, v1.x, v1.y);
+                const uint32_t ad = s_copy + ((uint32_t)P & (RB - 1)) * PLANE_B;
+                uint4 x = lds128u(ad);
+                if (((uint32_t)P & (RB - 1)) < (uint32_t)(KT - 1)) x = fold_slot<RB>(ad, x);
+                const uint4 y = lds128u(s_copy + ((uint32_t)(P - 1) & (RB - 1)) * PLANE_B);
+                const float4 v = make_float4(__uint_as_float(x.x) - __uint_as_float(y.x),
+                                             __uint_as_float(x.y) - __uint_as_float(y.y),
+                                             __uint_as_float(x.z) - __uint_as_float(y.z),
+                                             __uint_as_float(x.w) - __uint_as_float(y.w));
                 if (lane_out) {
                     if (a.acc)
-                        red_add_v4(gnext, v);  // both-edges mode: the second edge adds
+                        red_add_v4(g, v);  // both-edges mode: the second edge adds
                     else
-                        stg_cs_v4(gnext, v);
+                        stg_cs_v4(g, v);
                 }
                 if (a.prof_part) {  // fused depth-profile epilogue: the tile's sum of the plane
                     float t = lane_out ? (v.x + v.y) + (v.z + v.w) : 0.f;
@@ -529,9 +524,10 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
                     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
                     if (lane == 0) a.prof_part[(size_t)rt * a.M + P] = t;
                 }
-                gnext += gplane;
+                g += gplane;
             } while (++P < nf);
         }
+        gnext = g;
         copied = nf;
         __syncwarp();  // every lane's reads before the next edge stores reuse the slots
     };
@@ -968,9 +964,8 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
             if (kmax > RW_KT) bad_sep |= RW_WHY_KT;
             if (kmax > RW_KT_GEN) bad_gen |= RW_WHY_KT;
             // edge e = pmax + 1 goes to slot pmax mod RB, whose previous occupant, edge e - RB, is free
-            // once it has been read: as the upper edge of plane e - RB - 1 (copied >= e - RB), or for
-            // edge 0 as the lower edge of plane 0 (copied >= 1): pmax + 1 - copied (+1) <= RB
-            if (pmax != INT_MIN) need = max(need, pmax + 1 - copied + (copied == 0 ? 1 : 0));
+            // once plane e - RB (which reads it as its lower edge) has been copied: pmax + 2 - copied <= RB
+            if (pmax != INT_MIN) need = max(need, pmax + 2 - copied);
             fr_e = frontier();
             copied = max(copied, min(fr_e - 1, a.M));  // copy_upto, exactly as the kernel
         }
