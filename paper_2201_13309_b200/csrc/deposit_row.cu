@@ -45,9 +45,6 @@
 #include "fp2.cuh"
 #include "ptx.cuh"
 
-#ifndef DAXM_RW_TAU_GLOBAL
-#define DAXM_RW_TAU_GLOBAL 0  // 1: wire travel tau read from the plan's fp64 t (L1) instead of a shared table
-#endif
 #define DAXM_PRAGMA_(x) _Pragma(#x)
 #define DAXM_PRAGMA_UNROLL(n) DAXM_PRAGMA_(unroll n)
 #ifndef DAXM_ROW_CHECK
@@ -70,7 +67,7 @@ struct RowSmem {
     static constexpr int OFF_IN = OFF_OUT + OUT_SLOTS * PLANE_B;
     static constexpr int OFF_BAR = OFF_IN + RW_H * IN_HALF;
     static constexpr int OFF_TAU = OFF_BAR + NG * 8;
-    static size_t bytes(int max_nv) { return (size_t)OFF_TAU + (DAXM_RW_TAU_GLOBAL ? 0 : 4 * (size_t)(max_nv + 4)) + 128; }
+    static size_t bytes(int max_nv) { return (size_t)OFF_TAU + 4 * (size_t)(max_nv + 4) + 128; }
 };
 
 __device__ __forceinline__ void sts_zero4(uint32_t addr) {
@@ -276,7 +273,7 @@ __device__ __forceinline__ void row_starts(const RowWalk wk[2][2], int lane, int
 #ifndef DAXM_RW_MINB
 #define DAXM_RW_MINB 11  // resident CTAs (= warps) per SM the separated variant's registers allow
 #endif
-template <typename T, bool POINT, int RB, bool GEN, int NB>
+template <typename T, bool POINT, int RB, bool GEN, int NB, bool CLAMP>
 __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const __grid_constant__ CUtensorMap in_map,
                                                             const __grid_constant__ CUtensorMap out_map,
                                                             const RowArgs a) {
@@ -300,8 +297,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
     float* tau = reinterpret_cast<float*>(smem + L::OFF_TAU);
 
-    if (!DAXM_RW_TAU_GLOBAL)
-        for (int q = lane; q < nvt; q += 32) tau[q] = (float)(a.t[dir > 0 ? ti.k_lo + q : ti.k_hi - q] - ti.t_ref);
+    for (int q = lane; q < nvt; q += 32) tau[q] = (float)(a.t[dir > 0 ? ti.k_lo + q : ti.k_hi - q] - ti.t_ref);
     if (lane == 0) {
         for (int g = 0; g < NG; ++g) mbar_init(&bars[g], 1);
         fence_mbar_init();
@@ -403,12 +399,10 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
     const uint32_t in_lane =
         opaque(sbase + L::OFF_IN + (uint32_t)(hh * L::IN_HALF) + (uint32_t)(2 * (lane & 15)) * (uint32_t)sizeof(T));
     const uint32_t tau_l = opaque(sbase + L::OFF_TAU + 4u * (uint32_t)vmin_h);
-    // (DAXM_RW_TAU_GLOBAL) visit v of the lane's half is step tg[dir v]; tau = (float)(t - t_ref) as the table
-    const double* tg = a.t + (dir > 0 ? ti.k_lo + vmin_h : ti.k_hi - vmin_h);
-    const double t_ref = ti.t_ref;
     const uint32_t ob = sbase + L::OFF_OUT + (uint32_t)(32 * hh + 2 * (lane & 15)) * 4u;  // column 2i of a plane
     const uint32_t ob0 = opaque(ob + 4u * (uint32_t)hh), ob1 = opaque(ob + 4u * (uint32_t)(hh ^ 1));  // pair 0 / 1
-    const uint32_t swap = hh ? 0x1032u : 0x3210u;  // pair p's column is the (p ^ h)-th of the lane's two
+    // pair p's column is the (p ^ h)-th half-word of the lane's 32-bit input word
+    const uint32_t sel0 = opaque(hh ? 0x5432u : 0x5410u), sel1 = opaque(hh ? 0x5410u : 0x5432u);
     const float2 sdir2 = f2(opaque(2.f * a.sign * (float)dir));
     const float2 dfl2 = f2(opaque(a.dI_floor));  // c = 2 s dir dI / (sum_{q+1} - sum_q)
     const float EM = opaque((float)(a.M - a.m_ref));
@@ -421,15 +415,16 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
 
     // wire travel and the two pairs' intensities (rows 0, 1) at visit v of the lane's half
     auto fetch = [&](int v, float& t, float2 I[2]) {
-        if (DAXM_RW_TAU_GLOBAL)
-            t = (float)(__ldg(tg + (dir > 0 ? v : -v)) - t_ref);
-        else
-            t = lds_f32(tau_l + 4u * (uint32_t)v);
+        t = lds_f32(tau_l + 4u * (uint32_t)v);
         const uint32_t ad = in_lane + (uint32_t)((v ^ xr_) & (NB - 1)) * (uint32_t)L::IN_SLOT;
         if constexpr (sizeof(T) == 2) {
-            const uint32_t w0 = __byte_perm(lds_u32(ad), 0u, swap), w1 = __byte_perm(lds_u32(ad + 64u), 0u, swap);
-            I[0] = make_float2((float)(w0 & 0xffffu), (float)(w1 & 0xffffu));
-            I[1] = make_float2((float)(w0 >> 16), (float)(w1 >> 16));
+            // u16 -> fp32 exactly: 0x4B00'xxxx is 2^23 + x, one PRMT builds it from the lane's
+            // half-word (the pair's column), one packed FADD removes 2^23
+            const uint32_t w0 = lds_u32(ad), w1 = lds_u32(ad + 64u);
+            I[0] = add2(make_float2(__uint_as_float(__byte_perm(w0, 0x4B00u, sel0)),
+                                    __uint_as_float(__byte_perm(w1, 0x4B00u, sel0))), f2(-8388608.f));
+            I[1] = add2(make_float2(__uint_as_float(__byte_perm(w0, 0x4B00u, sel1)),
+                                    __uint_as_float(__byte_perm(w1, 0x4B00u, sel1))), f2(-8388608.f));
         } else {
             const float2 a0 = lds_f2(ad), a1 = lds_f2(ad + 128u);
             I[0] = hh ? make_float2(a0.y, a1.y) : make_float2(a0.x, a1.x);
@@ -487,20 +482,31 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
         int P = copied;
         float* g = gnext;
         if (plain) {
-#pragma unroll 1
-            do {
-                // plane P = F(E_{P+1}) (slot P mod RB) - F(E_P) (slot (P - 1) mod RB; E_0: slot RB - 1)
-                const uint32_t ad = s_copy + ((uint32_t)P & (RB - 1)) * PLANE_B;
-                uint4 x = lds128u(ad);
-                if (((uint32_t)P & (RB - 1)) < (uint32_t)(KT - 1)) x = fold_slot<RB>(ad, x);
-                const uint4 y = lds128u(s_copy + ((uint32_t)(P - 1) & (RB - 1)) * PLANE_B);
-                stg_cs_v4_if(g, sub2(make_float2(__uint_as_float(x.x), __uint_as_float(x.y)),
-                                     make_float2(__uint_as_float(y.x), __uint_as_float(y.y))),
-                             sub2(make_float2(__uint_as_float(x.z), __uint_as_float(x.w)),
-                                  make_float2(__uint_as_float(y.z), __uint_as_float(y.w))),
+            // plane P = F(E_{P+1}) (slot P mod RB) - F(E_P) (slot (P - 1) mod RB; E_0: slot RB - 1); the
+            // upper edge of one plane is the lower edge of the next (two planes per trip, no copies)
+            auto edge = [&](int Q) {  // F(E_{Q+1}) with the overflow fold
+                const uint32_t ad = s_copy + ((uint32_t)Q & (RB - 1)) * PLANE_B;
+                const uint4 x = lds128u(ad);
+                return ((uint32_t)Q & (RB - 1)) < (uint32_t)(KT - 1) ? fold_slot<RB>(ad, x) : x;
+            };
+            auto put = [&](uint4 hi, uint4 lo) {
+                stg_cs_v4_if(g, sub2(make_float2(__uint_as_float(hi.x), __uint_as_float(hi.y)),
+                                     make_float2(__uint_as_float(lo.x), __uint_as_float(lo.y))),
+                             sub2(make_float2(__uint_as_float(hi.z), __uint_as_float(hi.w)),
+                                  make_float2(__uint_as_float(lo.z), __uint_as_float(lo.w))),
                              lane_out);
                 g += gplane;
-            } while (++P < nf);
+            };
+            uint4 lo = lds128u(s_copy + ((uint32_t)(P - 1) & (RB - 1)) * PLANE_B);
+#pragma unroll 1
+            for (;;) {
+                const uint4 hi = edge(P);
+                put(hi, lo);
+                if (++P == nf) break;
+                lo = edge(P);
+                put(lo, hi);
+                if (++P == nf) break;
+            }
         } else {
 #pragma unroll 1
             do {
@@ -587,7 +593,8 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
             // (hi - lo_v) + |hi_v - lo| in general (the sorted corners' two parallel sides)
             const float2 dn = GEN ? add2(sub2(hi, S.plo[p]), abs2(sub2(S.phi[p], lo))) : sub2(s, S.ps[p]);
             // (both-edges mode: the clamp keeps this edge's sign of change, reading R16; -inf otherwise)
-            const float2 c = mul2(max2(mul2(sdir2, sub2(S.pI[p], S.Iq[p])), dfl2), rcp2(dn));
+            const float2 sdI = mul2(sdir2, sub2(S.pI[p], S.Iq[p]));
+            const float2 c = mul2(CLAMP ? max2(sdI, dfl2) : sdI, rcp2(dn));
             // edges of the zone [plo, lo): En .. floor(min(lo, EM))
             const float2 fl = add2(floor2(min2(lo, f2(EM))), f2(1.f));
             const float2 cnt = sub2(fl, add2(S.En[p], gate[p]));
@@ -1006,18 +1013,19 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
     }
 }
 
-// kernel variants: 0 separated, 1 general-span, 2 general-span with the wide input ring
-template <typename T, bool POINT, int RB, int V>
+// kernel variants: 0 separated, 1 general-span, 2 general-span with the wide input ring; CLAMP: the
+// both-edges children (each edge keeps its sign of change, reading R16)
+template <typename T, bool POINT, int RB, int V, bool CLAMP>
 struct RowVariant {
     static constexpr bool GEN = V >= 1;
     static constexpr int NB = V == 2 ? RW_NB_WIDE : RW_NB;
     using Smem = RowSmem<T, RB, GEN ? RW_KT_GEN : RW_KT, NB>;
-    static constexpr auto kernel = deposit_row<T, POINT, RB, GEN, NB>;
+    static constexpr auto kernel = deposit_row<T, POINT, RB, GEN, NB, CLAMP>;
 };
 
-template <typename T, bool POINT, int RB, int V>
-cudaError_t set_attr_one() {
-    using K = RowVariant<T, POINT, RB, V>;
+template <typename T, bool POINT, int RB, int V, bool CLAMP>
+cudaError_t set_attr_cl() {
+    using K = RowVariant<T, POINT, RB, V, CLAMP>;
     cudaError_t e = cudaFuncSetAttribute(K::kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)K::Smem::bytes(MAX_FAST_NV));
     if (e != cudaSuccess) return e;
@@ -1026,10 +1034,22 @@ cudaError_t set_attr_one() {
 }
 
 template <typename T, bool POINT, int RB, int V>
-cudaError_t launch_one(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, cudaStream_t st) {
-    using K = RowVariant<T, POINT, RB, V>;
+cudaError_t set_attr_one() {
+    cudaError_t e = set_attr_cl<T, POINT, RB, V, false>();
+    return e != cudaSuccess ? e : set_attr_cl<T, POINT, RB, V, true>();
+}
+
+template <typename T, bool POINT, int RB, int V, bool CLAMP>
+cudaError_t launch_cl(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, cudaStream_t st) {
+    using K = RowVariant<T, POINT, RB, V, CLAMP>;
     K::kernel<<<(unsigned)a.n_list, 32, K::Smem::bytes(a.max_nv), st>>>(*in_map, *out_map, a);
     return cudaGetLastError();
+}
+
+template <typename T, bool POINT, int RB, int V>
+cudaError_t launch_one(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, cudaStream_t st) {
+    return a.dI_floor > -INFINITY ? launch_cl<T, POINT, RB, V, true>(a, in_map, out_map, st)
+                                  : launch_cl<T, POINT, RB, V, false>(a, in_map, out_map, st);
 }
 
 template <typename T, int RB>
