@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 #include <limits.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <atomic>
 #include <type_traits>
@@ -1042,7 +1043,8 @@ cudaError_t set_attr_one() {
 template <typename T, bool POINT, int RB, int V, bool CLAMP>
 cudaError_t launch_cl(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, cudaStream_t st) {
     using K = RowVariant<T, POINT, RB, V, CLAMP>;
-    K::kernel<<<(unsigned)a.n_list, 32, K::Smem::bytes(a.max_nv), st>>>(*in_map, *out_map, a);
+    static const size_t extra = getenv("DAXM_ROW_EXTRA_SMEM") ? (size_t)atol(getenv("DAXM_ROW_EXTRA_SMEM")) : 0;
+    K::kernel<<<(unsigned)a.n_list, 32, K::Smem::bytes(a.max_nv) + extra, st>>>(*in_map, *out_map, a);
     return cudaGetLastError();
 }
 
