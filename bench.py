@@ -219,6 +219,12 @@ def main():
                     help="override the config's stack dtype (e.g. C5 in fp32, SURVEY §8(d))")
     ap.add_argument("--edge", choices=["leading", "trailing", "both"], default="leading",
                     help="wire edge(s): both = leading on the decreases + trailing on the increases (R16)")
+    ap.add_argument("--host-budget", type=float, default=0.0,
+                    help="e2e leg out of core: cap the device memory of daxm_reconstruct_host at this many GB "
+                         "(daxm_set_host_budget; 0 = whole stack resident)")
+    ap.add_argument("--jitter", type=float, default=0.0,
+                    help="non-straight scan (SURVEY f4): wire positions jittered by up to +-JITTER um "
+                         "(exact per-step depth table + the general kernel)")
     ap.add_argument("--fraction", type=float, default=1.0,
                     help="pixel percentage (P:L299-303): reconstruct only this fraction of the pixels, the "
                          "brightest by first-step intensity (daxm_select_cutoff + daxm_set_cutoff)")
@@ -258,6 +264,8 @@ def main():
         cfg = dataclasses.replace(cfg, dtype=args.dtype)
     noise = (not cfg.sparse) if args.noise is None else args.noise
     g = synth.geometry(cfg, edge=args.edge)
+    if args.jitter > 0:
+        g["wire_xyz"] = synth.jittered_wire_positions(cfg.n_steps, t_range=cfg.t_range, amp_um=args.jitter)
     R = cfg.n
     from paper_2201_13309_b200 import multi
     r0, r1 = multi.my_band(rank, world, R)  # tile-aligned row band
@@ -347,7 +355,11 @@ def main():
     h_out = torch.empty(plan.output_shape(), dtype=torch.float32).pin_memory()
     del stack
     torch.cuda.empty_cache()
+    pcie = measure_pcie(dev, stream)
+    if args.host_budget > 0:
+        plan.set_host_budget(int(args.host_budget * 1e9))
     plan.reconstruct_host(h_stack, h_out, stream)  # warm (allocates the plan's device buffers)
+    ring = plan.host_ring_info()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -364,7 +376,14 @@ def main():
     h2d = h_stack.numel() * h_stack.element_size() * world
     d2h = h_out.numel() * h_out.element_size() * world
     e2e = {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "ms_per_step": e2e_ms, "path": "daxm_reconstruct_host, pinned host buffers"}
+           "ms_per_step": e2e_ms, "path": "daxm_reconstruct_host, pinned host buffers" +
+           (f", out of core: {ring['n_bands']} bands of {ring['band_rows']} rows in a {ring['ring_bytes'] / 1e9:.2f} GB "
+            f"device ring" if ring["n_bands"] else ", whole stack resident")}
+    if pcie:
+        # PCIe roofline: the copies of both directions overlap (full duplex), so the bound is the
+        # slower direction's bytes / its measured pinned-copy bandwidth
+        bound_ms = max(h2d / world / (pcie["h2d_gbs"] * 1e9), d2h / world / (pcie["d2h_gbs"] * 1e9)) * 1e3
+        e2e["pcie_roofline"] = dict(pcie, bound_ms=bound_ms, frac=bound_ms / e2e_ms)
     return finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_max, achieved_min, value,
                   units, st, clocks, r0, r1, alg_bytes, allgather_ms, e2e, (cutoff, active), out,
                   kern_median, gather_check)
@@ -405,6 +424,31 @@ def check_gather(daxm, g, full, maps, cfg, noise, dev, stream, cutoff):
     del ref
     return {"bitexact": same, "differing_words": n_diff, "shape": list(full.shape),
             "what": "all-gathered row bands vs a single plan of the whole detector"}
+
+
+def measure_pcie(dev, stream, nbytes=1 << 30):
+    """Pinned host <-> device copy bandwidth (GB/s) of this box, one direction at a time (1 GiB, best of 3)."""
+    import torch
+    try:
+        h = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+        d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        res = {}
+        for name, dst, src in (("h2d_gbs", d, h), ("d2h_gbs", h, d)):
+            best = None
+            for _ in range(3):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                dst.copy_(src, non_blocking=True)
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                ms = a.elapsed_time(b)
+                best = ms if best is None else min(best, ms)
+            res[name] = nbytes / (best * 1e-3) / 1e9
+        del h, d
+        torch.cuda.empty_cache()
+        return res
+    except Exception:
+        return None
 
 
 def parity_spot_check(out, kept, r0, cut):
@@ -471,7 +515,9 @@ def finish(args, rank, world, plan, cfg, g, maps, noise, K, ms_step_max, kern_ma
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": args.warmup,
             "ms_per_step": ms_step_max, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": workload_config(cfg, noise, world, r1 - r0, args.edge),
+            "config": dict(workload_config(cfg, noise, world, r1 - r0, args.edge),
+                           **({"wire_path": f"jittered +-{args.jitter} um (exact per-step depth table, general kernel)"}
+                              if args.jitter > 0 else {})),
             "roofline": {"bound": "hbm", "achieved": achieved_min, "peak": peak, "unit": "GB/s",
                          "frac": achieved_min / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "deposit (daxm_reconstruct)", "kernel_ms": kern_max,

@@ -129,6 +129,9 @@ typedef struct {
     int64_t row_launches;      /* kernel launches of one daxm_reconstruct on the row path: the zero-dI  */
                                /* scan, then one per non-empty class (separated / general-span / wide   */
                                /* input ring x ring 16 / 32, general)                                    */
+    int64_t row_tiles_nb_mid;  /* of them: separated-variant tiles that need the 32-slot input ring        */
+    int64_t row_kmax_hist[8];  /* admitted row tiles by the most bin edges one walk crosses in one wire    */
+                               /* step (index = that count, 7 = 7 or more)                               */
 } daxm_plan_stats;
 
 /* daxm_create -- validate `g`, run the fp64 geometry pre-pass on `cuda_device`,

@@ -61,7 +61,7 @@ class PlanStats(C.Structure):
         ("row_tiles_small", C.c_int64), ("row_tiles_large", C.c_int64), ("row_tiles_general", C.c_int64),
         ("row_ring_need_max", C.c_int64), ("row_reject_bits", C.c_int64), ("row_reject", C.c_int64 * 8),
         ("row_path", C.c_int64), ("row_tiles_gen", C.c_int64), ("row_reject_more", C.c_int64),
-        ("row_launches", C.c_int64),
+        ("row_launches", C.c_int64), ("row_tiles_nb_mid", C.c_int64), ("row_kmax_hist", C.c_int64 * 8),
     ]
 
 

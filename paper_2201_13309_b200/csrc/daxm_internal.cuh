@@ -173,7 +173,7 @@ static_assert(LOCK_NB % LOCK_G == 0 && (LOCK_NB / LOCK_G & (LOCK_NB / LOCK_G - 1
 #define DAXM_RW_ROWS 2
 #endif
 #ifndef DAXM_RW_NB
-#define DAXM_RW_NB 32
+#define DAXM_RW_NB 24
 #endif
 #ifndef DAXM_RW_KT
 #define DAXM_RW_KT 5
@@ -181,7 +181,7 @@ static_assert(LOCK_NB % LOCK_G == 0 && (LOCK_NB / LOCK_G & (LOCK_NB / LOCK_G - 1
 constexpr int RW_ROWS = DAXM_RW_ROWS;  // 2 (tile 2 x 64) or 4 (tile 4 x 32)
 constexpr int RW_COLS = 128 / RW_ROWS;
 constexpr int RW_H = RW_COLS / 32;  // column halves per lane: pair p = half p (RW_H = 2) or rows 2p, 2p+1
-constexpr int RW_NB = DAXM_RW_NB;   // input ring slots (wire steps) per warp
+constexpr int RW_NB = DAXM_RW_NB;   // input ring slots (wire steps) per column half (a multiple of RW_G)
 constexpr int RW_G = 4;             // wire steps per TMA load box
 #ifndef DAXM_RW_PB
 #define DAXM_RW_PB 4
@@ -195,6 +195,13 @@ constexpr int RW_CLS_FRONT_LO = 0x100;  //   the front pixel edge is the shallow
 constexpr int RW_CLS_GEN = 0x200;       //   general-span variant (overlapping spans, spans up to RW_NQ_GEN bins)
 constexpr int RW_CLS_NB_WIDE = 0x400;   //   general-span variant with the RW_NB_WIDE-slot input ring
 constexpr int RW_NB_WIDE = 64;          // input ring slots for tiles whose visits spread wider than RW_NB
+constexpr int RW_CLS_NB_MID = 0x800;    //   separated variant with the RW_NB_MID-slot input ring
+constexpr int RW_NB_MID = 32;           // input ring slots of that variant
+#ifndef DAXM_RW_NB_MARGIN
+#define DAXM_RW_NB_MARGIN 8
+#endif
+constexpr int RW_NB_MARGIN = DAXM_RW_NB_MARGIN;  // RW_NB ring: visits of load lookahead the admission keeps
+static_assert(RW_NB_MARGIN % RW_G == 0 && RW_NB_MARGIN < RW_NB, "ring margin");
 constexpr int RW_KT_GEN = 6;            // max bin edges per zone and iteration, general-span variant
 constexpr int RW_NQ_GEN = 4;            // general-span variant: zone edges evaluated exactly (then linear)
 static_assert(RW_ROWS * RW_COLS == 128 && RW_COLS % 32 == 0 && (RW_ROWS == 2 || RW_ROWS == 4),
@@ -212,6 +219,7 @@ struct RowTile {
     int cls;         // admission class (RW_CLS_*), 0 = general kernel
     int niter;       // iterations of the admitted schedule (pre-pass replay)
     int why;         // not admitted: RW_WHY_* bits
+    int kmax;        // most bin edges one walk crosses in one step (admission replay)
 };
 enum : unsigned {
     RW_WHY_MODE = 1u,      // not every pixel in the separated-span regime

@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
         if (lane == 0)
 #pragma unroll 1
             for (int g = g_issue; g <= lim; ++g) {  // (in the loop: one group per four steps)
-                const int b = g & (NG - 1);
+                const int b = g % NG;
                 const int dk = dir > 0 ? g * RW_G : -g * RW_G;
                 mbar_arrive_expect_tx(&bars[b], 2 * L::IN_GROUP);
                 tma_load_3d(smem + L::OFF_IN + b * L::IN_GROUP, &in_map, col0, rowl, kb0 + dk, &bars[b]);
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
         if (gn < g_wait) return;
 #pragma unroll 1
         for (; g_wait <= gn; ++g_wait)
-            while (!mbar_try(s_bar + (uint32_t)(g_wait & (NG - 1)) * 8u, (uint32_t)(g_wait / NG) & 1u)) {
+            while (!mbar_try(s_bar + (uint32_t)(g_wait % NG) * 8u, (uint32_t)(g_wait / NG) & 1u)) {
             }
         __syncwarp();
     };
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
     // wire travel and the two pairs' intensities (rows 0, 1) at visit v of the lane's half
     auto fetch = [&](int v, float& t, float2 I[2]) {
         t = lds_f32(tau_l + 4u * (uint32_t)v);
-        const uint32_t ad = in_lane + (uint32_t)((v ^ xr_) & (NB - 1)) * (uint32_t)L::IN_SLOT;
+        const uint32_t ad = in_lane + ((uint32_t)(v ^ xr_) % (uint32_t)NB) * (uint32_t)L::IN_SLOT;
         if constexpr (sizeof(T) == 2) {
             // u16 -> fp32 exactly: 0x4B00'xxxx is 2^23 + x, one PRMT builds it from the lane's
             // half-word (the pair's column), one packed FADD removes 2^23
@@ -760,7 +760,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
     if (lane == 0) {
         // every issued input load must have landed before the CTA exits
         for (; g_wait < g_issue; ++g_wait)
-            while (!mbar_try(s_bar + (uint32_t)(g_wait & (NG - 1)) * 8u, (uint32_t)(g_wait / NG) & 1u)) {
+            while (!mbar_try(s_bar + (uint32_t)(g_wait % NG) * 8u, (uint32_t)(g_wait / NG) & 1u)) {
             }
     }
 #if DAXM_ROW_CHECK
@@ -843,9 +843,9 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
     // reasons only the separated / only the general-span variant has
     unsigned bad_sep = (!empty && ti.sep != MODE_SEPARATED) ? RW_WHY_MODE : 0u;
     unsigned bad_gen = a.point_mode ? RW_WHY_MODE : 0u;
-    unsigned bad_in[2] = {0u, 0u};  // input ring of RW_NB / RW_NB_WIDE slots
+    unsigned bad_in[3] = {0u, 0u, 0u};  // input ring of RW_NB / RW_NB_WIDE / RW_NB_MID slots
     bool back_lo = true, front_lo = true;
-    int need = 0, iters = 0;
+    int need = 0, iters = 0, kmax_tile = 0;
     if (eligible) {
         const int nvt = ti.k_hi - ti.k_lo + 1;
         const float E0 = (float)(-a.m_ref), EM = (float)(a.M - a.m_ref);
@@ -893,12 +893,14 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
                 phm[p][r] = phmm[p][r] = lo;
                 ndone[p][r] = 0;
             }
-        // input ring of RW_NB (index 0) or RW_NB_WIDE (index 1) slots per half: the same schedule,
-        // loads issued further ahead with the wider ring
+        // input ring of RW_NB (index 0), RW_NB_WIDE (1) or RW_NB_MID (2) slots per half: the same
+        // schedule, loads issued further ahead with a wider ring.  The RW_NB ring must also keep
+        // every needed group in flight RW_NB_MARGIN visits early (latency hiding: a ring that is just
+        // deadlock-free makes the fastest lanes wait for their loads); the others only deadlock-free
         const int ngroups = vend / RW_G + 1;
-        constexpr int NBs[2] = {RW_NB, RW_NB_WIDE};
-        int g_issue[2] = {min(RW_NB / RW_G, ngroups), min(RW_NB_WIDE / RW_G, ngroups)};
-        for (int b = 0; b < 2; ++b)
+        constexpr int NBs[3] = {RW_NB - RW_NB_MARGIN, RW_NB_WIDE, RW_NB_MID};
+        int g_issue[3] = {min(NBs[0] / RW_G, ngroups), min(RW_NB_WIDE / RW_G, ngroups), min(RW_NB_MID / RW_G, ngroups)};
+        for (int b = 0; b < 3; ++b)
             if (__reduce_max_sync(0xffffffffu, min(vs + 1, ve)) / RW_G >= g_issue[b]) bad_in[b] = RW_WHY_INPUT;
         auto frontier = [&]() {
             return __reduce_min_sync(
@@ -918,7 +920,7 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
             if (n == 0 || (n - 1) % RW_G == 0) {
                 const int it2 = n + 2, ahead = n == 0 ? 0 : RW_G - 1;
                 const int nd_ = min(vs_max + it2 + ahead, vend);
-                for (int b = 0; b < 2; ++b) {
+                for (int b = 0; b < 3; ++b) {
                     g_issue[b] = max(g_issue[b], min((it2 + NBs[b] - RW_G) / RW_G, ngroups - 1) + 1);
                     if (nd_ / RW_G >= g_issue[b]) bad_in[b] = RW_WHY_INPUT;  // would wait for a group not yet loadable
                 }
@@ -968,6 +970,7 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
             }
             ++v;
             kmax = __reduce_max_sync(0xffffffffu, kmax);
+            kmax_tile = max(kmax_tile, kmax);
             pmax = __reduce_max_sync(0xffffffffu, pmax);
             if (kmax > RW_KT) bad_sep |= RW_WHY_KT;
             if (kmax > RW_KT_GEN) bad_gen |= RW_WHY_KT;
@@ -987,39 +990,43 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
     bad_gen = __reduce_or_sync(0xffffffffu, bad_gen);
     bad_in[0] = __reduce_or_sync(0xffffffffu, bad_in[0]);
     bad_in[1] = __reduce_or_sync(0xffffffffu, bad_in[1]);
+    bad_in[2] = __reduce_or_sync(0xffffffffu, bad_in[2]);
     back_lo = __all_sync(0xffffffffu, back_lo);
     front_lo = __all_sync(0xffffffffu, front_lo);
     if (lane == 0) {
         int cls = 0;
         if (!(back_lo || front_lo)) bad |= RW_WHY_ORDER;
         if (need > RW_RB_LARGE) bad |= RW_WHY_RING;
-        // first that applies: separated variant, general-span variant, general-span with the wide
-        // input ring (fewer warps per SM)
-        const int variant = !bad && !bad_sep && !bad_in[0] ? 0 : !bad && !bad_gen && !bad_in[0] ? 1
-                          : !bad && !bad_gen && !bad_in[1] ? 2 : -1;
+        // first that applies: separated variant, separated with the 32-slot input ring (one warp
+        // fewer per SM), general-span variant, general-span with the wide input ring
+        const int variant = !bad && !bad_sep && !bad_in[0] ? 0 : !bad && !bad_sep && !bad_in[2] ? 3
+                          : !bad && !bad_gen && !bad_in[0] ? 1 : !bad && !bad_gen && !bad_in[1] ? 2 : -1;
         if (variant >= 0) {
             cls = need <= RW_RB_SMALL ? RW_RB_SMALL : RW_RB_LARGE;
             if (!back_lo) cls |= RW_CLS_FRONT_LO;
-            if (variant >= 1) cls |= RW_CLS_GEN;
+            if (variant == 1 || variant == 2) cls |= RW_CLS_GEN;
             if (variant == 2) cls |= RW_CLS_NB_WIDE;
+            if (variant == 3) cls |= RW_CLS_NB_MID;
         } else {
-            bad |= bad_sep | bad_gen | bad_in[0] | bad_in[1];
+            bad |= bad_sep | bad_gen | bad_in[0] | bad_in[1] | bad_in[2];
         }
         ti.cls = cls;
         ti.why = (int)bad;
         ti.niter = iters;
+        ti.kmax = kmax_tile;
         rts[rt] = ti;
         atomicAdd(&d_stats[(cls & RW_CLS_RB) == RW_RB_SMALL ? 0 : (cls & RW_CLS_RB) == RW_RB_LARGE ? 1 : 2], 1);
         atomicMax(&d_stats[3], need);
     }
 }
 
-// kernel variants: 0 separated, 1 general-span, 2 general-span with the wide input ring; CLAMP: the
+// kernel variants: 0 separated, 1 general-span, 2 general-span with the wide input ring, 3 separated
+// with the 32-slot input ring; CLAMP: the
 // both-edges children (each edge keeps its sign of change, reading R16)
 template <typename T, bool POINT, int RB, int V, bool CLAMP>
 struct RowVariant {
-    static constexpr bool GEN = V >= 1;
-    static constexpr int NB = V == 2 ? RW_NB_WIDE : RW_NB;
+    static constexpr bool GEN = V == 1 || V == 2;
+    static constexpr int NB = V == 2 ? RW_NB_WIDE : V == 3 ? RW_NB_MID : RW_NB;
     using Smem = RowSmem<T, RB, GEN ? RW_KT_GEN : RW_KT, NB>;
     static constexpr auto kernel = deposit_row<T, POINT, RB, GEN, NB, CLAMP>;
 };
@@ -1057,11 +1064,14 @@ cudaError_t launch_one(const RowArgs& a, const CUtensorMap* in_map, const CUtens
 template <typename T, int RB>
 cudaError_t launch_rb(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int variant,
                       cudaStream_t st) {
-    if (a.point_mode) return launch_one<T, true, RB, 0>(a, in_map, out_map, st);
+    if (a.point_mode)
+        return variant == 3 ? launch_one<T, true, RB, 3>(a, in_map, out_map, st)
+                            : launch_one<T, true, RB, 0>(a, in_map, out_map, st);
     switch (variant) {
         case 0: return launch_one<T, false, RB, 0>(a, in_map, out_map, st);
         case 1: return launch_one<T, false, RB, 1>(a, in_map, out_map, st);
-        default: return launch_one<T, false, RB, 2>(a, in_map, out_map, st);
+        case 2: return launch_one<T, false, RB, 2>(a, in_map, out_map, st);
+        default: return launch_one<T, false, RB, 3>(a, in_map, out_map, st);
     }
 }
 
@@ -1071,7 +1081,9 @@ cudaError_t set_attr_rb() {
     if ((e = set_attr_one<T, true, RB, 0>()) != cudaSuccess) return e;
     if ((e = set_attr_one<T, false, RB, 0>()) != cudaSuccess) return e;
     if ((e = set_attr_one<T, false, RB, 1>()) != cudaSuccess) return e;
-    return set_attr_one<T, false, RB, 2>();
+    if ((e = set_attr_one<T, false, RB, 2>()) != cudaSuccess) return e;
+    if ((e = set_attr_one<T, true, RB, 3>()) != cudaSuccess) return e;
+    return set_attr_one<T, false, RB, 3>();
 }
 
 }  // namespace

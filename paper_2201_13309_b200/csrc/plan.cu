@@ -107,9 +107,10 @@ struct daxm_plan {
     int* d_rlist = nullptr;                // class lists [small][large][general], each ascending
     std::vector<int> h_rlist;
     // row tiles per class, in h_rlist order: ring 16 / 32 x (separated, general-span, general-span
-    // with the wide input ring) = class 2 variant + (ring 32), then the not admitted ones
-    static constexpr int N_RCLS = 7;
-    int n_rcls[N_RCLS] = {0, 0, 0, 0, 0, 0, 0};
+    // with the wide input ring, separated with the 32-slot input ring) = class 2 variant + (ring 32),
+    // then the not admitted ones
+    static constexpr int N_RCLS = 9;
+    int n_rcls[N_RCLS] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
     unsigned* d_row_err = nullptr;         // DAXM_ROW_CHECK builds: schedule violations
     CUtensorMap row_in_map{}, row_out_map{};
     daxm_plan_stats stats{};
@@ -855,8 +856,9 @@ daxm_status row_prepass(daxm_plan* p, int) {
             if (ht[q].why & (1 << b)) ++p->stats.row_reject[b];
         if (ht[q].why & RW_WHY_GEN) ++p->stats.row_reject_more;
         const int rb = ht[q].cls & RW_CLS_RB;
-        const int var = (ht[q].cls & RW_CLS_NB_WIDE) ? 2 : (ht[q].cls & RW_CLS_GEN) ? 1 : 0;
-        lists[rb == RW_RB_SMALL ? 2 * var : rb == RW_RB_LARGE ? 2 * var + 1 : 6].push_back((int)q);
+        if (ht[q].cls & RW_CLS_RB) ++p->stats.row_kmax_hist[std::min(std::max(ht[q].kmax, 0), 7)];
+        const int var = (ht[q].cls & RW_CLS_NB_MID) ? 3 : (ht[q].cls & RW_CLS_NB_WIDE) ? 2 : (ht[q].cls & RW_CLS_GEN) ? 1 : 0;
+        lists[rb == RW_RB_SMALL ? 2 * var : rb == RW_RB_LARGE ? 2 * var + 1 : 8].push_back((int)q);
     }
     p->h_rlist.clear();
     for (int c = 0; c < daxm_plan::N_RCLS; ++c) {
@@ -866,10 +868,11 @@ daxm_status row_prepass(daxm_plan* p, int) {
     CK(cudaMalloc(&p->d_rlist, sizeof(int) * std::max<size_t>(p->h_rlist.size(), 1)));
     CK(cudaMemcpy(p->d_rlist, p->h_rlist.data(), sizeof(int) * p->h_rlist.size(), cudaMemcpyHostToDevice));
     CK(row_set_attributes());
-    p->stats.row_tiles_small = p->n_rcls[0] + p->n_rcls[2] + p->n_rcls[4];
-    p->stats.row_tiles_large = p->n_rcls[1] + p->n_rcls[3] + p->n_rcls[5];
+    p->stats.row_tiles_small = p->n_rcls[0] + p->n_rcls[2] + p->n_rcls[4] + p->n_rcls[6];
+    p->stats.row_tiles_large = p->n_rcls[1] + p->n_rcls[3] + p->n_rcls[5] + p->n_rcls[7];
     p->stats.row_tiles_gen = p->n_rcls[2] + p->n_rcls[3] + p->n_rcls[4] + p->n_rcls[5];
-    p->stats.row_tiles_general = p->n_rcls[6];
+    p->stats.row_tiles_general = p->n_rcls[8];
+    p->stats.row_tiles_nb_mid = p->n_rcls[6] + p->n_rcls[7];
     p->stats.row_launches = 0;
     for (int c = 0; c < daxm_plan::N_RCLS; ++c) p->stats.row_launches += p->n_rcls[c] > 0;
     p->stats.row_launches += 1;  // row_live_kernel (exact zero-dI skip)
@@ -878,7 +881,7 @@ daxm_status row_prepass(daxm_plan* p, int) {
     // kernels (step-locked, fast, general) of round 1, which cover the overlapping-span regime
     // (both-edges children take the row path with the general kernel for the rest: the deposit-tile
     // kernels neither clamp nor accumulate)
-    if (p->n_rcls[6] > 0 && getenv("DAXM_ROW_PARTIAL") == nullptr && !p->is_child) return DAXM_OK;
+    if (p->n_rcls[8] > 0 && getenv("DAXM_ROW_PARTIAL") == nullptr && !p->is_child) return DAXM_OK;
     p->stats.fit_max_err_bins = std::max(p->stats.fit_max_err_bins, ferr[0]);
     p->stats.fit_model_err_bins = std::max(p->stats.fit_model_err_bins, ferr[1]);
     p->stats.device_bytes += (int64_t)(sizeof(RowTile) * n_rt + n_rt + sizeof(float) * n_rt * NCOEF * (RW_COLS + 1) * RW_ROWS +

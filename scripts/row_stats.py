@@ -17,5 +17,6 @@ for arg in sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"]:
     print(arg, json.dumps({"small": st["row_tiles_small"], "large": st["row_tiles_large"],
                             "general": st["row_tiles_general"], "gen": st["row_tiles_gen"], "rej_gen": st["row_reject_more"],
                             "row_path": st["row_path"], "need": st["row_ring_need_max"], "reject": rej,
+                            "nb_mid": st["row_tiles_nb_mid"], "kmax_hist": st["row_kmax_hist"],
                             "model_err": st["fit_model_err_bins"], "max_err": st["fit_max_err_bins"],
                             "prepass_ms": st["prepass_ms"]}), flush=True)
