@@ -196,6 +196,8 @@ constexpr int RW_CLS_GEN = 0x200;       //   general-span variant (overlapping s
 constexpr int RW_CLS_NB_WIDE = 0x400;   //   general-span variant with the RW_NB_WIDE-slot input ring
 constexpr int RW_NB_WIDE = 64;          // input ring slots for tiles whose visits spread wider than RW_NB
 constexpr int RW_CLS_NB_MID = 0x800;    //   separated variant with the RW_NB_MID-slot input ring
+constexpr int RW_CLS_KT_SHIFT = 12;     //   bits 12-13: edge-trip class ktc of the separated variants
+                                        //   (3, 4 or 5 edges per zone and step)
 constexpr int RW_NB_MID = 32;           // input ring slots of that variant
 #ifndef DAXM_RW_NB_MARGIN
 #define DAXM_RW_NB_MARGIN 8
@@ -304,7 +306,13 @@ cudaError_t row_set_attributes();
 cudaError_t launch_row_live(const RowArgs& a, int rt0, int n, unsigned char* live, int dtype,
                             cudaStream_t st);  // exact zero-dI skip flags of row tiles [rt0, rt0 + n)  // per device: dynamic shared memory of every instance
 cudaError_t launch_row(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int dtype, int rb,
-                       int variant, cudaStream_t st);  // variant: 0 separated, 1 general-span, 2 + wide input ring
+                       int variant, int ktc, cudaStream_t st);
+// per-translation-unit instance sets of the row kernel (deposit_row.cu, deposit_row_{1,2,3}.cu)
+template <int TU>
+cudaError_t row_part_attributes_t();
+template <int TU>
+cudaError_t row_part_launch_t(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int variant,
+                              int ktc, cudaStream_t st);  // variant: 0 separated, 1 general-span, 2 + wide input ring
 cudaError_t launch_general_rows(const DepositArgs& a, const int* rt_list, int n, int n_rc, int row_org,
                                 const void* stack, int dtype, float* out, cudaStream_t st);
 

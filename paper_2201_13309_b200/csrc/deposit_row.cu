@@ -46,6 +46,9 @@
 #include "fp2.cuh"
 #include "ptx.cuh"
 
+#ifndef DAXM_ROW_TU
+#define DAXM_ROW_TU 0  // which instance set this translation unit compiles (see the end of the file)
+#endif
 #define DAXM_PRAGMA_(x) _Pragma(#x)
 #define DAXM_PRAGMA_UNROLL(n) DAXM_PRAGMA_(unroll n)
 #ifndef DAXM_ROW_CHECK
@@ -274,12 +277,14 @@ __device__ __forceinline__ void row_starts(const RowWalk wk[2][2], int lane, int
 #ifndef DAXM_RW_MINB
 #define DAXM_RW_MINB 11  // resident CTAs (= warps) per SM the separated variant's registers allow
 #endif
-template <typename T, bool POINT, int RB, bool GEN, int NB, bool CLAMP>
+template <typename T, bool POINT, int RB, bool GEN, int NB, bool CLAMP, int KTS>
 __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const __grid_constant__ CUtensorMap in_map,
                                                             const __grid_constant__ CUtensorMap out_map,
                                                             const RowArgs a) {
     static_assert(!(GEN && POINT), "the general-span variant is for finite pixels");
-    constexpr int KT = GEN ? RW_KT_GEN : RW_KT;  // max edges per zone and iteration
+    // max edges per zone and iteration: the separated variants by class (the tile's largest count,
+    // admission replay; every trip unrolled), the general-span variant RW_KT_GEN (5 trips + a rare 6th)
+    constexpr int KT = GEN ? RW_KT_GEN : KTS;
     using L = RowSmem<T, RB, KT, NB>;
     constexpr int NG = L::NG;
     static_assert(RB % RW_PB == 0 && (RB & (RB - 1)) == 0, "ring");
@@ -691,7 +696,9 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
     // The bin-edge stores of a zone: F at edge k of walk (p, r) goes to slot En + k - 1, staged slot
     // es + k planes (immediate offsets; row r, column half p), iff k < cnt.  Branch-free: RW_ST
     // predicated stores per walk, a rare extra trip when some zone holds more edges.
-    constexpr int RW_ST = GEN ? 5 : 4;  // (general-span zones, up to 5 bins, hold more edges)
+    // unrolled trips: every one of KT for the 3- and 4-edge classes; 4 + a rare 5th (warp vote) for the
+    // 5-edge class (measured: all five unconditional cost C5 4 %); general spans 5 + a rare 6th
+    constexpr int RW_ST = GEN ? 5 : (KT < 4 ? KT : 4);
     auto edges = [&](const Zone Z[2]) {
         static_for<0, 2>([&](auto pc) {
             constexpr int p = decltype(pc)::value;
@@ -706,6 +713,13 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
             });
             return true;
         });
+#if DAXM_ROW_CHECK
+        if constexpr (RW_ST == KT) {
+            const float cm = fmaxf(fmaxf(Z[0].cnt.x, Z[0].cnt.y), fmaxf(Z[1].cnt.x, Z[1].cnt.y));
+            if (cm > (float)KT) viol |= 2u;
+        }
+#endif
+        if constexpr (RW_ST < KT) {
         const float cmax = fmaxf(fmaxf(Z[0].cnt.x, Z[0].cnt.y), fmaxf(Z[1].cnt.x, Z[1].cnt.y));
         if (__any_sync(0xffffffffu, cmax > (float)RW_ST)) {  // rare: zones with more edges
             static_for<0, 2>([&](auto pc) {
@@ -723,6 +737,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
 #if DAXM_ROW_CHECK
             if (cmax > (float)KT) viol |= 2u;
 #endif
+        }
         }
     };
     // Software pipeline: the stores of step n's zones and step n + 1's transition are independent,
@@ -769,6 +784,7 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
 #endif
 }
 
+#if DAXM_ROW_TU == 0
 // ------------------------------------------------------------------ exact zero-dI skip
 // One warp per row tile of [rt0, rt0 + n).  A tile whose intensities are the same at every step of
 // its range [k_lo, k_hi] has every dI = 0, so every bin value the row kernel would store is exactly 0:
@@ -1003,6 +1019,9 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
                           : !bad && !bad_gen && !bad_in[0] ? 1 : !bad && !bad_gen && !bad_in[1] ? 2 : -1;
         if (variant >= 0) {
             cls = need <= RW_RB_SMALL ? RW_RB_SMALL : RW_RB_LARGE;
+            // edge-trip class of the separated variants (POINT plans: 5 only)
+            const int ktc = (variant == 1 || variant == 2 || a.point_mode) ? 2 : kmax_tile <= 3 ? 0 : kmax_tile == 4 ? 1 : 2;
+            cls |= ktc << RW_CLS_KT_SHIFT;
             if (!back_lo) cls |= RW_CLS_FRONT_LO;
             if (variant == 1 || variant == 2) cls |= RW_CLS_GEN;
             if (variant == 2) cls |= RW_CLS_NB_WIDE;
@@ -1020,20 +1039,23 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
     }
 }
 
+#endif  // DAXM_ROW_TU == 0
+
 // kernel variants: 0 separated, 1 general-span, 2 general-span with the wide input ring, 3 separated
 // with the 32-slot input ring; CLAMP: the
 // both-edges children (each edge keeps its sign of change, reading R16)
-template <typename T, bool POINT, int RB, int V, bool CLAMP>
+// KTS: edges per zone of the separated variants (3, 4 or 5 = RW_KT_CLASS[ktc])
+template <typename T, bool POINT, int RB, int V, bool CLAMP, int KTS>
 struct RowVariant {
     static constexpr bool GEN = V == 1 || V == 2;
     static constexpr int NB = V == 2 ? RW_NB_WIDE : V == 3 ? RW_NB_MID : RW_NB;
-    using Smem = RowSmem<T, RB, GEN ? RW_KT_GEN : RW_KT, NB>;
-    static constexpr auto kernel = deposit_row<T, POINT, RB, GEN, NB, CLAMP>;
+    using Smem = RowSmem<T, RB, GEN ? RW_KT_GEN : KTS, NB>;
+    static constexpr auto kernel = deposit_row<T, POINT, RB, GEN, NB, CLAMP, GEN ? RW_KT : KTS>;
 };
 
-template <typename T, bool POINT, int RB, int V, bool CLAMP>
+template <typename T, bool POINT, int RB, int V, bool CLAMP, int KTS>
 cudaError_t set_attr_cl() {
-    using K = RowVariant<T, POINT, RB, V, CLAMP>;
+    using K = RowVariant<T, POINT, RB, V, CLAMP, KTS>;
     cudaError_t e = cudaFuncSetAttribute(K::kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)K::Smem::bytes(MAX_FAST_NV));
     if (e != cudaSuccess) return e;
@@ -1041,37 +1063,47 @@ cudaError_t set_attr_cl() {
                                 (int)cudaSharedmemCarveoutMaxShared);
 }
 
-template <typename T, bool POINT, int RB, int V>
+template <typename T, bool POINT, int RB, int V, int KTS = RW_KT>
 cudaError_t set_attr_one() {
-    cudaError_t e = set_attr_cl<T, POINT, RB, V, false>();
-    return e != cudaSuccess ? e : set_attr_cl<T, POINT, RB, V, true>();
+    cudaError_t e = set_attr_cl<T, POINT, RB, V, false, KTS>();
+    return e != cudaSuccess ? e : set_attr_cl<T, POINT, RB, V, true, KTS>();
 }
 
-template <typename T, bool POINT, int RB, int V, bool CLAMP>
+template <typename T, bool POINT, int RB, int V, bool CLAMP, int KTS>
 cudaError_t launch_cl(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, cudaStream_t st) {
-    using K = RowVariant<T, POINT, RB, V, CLAMP>;
+    using K = RowVariant<T, POINT, RB, V, CLAMP, KTS>;
     static const size_t extra = getenv("DAXM_ROW_EXTRA_SMEM") ? (size_t)atol(getenv("DAXM_ROW_EXTRA_SMEM")) : 0;
     K::kernel<<<(unsigned)a.n_list, 32, K::Smem::bytes(a.max_nv) + extra, st>>>(*in_map, *out_map, a);
     return cudaGetLastError();
 }
 
-template <typename T, bool POINT, int RB, int V>
+template <typename T, bool POINT, int RB, int V, int KTS = RW_KT>
 cudaError_t launch_one(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, cudaStream_t st) {
-    return a.dI_floor > -INFINITY ? launch_cl<T, POINT, RB, V, true>(a, in_map, out_map, st)
-                                  : launch_cl<T, POINT, RB, V, false>(a, in_map, out_map, st);
+    return a.dI_floor > -INFINITY ? launch_cl<T, POINT, RB, V, true, KTS>(a, in_map, out_map, st)
+                                  : launch_cl<T, POINT, RB, V, false, KTS>(a, in_map, out_map, st);
+}
+
+template <typename T, int RB, int V>
+cudaError_t launch_kt(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int ktc,
+                      cudaStream_t st) {  // separated variants: edge-trip class
+    switch (ktc) {
+        case 0: return launch_one<T, false, RB, V, 3>(a, in_map, out_map, st);
+        case 1: return launch_one<T, false, RB, V, 4>(a, in_map, out_map, st);
+        default: return launch_one<T, false, RB, V, 5>(a, in_map, out_map, st);
+    }
 }
 
 template <typename T, int RB>
-cudaError_t launch_rb(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int variant,
+cudaError_t launch_rb(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int variant, int ktc,
                       cudaStream_t st) {
     if (a.point_mode)
         return variant == 3 ? launch_one<T, true, RB, 3>(a, in_map, out_map, st)
                             : launch_one<T, true, RB, 0>(a, in_map, out_map, st);
     switch (variant) {
-        case 0: return launch_one<T, false, RB, 0>(a, in_map, out_map, st);
+        case 0: return launch_kt<T, RB, 0>(a, in_map, out_map, ktc, st);
         case 1: return launch_one<T, false, RB, 1>(a, in_map, out_map, st);
         case 2: return launch_one<T, false, RB, 2>(a, in_map, out_map, st);
-        default: return launch_one<T, false, RB, 3>(a, in_map, out_map, st);
+        default: return launch_kt<T, RB, 3>(a, in_map, out_map, ktc, st);
     }
 }
 
@@ -1079,33 +1111,56 @@ template <typename T, int RB>
 cudaError_t set_attr_rb() {
     cudaError_t e;
     if ((e = set_attr_one<T, true, RB, 0>()) != cudaSuccess) return e;
-    if ((e = set_attr_one<T, false, RB, 0>()) != cudaSuccess) return e;
+    if ((e = set_attr_one<T, false, RB, 0, 3>()) != cudaSuccess) return e;
+    if ((e = set_attr_one<T, false, RB, 0, 4>()) != cudaSuccess) return e;
+    if ((e = set_attr_one<T, false, RB, 0, 5>()) != cudaSuccess) return e;
     if ((e = set_attr_one<T, false, RB, 1>()) != cudaSuccess) return e;
     if ((e = set_attr_one<T, false, RB, 2>()) != cudaSuccess) return e;
     if ((e = set_attr_one<T, true, RB, 3>()) != cudaSuccess) return e;
-    return set_attr_one<T, false, RB, 3>();
+    if ((e = set_attr_one<T, false, RB, 3, 3>()) != cudaSuccess) return e;
+    if ((e = set_attr_one<T, false, RB, 3, 4>()) != cudaSuccess) return e;
+    return set_attr_one<T, false, RB, 3, 5>();
 }
 
 }  // namespace
 
+// Instances are spread over four translation units (deposit_row.cu and deposit_row_{1,2,3}.cu, which
+// include this file with DAXM_ROW_TU = 1, 2, 3) so that they compile in parallel:
+// TU 0 u16 / ring 16 (+ the replay, the zero-dI scan and the dispatch), 1 u16 / ring 32, 2 f32 / ring 16,
+// 3 f32 / ring 32.
+using RowT = std::conditional_t<(DAXM_ROW_TU >= 2), float, uint16_t>;
+constexpr int ROW_RB = (DAXM_ROW_TU & 1) ? RW_RB_LARGE : RW_RB_SMALL;
+template <>
+cudaError_t row_part_attributes_t<DAXM_ROW_TU>() {
+    return set_attr_rb<RowT, ROW_RB>();
+}
+template <>
+cudaError_t row_part_launch_t<DAXM_ROW_TU>(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
+                                          int variant, int ktc, cudaStream_t st) {
+    return launch_rb<RowT, ROW_RB>(a, in_map, out_map, variant, ktc, st);
+}
+
+#if DAXM_ROW_TU == 0
 // The dynamic shared memory limit is a per-device function attribute: set it on the current
 // device for every instance (daxm_create calls this on the plan's device).
 cudaError_t row_set_attributes() {
     cudaError_t e;
-    if ((e = set_attr_rb<uint16_t, RW_RB_SMALL>()) != cudaSuccess) return e;
-    if ((e = set_attr_rb<uint16_t, RW_RB_LARGE>()) != cudaSuccess) return e;
-    if ((e = set_attr_rb<float, RW_RB_SMALL>()) != cudaSuccess) return e;
-    return set_attr_rb<float, RW_RB_LARGE>();
+    if ((e = row_part_attributes_t<0>()) != cudaSuccess) return e;
+    if ((e = row_part_attributes_t<1>()) != cudaSuccess) return e;
+    if ((e = row_part_attributes_t<2>()) != cudaSuccess) return e;
+    return row_part_attributes_t<3>();
 }
 
 cudaError_t launch_row(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int dtype, int rb,
-                       int variant, cudaStream_t st) {
+                       int variant, int ktc, cudaStream_t st) {
     if (a.n_list <= 0) return cudaSuccess;
-    if (dtype == DAXM_U16)
-        return rb == RW_RB_SMALL ? launch_rb<uint16_t, RW_RB_SMALL>(a, in_map, out_map, variant, st)
-                                 : launch_rb<uint16_t, RW_RB_LARGE>(a, in_map, out_map, variant, st);
-    return rb == RW_RB_SMALL ? launch_rb<float, RW_RB_SMALL>(a, in_map, out_map, variant, st)
-                             : launch_rb<float, RW_RB_LARGE>(a, in_map, out_map, variant, st);
+    const int tu = (dtype == DAXM_U16 ? 0 : 2) + (rb == RW_RB_SMALL ? 0 : 1);
+    switch (tu) {
+        case 0: return row_part_launch_t<0>(a, in_map, out_map, variant, ktc, st);
+        case 1: return row_part_launch_t<1>(a, in_map, out_map, variant, ktc, st);
+        case 2: return row_part_launch_t<2>(a, in_map, out_map, variant, ktc, st);
+        default: return row_part_launch_t<3>(a, in_map, out_map, variant, ktc, st);
+    }
 }
 
 cudaError_t launch_row_live(const RowArgs& a, int rt0, int n, unsigned char* live, int dtype, cudaStream_t st) {
@@ -1123,5 +1178,7 @@ cudaError_t launch_row_admit(const RowArgs& a, RowTile* rt, int n_rt, int* d_sta
     row_admit_kernel<<<(unsigned)n_rt, 32, 0, st>>>(a, rt, n_rt, d_stats);
     return cudaGetLastError();
 }
+
+#endif  // DAXM_ROW_TU == 0
 
 }  // namespace daxm

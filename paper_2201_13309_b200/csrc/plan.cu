@@ -89,8 +89,9 @@ struct daxm_plan {
     size_t ring_in_bytes = 0, ring_out_bytes = 0;
     cudaEvent_t ev_ring[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int last_ring_rows = 0, last_ring_bands = 0;  // layout of the last host call (0: in core)
-    cudaStream_t st_cls[2] = {nullptr, nullptr};     // concurrent step-locked class launches (fork/join)
-    cudaEvent_t ev_cls[3] = {nullptr, nullptr, nullptr};
+    static constexpr int N_FORK = 7;                 // forked streams for concurrent class launches
+    cudaStream_t st_cls[N_FORK] = {};                 // (deposit-tile path: the first two)
+    cudaEvent_t ev_cls[N_FORK + 1] = {};
     std::vector<cudaEvent_t> ev;
     int use_cutoff = 0;  // intensity cutoff (f1, reading R14)
     float cutoff = 0.f;
@@ -106,11 +107,12 @@ struct daxm_plan {
     float* d_rcoef = nullptr;
     int* d_rlist = nullptr;                // class lists [small][large][general], each ascending
     std::vector<int> h_rlist;
-    // row tiles per class, in h_rlist order: ring 16 / 32 x (separated, general-span, general-span
-    // with the wide input ring, separated with the 32-slot input ring) = class 2 variant + (ring 32),
-    // then the not admitted ones
-    static constexpr int N_RCLS = 9;
-    int n_rcls[N_RCLS] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    // row tiles per class, in h_rlist order: class 2 (variant + 4 ktc) + (ring 32): ring 16 / 32 x
+    // variant (separated, general-span, general-span with the wide input ring, separated with the
+    // 32-slot input ring) x edge-trip class ktc (3 / 4 / 5 edges per zone; separated variants), then
+    // the not admitted ones (general kernel)
+    static constexpr int N_RCLS = 25;
+    int n_rcls[N_RCLS] = {};
     unsigned* d_row_err = nullptr;         // DAXM_ROW_CHECK builds: schedule violations
     CUtensorMap row_in_map{}, row_out_map{};
     daxm_plan_stats stats{};
@@ -694,10 +696,14 @@ void free_plan_memory(daxm_plan* p) {
     p->d_rcoef = nullptr;
     p->d_rlist = nullptr;
     p->d_row_err = nullptr;
-    for (int i = 0; i < 2; ++i)
-        if (p->st_cls[i]) cudaStreamDestroy(p->st_cls[i]);
-    for (int i = 0; i < 3; ++i)
-        if (p->ev_cls[i]) cudaEventDestroy(p->ev_cls[i]);
+    for (cudaStream_t& x : p->st_cls) {
+        if (x) cudaStreamDestroy(x);
+        x = nullptr;
+    }
+    for (cudaEvent_t& x : p->ev_cls) {
+        if (x) cudaEventDestroy(x);
+        x = nullptr;
+    }
     if (p->st_in) cudaStreamDestroy(p->st_in);
     if (p->st_out) cudaStreamDestroy(p->st_out);
     p->st_in = p->st_out = nullptr;
@@ -858,7 +864,9 @@ daxm_status row_prepass(daxm_plan* p, int) {
         const int rb = ht[q].cls & RW_CLS_RB;
         if (ht[q].cls & RW_CLS_RB) ++p->stats.row_kmax_hist[std::min(std::max(ht[q].kmax, 0), 7)];
         const int var = (ht[q].cls & RW_CLS_NB_MID) ? 3 : (ht[q].cls & RW_CLS_NB_WIDE) ? 2 : (ht[q].cls & RW_CLS_GEN) ? 1 : 0;
-        lists[rb == RW_RB_SMALL ? 2 * var : rb == RW_RB_LARGE ? 2 * var + 1 : 8].push_back((int)q);
+        const int ktc = (ht[q].cls >> RW_CLS_KT_SHIFT) & 3;
+        const int c = 2 * (var + 4 * ktc);
+        lists[rb == RW_RB_SMALL ? c : rb == RW_RB_LARGE ? c + 1 : daxm_plan::N_RCLS - 1].push_back((int)q);
     }
     p->h_rlist.clear();
     for (int c = 0; c < daxm_plan::N_RCLS; ++c) {
@@ -868,11 +876,13 @@ daxm_status row_prepass(daxm_plan* p, int) {
     CK(cudaMalloc(&p->d_rlist, sizeof(int) * std::max<size_t>(p->h_rlist.size(), 1)));
     CK(cudaMemcpy(p->d_rlist, p->h_rlist.data(), sizeof(int) * p->h_rlist.size(), cudaMemcpyHostToDevice));
     CK(row_set_attributes());
-    p->stats.row_tiles_small = p->n_rcls[0] + p->n_rcls[2] + p->n_rcls[4] + p->n_rcls[6];
-    p->stats.row_tiles_large = p->n_rcls[1] + p->n_rcls[3] + p->n_rcls[5] + p->n_rcls[7];
-    p->stats.row_tiles_gen = p->n_rcls[2] + p->n_rcls[3] + p->n_rcls[4] + p->n_rcls[5];
-    p->stats.row_tiles_general = p->n_rcls[8];
-    p->stats.row_tiles_nb_mid = p->n_rcls[6] + p->n_rcls[7];
+    for (int c = 0; c + 1 < daxm_plan::N_RCLS; ++c) {
+        const int var = (c / 2) % 4;
+        ((c & 1) ? p->stats.row_tiles_large : p->stats.row_tiles_small) += p->n_rcls[c];
+        if (var == 1 || var == 2) p->stats.row_tiles_gen += p->n_rcls[c];
+        if (var == 3) p->stats.row_tiles_nb_mid += p->n_rcls[c];
+    }
+    p->stats.row_tiles_general = p->n_rcls[daxm_plan::N_RCLS - 1];
     p->stats.row_launches = 0;
     for (int c = 0; c < daxm_plan::N_RCLS; ++c) p->stats.row_launches += p->n_rcls[c] > 0;
     p->stats.row_launches += 1;  // row_live_kernel (exact zero-dI skip)
@@ -881,7 +891,7 @@ daxm_status row_prepass(daxm_plan* p, int) {
     // kernels (step-locked, fast, general) of round 1, which cover the overlapping-span regime
     // (both-edges children take the row path with the general kernel for the rest: the deposit-tile
     // kernels neither clamp nor accumulate)
-    if (p->n_rcls[8] > 0 && getenv("DAXM_ROW_PARTIAL") == nullptr && !p->is_child) return DAXM_OK;
+    if (p->n_rcls[daxm_plan::N_RCLS - 1] > 0 && getenv("DAXM_ROW_PARTIAL") == nullptr && !p->is_child) return DAXM_OK;
     p->stats.fit_max_err_bins = std::max(p->stats.fit_max_err_bins, ferr[0]);
     p->stats.fit_model_err_bins = std::max(p->stats.fit_model_err_bins, ferr[1]);
     p->stats.device_bytes += (int64_t)(sizeof(RowTile) * n_rt + n_rt + sizeof(float) * n_rt * NCOEF * (RW_COLS + 1) * RW_ROWS +
@@ -889,8 +899,8 @@ daxm_status row_prepass(daxm_plan* p, int) {
     p->row_ok = true;
     p->stats.row_path = 1;
     if (p->stats.row_launches > 1 && !p->st_cls[0]) {  // class launches fork
-        for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&p->st_cls[i], cudaStreamNonBlocking));
-        for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&p->ev_cls[i], cudaEventDisableTiming));
+        for (cudaStream_t& x : p->st_cls) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+        for (cudaEvent_t& x : p->ev_cls) CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     }
     return DAXM_OK;
 }
@@ -1068,8 +1078,8 @@ daxm_status device_prepass(daxm_plan* p) {
         // several tile classes: their launches run concurrently on forked streams
         const int ncls = (p->lock_small > 0) + (p->lock_large > 0) + (p->lock_ov_small > 0) + (p->lock_ov_large > 0);
         if (ncls >= 2) {
-            for (int i = 0; i < 2; ++i) CK(cudaStreamCreateWithFlags(&p->st_cls[i], cudaStreamNonBlocking));
-            for (int i = 0; i < 3; ++i) CK(cudaEventCreateWithFlags(&p->ev_cls[i], cudaEventDisableTiming));
+            for (cudaStream_t& x : p->st_cls) CK(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking));
+            for (cudaEvent_t& x : p->ev_cls) CK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
         }
     }
     if (!use_table) {
@@ -1477,34 +1487,37 @@ static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_o
         }
         a.live = p->d_rlive;
     }
-    const bool fork = n_launch >= 2 && p->st_cls[0] != nullptr && getenv("DAXM_NO_FORK") == nullptr;
-    cudaStream_t sts[3] = {st, fork ? p->st_cls[0] : st, fork ? p->st_cls[1] : st};
+    // every class launch on its own stream (up to N_FORK + 1): they run concurrently, so no launch
+    // waits for another's tail; forked from st and joined back into it (graph-capturable)
+    const int nfork = n_launch >= 2 && p->st_cls[0] != nullptr && getenv("DAXM_NO_FORK") == nullptr
+                          ? std::min(n_launch - 1, (int)daxm_plan::N_FORK) : 0;
+    cudaStream_t sts[daxm_plan::N_FORK + 1];
+    sts[0] = st;
+    for (int i = 0; i < daxm_plan::N_FORK; ++i) sts[1 + i] = i < nfork ? p->st_cls[i] : st;
     cudaError_t e = cudaSuccess;
-    if (fork) {
+    if (nfork) {
         e = cudaEventRecord(p->ev_cls[0], st);
-        for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(p->st_cls[i], p->ev_cls[0], 0);
+        for (int i = 0; i < nfork && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(p->st_cls[i], p->ev_cls[0], 0);
     }
-    // launches in class order, spread over the three streams (largest classes first on separate ones)
     int li = 0;
     for (int c = 0; c < NC - 1 && e == cudaSuccess; ++c) {
         a.list = p->d_rlist + seg[c][0];
         a.n_list = seg[c][1] - seg[c][0];
         if (a.n_list <= 0) continue;
-        e = launch_row(a, &p->row_in_map, &p->row_out_map, dt, (c & 1) == 0 ? RW_RB_SMALL : RW_RB_LARGE, c / 2,
-                       sts[li++ % 3]);
+        e = launch_row(a, &p->row_in_map, &p->row_out_map, dt, (c & 1) == 0 ? RW_RB_SMALL : RW_RB_LARGE, (c / 2) % 4, c / 8,
+                       sts[li++ % (nfork + 1)]);
     }
     if (e == cudaSuccess && seg[NC - 1][1] > seg[NC - 1][0]) {
         DepositArgs ga = make_args(p, dt);
         ga.stack = d_stack;
         e = launch_general_rows(ga, p->d_rlist + seg[NC - 1][0], seg[NC - 1][1] - seg[NC - 1][0], p->n_rc, p->row_org,
-                                d_stack, dt, d_out, sts[li++ % 3]);
+                                d_stack, dt, d_out, sts[li++ % (nfork + 1)]);
     }
-    if (fork) {  // join even after a failed launch, so a capture or the caller's stream stays consistent
-        for (int i = 0; i < 2; ++i) {
-            cudaError_t j = cudaEventRecord(p->ev_cls[1 + i], p->st_cls[i]);
-            if (j == cudaSuccess) j = cudaStreamWaitEvent(st, p->ev_cls[1 + i], 0);
-            if (e == cudaSuccess) e = j;
-        }
+    // join even after a failed launch, so a capture or the caller's stream stays consistent
+    for (int i = 0; i < nfork; ++i) {
+        cudaError_t j = cudaEventRecord(p->ev_cls[1 + i], p->st_cls[i]);
+        if (j == cudaSuccess) j = cudaStreamWaitEvent(st, p->ev_cls[1 + i], 0);
+        if (e == cudaSuccess) e = j;
     }
     if (e == cudaSuccess && d_profile) e = launch_profile_reduce(p->d_prof_part, ra * p->n_rc, (rb - ra) * p->n_rc, p->M,
                                                                 d_profile, st);

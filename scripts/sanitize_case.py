@@ -34,7 +34,7 @@ def case(name, g, host, cutoff=None, host_path=False):
     print("ok", name, flush=True)
 
 
-which = sys.argv[1:] or ["c1", "c1p", "c2t", "ragged", "cut", "host", "general"]
+which = sys.argv[1:] or ["c1", "c1p", "c2t", "ragged", "cut", "host", "both", "prof", "ooc", "general"]
 if "c1" in which:
     case("C1 finite f32", synth.geometry("C1"), synth.stack_numpy(synth.make_maps("C1"), "f32", noise=True))
 if "c1p" in which:
@@ -53,6 +53,27 @@ if "cut" in which:
 if "host" in which:
     case("C2 host path", synth.geometry("C2"), synth.stack_numpy(synth.make_maps("C2"), "u16", noise=True),
          host_path=True)
+if "both" in which:  # both-edges children: clamp + red.global.add copy-out
+    case("C2 both edges", synth.geometry("C2", edge="both"), synth.stack_numpy(synth.make_maps("C2"), "f32", noise=True))
+if "prof" in which:  # fused depth profile (the copy-out's warp sums)
+    g = synth.geometry("C2")
+    host = synth.stack_numpy(synth.make_maps("C2"), "u16", noise=True)
+    with daxm.create(g, device=0) as plan:
+        out, prof = plan.reconstruct_profile(torch.from_numpy(host).cuda())
+        torch.cuda.synchronize()
+        ref = oracle.reconstruct(g, host)
+        parity.check(out.cpu().numpy(), ref, host, "C2 fused profile")
+        assert np.allclose(prof.cpu().numpy(), oracle.depth_profile(ref), rtol=1e-5, atol=1e-3 * np.abs(ref).sum())
+    print("ok C2 fused profile", flush=True)
+if "ooc" in which:  # out-of-core host ring (two device slots, band plans)
+    g = synth.geometry("C2")
+    host = synth.stack_numpy(synth.make_maps("C2"), "u16", noise=True)
+    with daxm.create(g, device=0) as plan:
+        plan.set_host_budget((host.nbytes + 101 * 512 * 512 * 4) // 2)
+        gpu = np.asarray(plan.reconstruct_host(host))
+        assert plan.host_ring_info()["n_bands"] >= 2
+    parity.check(gpu, oracle.reconstruct(g, host), host, "C2 out of core")
+    print("ok C2 out of core", flush=True)
 if "general" in which:
     os.environ["DAXM_FORCE_GENERAL"] = "1"
     case("C1 general", synth.geometry("C1"), synth.stack_numpy(synth.make_maps("C1"), "f32", noise=True))
