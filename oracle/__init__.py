@@ -43,6 +43,7 @@ class OracleGeometry(C.Structure):
         ("n_steps", C.c_int32), ("wire_xyz", C.POINTER(C.c_double)),
         ("depth_start", C.c_double), ("depth_end", C.c_double), ("depth_res", C.c_double),
         ("edge", C.c_int32), ("pixel_model", C.c_int32), ("raw_sign", C.c_int32),
+        ("step_weight", C.POINTER(C.c_double)),
     ]
 
 
@@ -103,7 +104,13 @@ class Geometry:
             int(g["n_rows"]), int(g["n_cols"]), float(g["pitch_col"]), float(g["pitch_row"]),
             _v3(g["det_rot"]), _v3(g["det_trans"]), _v3(g["beam_dir"]), _v3(g["beam_origin"]),
             _v3(g["wire_axis"]), float(g["wire_radius"]), int(self.wire.shape[0]), _dp(self.wire),
-            float(g["depth_start"]), float(g["depth_end"]), float(g["depth_res"]), edge, pm, int(raw_sign))
+            float(g["depth_start"]), float(g["depth_end"]), float(g["depth_res"]), edge, pm, int(raw_sign),
+            None)
+        w = g.get("step_weight")
+        if w is not None:  # per-step intensity normalisation (reading R17)
+            self.weight = np.ascontiguousarray(np.asarray(w, dtype=np.float64).reshape(-1))
+            assert self.weight.shape[0] == self.wire.shape[0]
+            self.s.step_weight = _dp(self.weight)
 
     @property
     def n_bins(self) -> int:

@@ -51,6 +51,9 @@ typedef struct {
     int32_t edge;                  /* 0 leading, 1 trailing, 2 both (reading R16)            */
     int32_t pixel_model;           /* 0 finite (trapezoid), 1 point (box)                    */
     int32_t raw_sign;              /* 1: s = +1 even for trailing (used by identity tests)   */
+    const double *step_weight;     /* NULL, or [S] per-step intensity normalisation w_k      */
+                                   /* (SURVEY §8(f)4 "per-step I0 normalisation"; the paper */
+                                   /* is silent, reading R17: dI = s (w_k I_k - w_k+1 I_k+1)) */
 } oracle_geometry;
 
 enum { ORC_OK = 0, ORC_ERR_ARG = 1 };
@@ -226,7 +229,8 @@ int oracle_reconstruct_pixels(const oracle_geometry *g, int n_pix, const int32_t
         double sb = oracle_edge_sigma(back, W0, Wl, axis, e);
         double sf = oracle_edge_sigma(front, W0, Wl, axis, e);
         for (int k = 0; k + 1 < S; ++k) {
-            double dI = s * (I[k] - I[k + 1]);
+            const double wa = g->step_weight ? g->step_weight[k] : 1.0, wb = g->step_weight ? g->step_weight[k + 1] : 1.0;
+            double dI = s * (wa * I[k] - wb * I[k + 1]); /* reading R17 (w = 1 without normalisation) */
             if (g->edge == 2 && dI < 0.0) dI = 0.0; /* reading R16: each edge its own sign of change */
             if (dI == 0.0) continue;
             const double *Wa = g->wire_xyz + 3 * k, *Wb = g->wire_xyz + 3 * (k + 1);
