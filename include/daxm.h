@@ -193,6 +193,15 @@ daxm_status daxm_reconstruct(daxm_plan *p, const void *d_stack, daxm_dtype dt, f
 daxm_status daxm_reconstruct_host(daxm_plan *p, const void *h_stack, daxm_dtype dt, float *h_out,
                                   void *cuda_stream);
 
+/* daxm_set_step_weights -- per-step intensity normalisation (SURVEY §8(f)4 "per-step I0
+ * normalisation"; the paper is silent, reading R17 in DESIGN.md): with w (host pointer, S
+ * finite positive doubles, copied) later reconstructions use dI_k = s (w_k I_k - w_{k+1} I_{k+1}),
+ * e.g. w_k = I0_ref / I0_k from the beam monitor; w = NULL switches it off.  The cutoff still
+ * compares the raw first image (reading R14).  Normalised plans run the general kernel (one
+ * thread per pixel; the fast kernels stream raw intensities).  Errors: INVALID_ARGUMENT (a weight
+ * not finite or <= 0), OUT_OF_MEMORY, CUDA. */
+daxm_status daxm_set_step_weights(daxm_plan *p, const double *w);
+
 /* daxm_set_host_budget -- cap, in bytes, on the device memory daxm_reconstruct_host may hold for
  * stack and output buffers (0 = no cap, the default).  Takes effect at the next host call; band
  * plans already built for another band height are rebuilt.  Errors: INVALID_ARGUMENT (NULL plan). */

@@ -86,6 +86,8 @@ def lib():
         L.daxm_reconstruct.restype = C.c_int
         L.daxm_reconstruct_host.argtypes = [P, P, C.c_int, P, P]
         L.daxm_reconstruct_host.restype = C.c_int
+        L.daxm_set_step_weights.argtypes = [P, C.POINTER(C.c_double)]
+        L.daxm_set_step_weights.restype = C.c_int
         L.daxm_set_host_budget.argtypes = [P, C.c_uint64]
         L.daxm_set_host_budget.restype = C.c_int
         L.daxm_host_ring_info.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
@@ -300,6 +302,16 @@ class Plan:
         self._check(lib().daxm_reconstruct_host(self._h, C.c_void_p(stack.data_ptr()), dt,
                                                 C.c_void_p(out.data_ptr()), C.c_void_p(st)))
         return out
+
+    def set_step_weights(self, w):
+        """Per-step intensity normalisation w_k (S positive values; None: off), daxm_set_step_weights."""
+        if w is None:
+            self._check(lib().daxm_set_step_weights(self._h, None))
+            return
+        w = np.ascontiguousarray(np.asarray(w, dtype=np.float64).reshape(-1))
+        if w.shape[0] != self.n_steps:
+            raise ValueError(f"{w.shape[0]} weights, the plan has {self.n_steps} steps")
+        self._check(lib().daxm_set_step_weights(self._h, w.ctypes.data_as(C.POINTER(C.c_double))))
 
     def set_host_budget(self, device_bytes: int):
         """Cap the device memory reconstruct_host may hold (0 = no cap): above it the host path runs

@@ -30,6 +30,7 @@ constexpr int TILE_E = TILE_C + 1;  // pixel edge columns per tile (finite pixel
 constexpr int NCOEF = 3;            // depth model per edge point: polynomial of degree NCOEF-1 in wire travel
 // fp64 approximation error allowed for the depth model (bins); the fp32 evaluation adds ~ulp(M/2)
 constexpr double MODEL_ERR_MAX = NCOEF >= 4 ? 1e-6 : 2e-5;
+constexpr double ROW_TAU_ERR_MAX = 2e-4;  // row path: max fp32 depth error (bins) incl. its wire travel
 #ifndef DAXM_CPT
 #define DAXM_CPT 4
 #endif
@@ -123,6 +124,7 @@ struct DepositArgs {
     float sign;               // s: +1 leading, -1 trailing (reading R2)
     float dI_floor;           // s dI -> max(s dI, dI_floor): -inf, or 0 in the both-edges mode (R16)
     int acc;                  // 1: add into the output (both-edges mode, second edge) instead of storing
+    const float* w;           // [S] per-step intensity normalisation weights (reading R17), or NULL
     const void* stack;        // band stack [S][rows][C] (plane 0 read for the intensity cutoff)
     const float* table;       // exact depth table (general kernel) or nullptr: per tile at toff[tile],
     const long long* toff;    //   [k - k_lo][TILE_E][TILE_R] fp32 bins relative to m_ref
@@ -254,12 +256,26 @@ struct RowArgs {
     int acc;               // 1: add into the output (both-edges mode, second edge)
     const void* stack;     // band stack (plane 0 read for the intensity cutoff)
     float* out;            // band output [M][rows][C] (the row kernel's plane copy-out)
+    float dth, dtl;        // wire travel per step Delta = t_{S-1} / (S - 1), split hi + lo (row_tau)
     int use_cutoff;
     float cutoff;
     const unsigned char* live;  // [n_rt] per-call row_live_kernel flags (0: zeros written), or NULL
     float* prof_part;      // [n_rt][M] per-tile plane sums (fused depth-profile epilogue), or NULL
     unsigned* err;         // DAXM_ROW_CHECK builds: schedule violations (must stay 0)
 };
+
+#ifndef DAXM_ROW_TAU_LINEAR
+#define DAXM_ROW_TAU_LINEAR 1  // row kernel: wire travel from row_tau (0: a per-warp shared-memory table)
+#endif
+// Wire travel of a row tile's visit v (its step k = k_lo + v, or k_hi - v for dir < 0) relative to
+// the tile's t_ref, in fp32, as the row kernel, its admission replay and the row fit's error check
+// all evaluate it: Af = (float)(t_{k_first} - t_ref), (dh, dl) = dir * (Delta_hi, Delta_lo) with
+// Delta the mean step -- the scan's own travel for uniformly stepped scans; the fit check bounds the
+// depth error of the approximation for any other straight scan (the row path is refused above it).
+__device__ __forceinline__ float row_tau(float Af, float dh, float dl, int v) {
+    const float fv = __int_as_float(0x4B000000 | v) - 8388608.f;  // (float)v, exact for v < 2^23
+    return fmaf(fv, dh, fmaf(fv, dl, Af));
+}
 
 // Corner depth of one pixel edge at fp32 wire travel tau (bins relative to m_ref): the
 // pre-pass ring check and the step-locked kernel evaluate exactly this expression.

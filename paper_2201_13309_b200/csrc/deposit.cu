@@ -670,8 +670,12 @@ __device__ void general_pixel(const DepositArgs& a, int tile, int r, int c, int 
     };
     const T* px = stack + (size_t)jl * a.C + i;
     const float sgn = a.sign * (float)dir;
+    auto Iw = [&](int k) -> float {  // the step's intensity, normalised by its weight (reading R17)
+        const float v = (float)px[(size_t)k * plane];
+        return a.w ? v * a.w[k] : v;
+    };
     auto dI = [&](int q) -> float {
-        return fmaxf(sgn * ((float)px[(size_t)step_of(q) * plane] - (float)px[(size_t)step_of(q + 1) * plane]),
+        return fmaxf(sgn * (Iw(step_of(q)) - Iw(step_of(q + 1))),
                      a.dI_floor);  // both-edges mode: this edge's sign of change only (R16)
     };
     int qc = 0, qo = 0;

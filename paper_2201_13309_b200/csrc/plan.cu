@@ -56,6 +56,9 @@ struct daxm_plan {
     signed char* d_psep = nullptr;
     int* d_vneed = nullptr;     // [n_tiles][n_states + 1] furthest visit index needed (fast kernel)
     bool straight = true;       // wire centres on a line: travel-polynomial depth model possible
+    float dt_h = 0.f, dt_l = 0.f;  // mean wire travel per step, hi + lo (row kernel's tau, row_tau)
+    float* d_w = nullptr;          // per-step normalisation weights (daxm_set_step_weights), or NULL
+    std::vector<double> step_w;    // ... their host copy (for band plans built later)
     float* d_table = nullptr;   // exact per-step depth table (general wire paths / model miss)
     long long* d_toff = nullptr;
     int n_states = 0;
@@ -448,7 +451,8 @@ __global__ void __launch_bounds__(1024) tile_kernel(GeomConst g, const double* _
 // fp32 tau, the kernels' evaluation).
 __device__ void fit_point(const GeomConst& g, const double* __restrict__ t, const double* __restrict__ wire,
                           double t_ref, int k_lo, int k_hi, const double Q[3], double sg, unsigned* flags,
-                          float cf[NCOEF], double& local_err, double& local_model) {
+                          float cf[NCOEF], double& local_err, double& local_model, int lin_dir = 0,
+                          float dth = 0.f, float dtl = 0.f) {
     const double h = 0.5 * (t[k_hi] - t[k_lo]);
     double b[NCOEF];
     for (int m = 0; m < NCOEF; ++m) b[m] = 0.0;
@@ -497,7 +501,10 @@ __device__ void fit_point(const GeomConst& g, const double* __restrict__ t, cons
         const double ex = tangent_u(g, Q, sg, wire + 3 * k);
         if (isnan(ex)) continue;
         const double td = t[k] - t_ref;
-        const double tau = (double)(float)td;
+        // the kernel's fp32 tau: the tile table's rounding, or the row kernel's row_tau
+        const double tau = lin_dir == 0 ? (double)(float)td
+                         : (double)row_tau((float)(t[lin_dir > 0 ? k_lo : k_hi] - t_ref), lin_dir * dth, lin_dir * dtl,
+                                           lin_dir > 0 ? k - k_lo : k_hi - k);
         double pm = b[NCOEF - 1], pp = (double)cf[NCOEF - 1];
         for (int m = NCOEF - 2; m >= 0; --m) {
             pm = b[m] + td * pm;
@@ -591,7 +598,7 @@ __global__ void __launch_bounds__(RW_ROWS * RW_COLS) row_tile_kernel(
 __global__ void __launch_bounds__(RW_ROWS * (RW_COLS + 1)) row_fit_kernel(
     GeomConst g, const double* __restrict__ t, const double* __restrict__ wire, int row_org, int n_rc,
     const RowTile* __restrict__ rts, float* __restrict__ coef, unsigned* __restrict__ flags,
-    double* __restrict__ max_err) {
+    double* __restrict__ max_err, float dth, float dtl) {
     const int rt = blockIdx.x;
     const RowTile ti = rts[rt];
     const int rr = rt / n_rc, rc = rt % n_rc;
@@ -604,7 +611,8 @@ __global__ void __launch_bounds__(RW_ROWS * (RW_COLS + 1)) row_fit_kernel(
     if (ti.k_hi >= ti.k_lo && j < g.R && eg < n_edges) {
         double Q[3];
         edge_point(g, j, eg, Q);
-        fit_point(g, t, wire, ti.t_ref, ti.k_lo, ti.k_hi, Q, edge_sigma(g, Q), flags, cf, local_err, local_model);
+        fit_point(g, t, wire, ti.t_ref, ti.k_lo, ti.k_hi, Q, edge_sigma(g, Q), flags, cf, local_err, local_model,
+                  DAXM_ROW_TAU_LINEAR ? (ti.dir > 0 ? 1 : -1) : 0, dth, dtl);
     }
     for (int m = 0; m < NCOEF; ++m) coef[(((size_t)rt * NCOEF + m) * (RW_COLS + 1) + e) * RW_ROWS + r] = cf[m];
     if (local_err > 0.0) atomic_max_pos_double(max_err, local_err);
@@ -688,6 +696,8 @@ void free_plan_memory(daxm_plan* p) {
     cudaFree(p->d_rlive);
     cudaFree(p->d_prof_part);
     cudaFree(p->d_rcoef);
+    cudaFree(p->d_w);
+    p->d_w = nullptr;
     cudaFree(p->d_rlist);
     cudaFree(p->d_row_err);
     p->d_rt = nullptr;
@@ -767,6 +777,11 @@ daxm_status host_prepare(daxm_plan* p) {
         if (norm3(res) > 1e-6 + 1e-9 * fabs(tk)) p->straight = false;  // general path: exact depth table
         p->t[k] = tk;
     }
+    {
+        const double D = p->t[S - 1] / (double)(S - 1);
+        p->dt_h = (float)D;
+        p->dt_l = (float)(D - (double)p->dt_h);
+    }
     for (int k = 1; k < S && p->straight; ++k)
         if (p->t[k] < p->t[k - 1])
             return fail(nullptr, DAXM_ERR_NONMONOTONE_SCAN, "wire travel decreases between steps %d and %d", k - 1, k);
@@ -831,7 +846,8 @@ daxm_status row_prepass(daxm_plan* p, int) {
                                                                 d_flags);
     CK(cudaGetLastError());
     row_fit_kernel<<<(unsigned)n_rt, dim3(RW_ROWS, RW_COLS + 1)>>>(gc, p->d_t, p->d_wire, p->row_org, p->n_rc,
-                                                                   p->d_rt, p->d_rcoef, d_flags, d_err);
+                                                                   p->d_rt, p->d_rcoef, d_flags, d_err, p->dt_h,
+                                                                   p->dt_l);
     CK(cudaGetLastError());
     std::vector<RowTile> ht(n_rt);
     CK(cudaMemcpy(ht.data(), p->d_rt, sizeof(RowTile) * n_rt, cudaMemcpyDeviceToHost));
@@ -853,7 +869,9 @@ daxm_status row_prepass(daxm_plan* p, int) {
     CK(cudaMemset(p->d_row_err, 0, 64));
     CK(cudaMemcpy(ht.data(), p->d_rt, sizeof(RowTile) * n_rt, cudaMemcpyDeviceToHost));
     // the row path needs the same depth-model tolerance as the deposit tiles' (else: old path)
-    if ((flags & (FLAG_FIT_NAN | FLAG_MIXED_DIR)) || !(ferr[1] <= MODEL_ERR_MAX) || !(ferr[0] <= 1e-3)) return DAXM_OK;
+    // (the fp32 error includes the row kernel's wire travel: non-uniformly stepped scans fail it)
+    if ((flags & (FLAG_FIT_NAN | FLAG_MIXED_DIR)) || !(ferr[1] <= MODEL_ERR_MAX) || !(ferr[0] <= ROW_TAU_ERR_MAX))
+        return DAXM_OK;
     std::vector<int> lists[daxm_plan::N_RCLS];
     p->stats.row_reject_bits = 0;
     for (size_t q = 0; q < n_rt; ++q) {
@@ -1311,6 +1329,7 @@ static DepositArgs make_args(const daxm_plan* p, int dtype) {
     a.sign = p->g.edge == DAXM_EDGE_TRAILING ? -1.f : 1.f;
     a.dI_floor = p->dI_floor;
     a.acc = p->acc;
+    a.w = p->d_w;
     a.stack = nullptr;
     a.table = p->d_table;
     a.toff = p->d_toff;
@@ -1355,6 +1374,8 @@ static RowArgs make_row_args(const daxm_plan* p) {
     a.acc = p->acc;
     a.stack = nullptr;
     a.out = nullptr;
+    a.dth = p->dt_h;
+    a.dtl = p->dt_l;
     a.use_cutoff = p->use_cutoff;
     a.cutoff = p->cutoff;
     a.live = nullptr;
@@ -1540,7 +1561,8 @@ static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float*
         }
         return DAXM_OK;
     }
-    bool fast = fast_possible(p, dt);
+    // (per-step weights: the general kernel normalises each intensity, the fast kernels do not)
+    bool fast = fast_possible(p, dt) && p->d_w == nullptr;
     if (fast && p->row_ok && getenv("DAXM_NO_ROW") == nullptr)
         return run_row(p, d_stack, dt, d_out, st, tr_begin, tr_end < 0 ? -1 : tr_end);
     // both-edges children off the row path: the general kernel alone clamps and accumulates
@@ -1670,6 +1692,7 @@ static daxm_status host_ring(daxm_plan* p, const void* h_stack, daxm_dtype dt, f
                 free_ring(p);
                 return fail(p, s, "band plan [%d, %d): %s", r, r1, g_create_err.c_str());
             }
+            if (!p->step_w.empty()) daxm_set_step_weights(bp, p->step_w.data());
             p->bands.push_back(bp);
             p->band_r0.push_back(r - p->g.row_begin);
             r = r1;
@@ -1750,6 +1773,50 @@ static daxm_status host_ring(daxm_plan* p, const void* h_stack, daxm_dtype dt, f
     }
     p->last_ring_rows = B;
     p->last_ring_bands = nb;
+    return DAXM_OK;
+}
+
+daxm_status daxm_set_step_weights(daxm_plan* p, const double* w) {
+    if (!p) return DAXM_ERR_INVALID_ARGUMENT;
+    p->err.clear();
+    std::vector<float> hw;
+    if (w) {
+        hw.resize(p->S);
+        for (int k = 0; k < p->S; ++k) {
+            if (!(isfinite(w[k]) && w[k] > 0.0))
+                return fail(p, DAXM_ERR_INVALID_ARGUMENT, "step weight %d = %g is not finite and > 0", k, w[k]);
+            hw[k] = (float)w[k];
+        }
+    }
+    for (daxm_plan* c : p->child)
+        if (c) {
+            daxm_status s = daxm_set_step_weights(c, w);
+            if (s != DAXM_OK) return s;
+        }
+    for (daxm_plan* b : p->bands) {
+        daxm_status s = daxm_set_step_weights(b, w);
+        if (s != DAXM_OK) return s;
+    }
+    DeviceGuard guard(p->device);
+    if (!w) {
+        cudaFree(p->d_w);
+        p->d_w = nullptr;
+        p->step_w.clear();
+        return DAXM_OK;
+    }
+    p->step_w.assign(w, w + p->S);
+    if (!p->d_w) {
+        cudaError_t e = cudaMalloc(&p->d_w, sizeof(float) * p->S);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            return fail(p, DAXM_ERR_OUT_OF_MEMORY, "step weights: %s", cudaGetErrorString(e));
+        }
+    }
+    cudaError_t e = cudaMemcpy(p->d_w, hw.data(), sizeof(float) * p->S, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(p, DAXM_ERR_CUDA, "step weights: %s", cudaGetErrorString(e));
+    }
     return DAXM_OK;
 }
 

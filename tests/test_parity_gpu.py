@@ -280,6 +280,32 @@ def test_single_bin_and_two_steps(daxm):
     parity.check(gpu2, oracle.reconstruct(g2, h2), h2, "S=2")
 
 
+@pytest.mark.parametrize("name,dtype,edge", [("C1", "f32", "leading"), ("C2", "u16", "trailing"),
+                                             ("C2", "f32", "both")])
+def test_step_weights(daxm, name, dtype, edge):
+    """Per-step intensity normalisation (reading R17, daxm_set_step_weights): element by element
+    against the oracle with the same weights; tolerance denominators from the normalised images.
+    Switching the weights off returns the fast path's result."""
+    import torch
+    g = synth.geometry(name, edge=edge)
+    host = synth.stack_numpy(synth.make_maps(name), dtype, noise=True)
+    S = host.shape[0]
+    w = np.random.default_rng(17).uniform(0.85, 1.2, S)
+    with daxm.create(g, device=0) as plan:
+        st = torch.from_numpy(host).cuda()
+        plain = plan.reconstruct(st).cpu().numpy()
+        plan.set_step_weights(w)
+        gpu = plan.reconstruct(st).cpu().numpy()
+        plan.set_step_weights(None)
+        again = plan.reconstruct(st).cpu().numpy()
+        assert np.array_equal(again, plain)
+        with pytest.raises(daxm.DaxmError):
+            plan.set_step_weights(np.full(S, -1.0))
+    ref = oracle.reconstruct(dict(g, step_weight=w), host)
+    parity.check(gpu, ref, host.astype(np.float64) * w[:, None, None], f"{name} {edge} step weights")
+    assert np.abs(gpu - plain).max() > 1.0
+
+
 @pytest.mark.parametrize("pixel_model", ["finite", "point"])
 def test_repeated_wire_positions(daxm, pixel_model):
     """Zero-travel pairs: POINT mode gives the degenerate delta (z1 == z4, reading R8)."""
