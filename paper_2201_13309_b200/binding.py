@@ -86,12 +86,15 @@ def lib():
         L.daxm_reconstruct.restype = C.c_int
         L.daxm_reconstruct_host.argtypes = [P, P, C.c_int, P, P]
         L.daxm_reconstruct_host.restype = C.c_int
-        L.daxm_set_step_weights.argtypes = [P, C.POINTER(C.c_double)]
-        L.daxm_set_step_weights.restype = C.c_int
-        L.daxm_set_host_budget.argtypes = [P, C.c_uint64]
-        L.daxm_set_host_budget.restype = C.c_int
-        L.daxm_host_ring_info.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
-        L.daxm_host_ring_info.restype = C.c_int
+        # (newer entry points: a build of an older source, DAXM_LIBRARY experiments, may lack them)
+        if hasattr(L, "daxm_set_step_weights"):
+            L.daxm_set_step_weights.argtypes = [P, C.POINTER(C.c_double)]
+            L.daxm_set_step_weights.restype = C.c_int
+        if hasattr(L, "daxm_set_host_budget"):
+            L.daxm_set_host_budget.argtypes = [P, C.c_uint64]
+            L.daxm_set_host_budget.restype = C.c_int
+            L.daxm_host_ring_info.argtypes = [P, C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
+            L.daxm_host_ring_info.restype = C.c_int
         L.daxm_set_cutoff.argtypes = [P, C.c_int, C.c_double]
         L.daxm_set_cutoff.restype = C.c_int
         L.daxm_select_cutoff.argtypes = [P, P, C.c_int, C.c_double, C.POINTER(C.c_double), P]

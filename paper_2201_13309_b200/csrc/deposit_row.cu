@@ -71,7 +71,7 @@ struct RowSmem {
     static constexpr int OFF_IN = OFF_OUT + OUT_SLOTS * PLANE_B;
     static constexpr int OFF_BAR = OFF_IN + RW_H * IN_HALF;
     static constexpr int OFF_TAU = OFF_BAR + NG * 8;
-    static size_t bytes(int max_nv) { return (size_t)OFF_TAU + 4 * (size_t)(max_nv + 4) + 128; }
+    static size_t bytes(int max_nv) { return (size_t)OFF_TAU + (DAXM_ROW_TAU_LINEAR ? 0 : 4 * (size_t)(max_nv + 4)) + 128; }
 };
 
 __device__ __forceinline__ void sts_zero4(uint32_t addr) {
@@ -303,7 +303,8 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
     float* tau = reinterpret_cast<float*>(smem + L::OFF_TAU);
 
-    for (int q = lane; q < nvt; q += 32) tau[q] = (float)(a.t[dir > 0 ? ti.k_lo + q : ti.k_hi - q] - ti.t_ref);
+    if (!DAXM_ROW_TAU_LINEAR)
+        for (int q = lane; q < nvt; q += 32) tau[q] = (float)(a.t[dir > 0 ? ti.k_lo + q : ti.k_hi - q] - ti.t_ref);
     if (lane == 0) {
         for (int g = 0; g < NG; ++g) mbar_init(&bars[g], 1);
         fence_mbar_init();
@@ -405,6 +406,9 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
     const uint32_t in_lane =
         opaque(sbase + L::OFF_IN + (uint32_t)(hh * L::IN_HALF) + (uint32_t)(2 * (lane & 15)) * (uint32_t)sizeof(T));
     const uint32_t tau_l = opaque(sbase + L::OFF_TAU + 4u * (uint32_t)vmin_h);
+    // (DAXM_ROW_TAU_LINEAR) wire travel of a visit: row_tau, the fit check bounds its depth error
+    const float tAf = (float)(a.t[dir > 0 ? ti.k_lo : ti.k_hi] - ti.t_ref);
+    const float tdh = dir > 0 ? a.dth : -a.dth, tdl = dir > 0 ? a.dtl : -a.dtl;
     const uint32_t ob = sbase + L::OFF_OUT + (uint32_t)(32 * hh + 2 * (lane & 15)) * 4u;  // column 2i of a plane
     const uint32_t ob0 = opaque(ob + 4u * (uint32_t)hh), ob1 = opaque(ob + 4u * (uint32_t)(hh ^ 1));  // pair 0 / 1
     // pair p's column is the (p ^ h)-th half-word of the lane's 32-bit input word
@@ -421,7 +425,10 @@ __global__ void __launch_bounds__(32, GEN ? 8 : DAXM_RW_MINB) deposit_row(const 
 
     // wire travel and the two pairs' intensities (rows 0, 1) at visit v of the lane's half
     auto fetch = [&](int v, float& t, float2 I[2]) {
-        t = lds_f32(tau_l + 4u * (uint32_t)v);
+        if (DAXM_ROW_TAU_LINEAR)
+            t = row_tau(tAf, tdh, tdl, vmin_h + v);
+        else
+            t = lds_f32(tau_l + 4u * (uint32_t)v);
         const uint32_t ad = in_lane + ((uint32_t)(v ^ xr_) % (uint32_t)NB) * (uint32_t)L::IN_SLOT;
         if constexpr (sizeof(T) == 2) {
             // u16 -> fp32 exactly: 0x4B00'xxxx is 2^23 + x, one PRMT builds it from the lane's
@@ -879,9 +886,12 @@ __global__ void __launch_bounds__(32) row_admit_kernel(RowArgs a, RowTile* __res
             }
         int vmin_h, vs, ve, vs_max, vend;
         row_starts(wk, lane, vmin_h, vs, ve, vs_max, vend);
-        auto tau_of = [&](int v) {  // v relative to the half's vmin, exactly as the kernel's table
+        const float tAf = (float)(a.t[ti.dir > 0 ? ti.k_lo : ti.k_hi] - ti.t_ref);
+        const float tdh = ti.dir > 0 ? a.dth : -a.dth, tdl = ti.dir > 0 ? a.dtl : -a.dtl;
+        auto tau_of = [&](int v) {  // v relative to the half's vmin, exactly as the kernel
             const int vv = vmin_h + v;
-            return (float)(a.t[ti.dir > 0 ? ti.k_lo + vv : ti.k_hi - vv] - ti.t_ref);
+            return DAXM_ROW_TAU_LINEAR ? row_tau(tAf, tdh, tdl, vv)
+                                       : (float)(a.t[ti.dir > 0 ? ti.k_lo + vv : ti.k_hi - vv] - ti.t_ref);
         };
         auto point = [&](int p, int r, int v, float& lo, float& hi) {  // walks with a window only
             const float t = tau_of(v);
@@ -1070,7 +1080,8 @@ cudaError_t set_attr_one() {
 }
 
 template <typename T, bool POINT, int RB, int V, bool CLAMP, int KTS>
-cudaError_t launch_cl(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, cudaStream_t st) {
+cudaError_t launch_cl(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
+                      cudaStream_t st) {
     using K = RowVariant<T, POINT, RB, V, CLAMP, KTS>;
     static const size_t extra = getenv("DAXM_ROW_EXTRA_SMEM") ? (size_t)atol(getenv("DAXM_ROW_EXTRA_SMEM")) : 0;
     K::kernel<<<(unsigned)a.n_list, 32, K::Smem::bytes(a.max_nv) + extra, st>>>(*in_map, *out_map, a);
@@ -1078,14 +1089,15 @@ cudaError_t launch_cl(const RowArgs& a, const CUtensorMap* in_map, const CUtenso
 }
 
 template <typename T, bool POINT, int RB, int V, int KTS = RW_KT>
-cudaError_t launch_one(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, cudaStream_t st) {
+cudaError_t launch_one(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
+                       cudaStream_t st) {
     return a.dI_floor > -INFINITY ? launch_cl<T, POINT, RB, V, true, KTS>(a, in_map, out_map, st)
                                   : launch_cl<T, POINT, RB, V, false, KTS>(a, in_map, out_map, st);
 }
 
 template <typename T, int RB, int V>
-cudaError_t launch_kt(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int ktc,
-                      cudaStream_t st) {  // separated variants: edge-trip class
+cudaError_t launch_kt(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
+                      int ktc, cudaStream_t st) {  // separated variants: edge-trip class
     switch (ktc) {
         case 0: return launch_one<T, false, RB, V, 3>(a, in_map, out_map, st);
         case 1: return launch_one<T, false, RB, V, 4>(a, in_map, out_map, st);
@@ -1094,8 +1106,8 @@ cudaError_t launch_kt(const RowArgs& a, const CUtensorMap* in_map, const CUtenso
 }
 
 template <typename T, int RB>
-cudaError_t launch_rb(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map, int variant, int ktc,
-                      cudaStream_t st) {
+cudaError_t launch_rb(const RowArgs& a, const CUtensorMap* in_map, const CUtensorMap* out_map,
+                      int variant, int ktc, cudaStream_t st) {
     if (a.point_mode)
         return variant == 3 ? launch_one<T, true, RB, 3>(a, in_map, out_map, st)
                             : launch_one<T, true, RB, 0>(a, in_map, out_map, st);
