@@ -195,33 +195,53 @@ __device__ __forceinline__ void atomic_max_pos_double(double* addr, double v) {
 }
 
 // ------------------------------------------------------------ pixel windows
-__global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire, int pre_row0, int pre_rows,
-                                    int band_r0, int band_r1, int2* __restrict__ win,
-                                    signed char* __restrict__ pdir, signed char* __restrict__ psep,
-                                    unsigned* __restrict__ flags, unsigned long long* __restrict__ counters) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int jl = blockIdx.y * blockDim.y + threadIdx.y;
-    if (i >= g.C || jl >= pre_rows) return;
+// One warp per PW_PIX = 31 consecutive pixels of one row: lane l evaluates pixel edge point
+// base + l (finite pixels: column base + l - 1/2; POINT: the pixel centre) at every wire step and
+// pixel base + l (l < 31) takes its front edge from lane l + 1 (warp shuffle), so every edge point's
+// tangent depth is computed once instead of twice.
+constexpr int PW_PIX = 31;
+__global__ void __launch_bounds__(128) pixel_window_kernel(GeomConst g, const double* __restrict__ wire, int pre_row0,
+                                                           int pre_rows, int band_r0, int band_r1,
+                                                           int2* __restrict__ win, signed char* __restrict__ pdir,
+                                                           signed char* __restrict__ psep, unsigned* __restrict__ flags,
+                                                           unsigned long long* __restrict__ counters) {
+    const int lane = threadIdx.x & 31;
+    const int wrow = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);  // warp index within the row
+    const int jl = blockIdx.y;
+    const int base = wrow * PW_PIX;
+    if (base >= g.C || jl >= pre_rows) return;  // (warp-uniform)
     const int j = pre_row0 + jl;
+    const int i = base + lane;  // this lane's pixel (lane < PW_PIX)
+    const bool pix = lane < PW_PIX && i < g.C;
     if (j < band_r0 || j >= band_r1) {  // rows of a boundary tile outside the band: never output
-        win[(size_t)jl * g.C + i] = make_int2(0, 0);
-        pdir[(size_t)jl * g.C + i] = 0;
-        psep[(size_t)jl * g.C + i] = 3;
+        if (pix) {
+            win[(size_t)jl * g.C + i] = make_int2(0, 0);
+            pdir[(size_t)jl * g.C + i] = 0;
+            psep[(size_t)jl * g.C + i] = 3;
+        }
         return;
     }
-    double Qb[3], Qf[3];
-    edge_point(g, j, i, Qb);
-    edge_point(g, j, g.point_mode ? i : i + 1, Qf);
-    const double sb = edge_sigma(g, Qb), sf = edge_sigma(g, Qf);
+    const int n_edges = g.point_mode ? g.C : g.C + 1;
+    double Q[3];
+    edge_point(g, j, min(i, n_edges - 1), Q);  // lane's edge point (lanes past the last edge: a copy)
+    const double sg = edge_sigma(g, Q);
     const double upper = (double)(g.M - g.m_ref), lower = (double)(-g.m_ref);
+    // back edge = this lane's point, front edge = the next lane's (POINT: the same point)
+    auto depths = [&](int k, double& ub, double& uf) {
+        ub = tangent_u(g, Q, sg, wire + 3 * k);
+        const double nx = __shfl_down_sync(0xffffffffu, ub, 1);
+        uf = g.point_mode ? ub : nx;
+    };
 
     // pass 1: relevant pairs (trapezoid overlaps (0, M) bins), NaN bookkeeping
-    double ub0 = tangent_u(g, Qb, sb, wire), uf0 = tangent_u(g, Qf, sf, wire);
+    double ub0, uf0;
+    depths(0, ub0, uf0);
     int first = -1, last = -1;
     bool prev_nan = false, first_prev_nan = false, pending_nan = false, next_nan = false, nan_inside = false;
     bool any_valid = false;
     for (int k = 0; k + 1 < g.S; ++k) {
-        double ub1 = tangent_u(g, Qb, sb, wire + 3 * (k + 1)), uf1 = tangent_u(g, Qf, sf, wire + 3 * (k + 1));
+        double ub1, uf1;
+        depths(k + 1, ub1, uf1);
         bool isn = isnan(ub0) || isnan(uf0) || isnan(ub1) || isnan(uf1);
         if (last >= 0 && k == last + 1) next_nan = isn;
         any_valid |= !isn;
@@ -244,25 +264,30 @@ __global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire
     }
     int2 w = make_int2(0, 0);
     signed char dir = 0, sep = 3;
-    if (any_valid) atomicAdd(&counters[4], 1ull);  // a pixel with every pair NaN is invalid (reading R8)
-    if (first >= 0) {
+    if (pix && any_valid) atomicAdd(&counters[4], 1ull);  // a pixel with every pair NaN is invalid (reading R8)
+    int kb = INT_MAX, ke = -1;  // window points kb..ke (pairs [kb, ke))
+    if (pix && first >= 0) {
         // NaN pairs inside the window (the pixel edge inside the wire cylinder at some step): the
         // pairs are skipped (reading R8) by the exact-table general kernel the host then selects
         if (nan_inside) atomicOr(flags, FLAG_NAN_IN_WINDOW);
         atomicAdd(&counters[2], (unsigned long long)(last - first + 1));
         atomicAdd(&counters[3], 1ull);
-        int kb = first, ke = last + 1;  // pairs [kb, ke)
-        if (kb > 0 && !first_prev_nan) --kb;             // one guard pair each side (fp32 rounding)
+        kb = first;
+        ke = last + 1;
+        if (kb > 0 && !first_prev_nan) --kb;  // one guard pair each side (fp32 rounding)
         if (ke <= g.S - 2 && !next_nan) ++ke;
-        // pass 2: monotonicity and direction over the window's points kb..ke, and
-        // "separation": consecutive points' edge spans [lo, hi] are disjoint (by a
-        // 1e-3-bin margin) and every trapezoid has area >= 1e-3 bins, in either
-        // visiting order -- the condition for the fast deposit kernel's
-        // piecewise-linear form.
-        bool pos = false, neg = false, sep_pos = true, sep_neg = true, ovl_pos = true, ovl_neg = true;
-        double pb = tangent_u(g, Qb, sb, wire + 3 * kb), pf = tangent_u(g, Qf, sf, wire + 3 * kb);
-        for (int k = kb + 1; k <= ke; ++k) {
-            double cb = tangent_u(g, Qb, sb, wire + 3 * k), cf = tangent_u(g, Qf, sf, wire + 3 * k);
+    }
+    // pass 2: monotonicity and direction over each window's points kb..ke, and "separation":
+    // consecutive points' edge spans [lo, hi] are disjoint (by a 1e-3-bin margin) and every trapezoid
+    // has area >= 1e-3 bins, in either visiting order -- the condition for the fast deposit kernel's
+    // piecewise-linear form.  The warp walks the union of its windows.
+    const int KB = __reduce_min_sync(0xffffffffu, kb), KE = __reduce_max_sync(0xffffffffu, ke);
+    bool pos = false, neg = false, sep_pos = true, sep_neg = true, ovl_pos = true, ovl_neg = true;
+    double pb = 0.0, pf = 0.0;
+    for (int k = KB; k <= KE; ++k) {
+        double cb, cf;
+        depths(k, cb, cf);
+        if (k > kb && k <= ke) {
             double db = cb - pb, df = cf - pf;
             pos |= (db > 0.0) || (df > 0.0);
             neg |= (db < 0.0) || (df < 0.0);
@@ -276,18 +301,22 @@ __global__ void pixel_window_kernel(GeomConst g, const double* __restrict__ wire
                        (0.5 * (hi1 + fmax(hi0, lo1) - fmin(hi0, lo1) - lo0) >= 1e-3);
             ovl_neg &= (fmin(hi1, lo0) >= lo1 + 1e-3) && (hi0 >= fmax(hi1, lo0) + 1e-3) &&
                        (0.5 * (hi0 + fmax(hi1, lo0) - fmin(hi1, lo0) - lo1) >= 1e-3);
-            pb = cb;
-            pf = cf;
         }
+        pb = cb;
+        pf = cf;
+    }
+    if (pix && ke >= 0) {
         if (pos && neg) atomicOr(flags, FLAG_NONMONOTONE);
         dir = neg ? -1 : 1;
         // bit 0: separated (single zone walk), bit 1: dual walk applicable
         sep = ((dir > 0 ? sep_pos : sep_neg) ? 1 : 0) | ((dir > 0 ? ovl_pos : ovl_neg) ? 2 : 0);
         w = make_int2(kb, ke);
     }
-    win[(size_t)jl * g.C + i] = w;
-    pdir[(size_t)jl * g.C + i] = dir;
-    psep[(size_t)jl * g.C + i] = sep;
+    if (pix) {
+        win[(size_t)jl * g.C + i] = w;
+        pdir[(size_t)jl * g.C + i] = dir;
+        psep[(size_t)jl * g.C + i] = sep;
+    }
 }
 
 // ------------------------------------------------------------ tiles
@@ -960,7 +989,8 @@ daxm_status device_prepass(daxm_plan* p) {
     CK(cudaEventCreate(&e1));
     CK(cudaEventRecord(e0, 0));
     {
-        dim3 blk(128, 1), grd((g.n_cols + 127) / 128, p->pre_rows);
+        const int warps_per_row = (g.n_cols + PW_PIX - 1) / PW_PIX;
+        dim3 blk(128, 1), grd((warps_per_row + 3) / 4, p->pre_rows);
         pixel_window_kernel<<<grd, blk>>>(gc, p->d_wire, p->pre_row0, p->pre_rows, g.row_begin, g.row_end,
                                           p->d_win, p->d_pdir, p->d_psep, d_flags, d_cnt);
         CK(cudaGetLastError());
