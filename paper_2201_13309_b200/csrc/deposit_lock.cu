@@ -151,8 +151,10 @@ __device__ __forceinline__ void stg128_cs_if(bool ok, float* p, float4 v) {  // 
                  : "memory");
 }
 
-template <typename T, bool POINT, int RB>
-__global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
+// The step-locked kernels share everything but the zone arithmetic: OV = false, separated spans
+// (one zone quadratic per walk); OV = true, overlapping spans (ramp superposition).
+template <typename T, bool POINT, int RB, bool OV>
+__global__ void __launch_bounds__(LK_THREADS, OV ? 2 : DAXM_LOCK_MINB)
     deposit_lock(const __grid_constant__ CUtensorMap in_map, float* __restrict__ out, const DepositArgs a) {
     using L = LockSmem<T, RB>;
     extern __shared__ unsigned char smem_raw[];
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
     const int tile = a.tr_begin * a.n_tc + (int)blockIdx.x / LOCK_SUBS;
     const int sub = (int)blockIdx.x % LOCK_SUBS;
     const TileInfo ti = a.tiles[tile];
-    if ((ti.lock & LOCK_CLASS_MASK) != RB) return;
+    if ((ti.lock & LOCK_CLASS_MASK) != (OV ? (RB | LOCK_OVB) : RB)) return;
     if (a.tile_live && !a.tile_live[tile]) return;  // cutoff: zero_dead_tiles writes this tile
     const int tr = tile / a.n_tc, tc = tile % a.n_tc;
     const int row0 = (a.tr0 + tr) * TILE_R;  // global row of tile row 0 (>= row_begin: pre-pass)
@@ -334,466 +336,280 @@ __global__ void __launch_bounds__(LK_THREADS, DAXM_LOCK_MINB)
         };
 
         wait_upto(vmin0 + 1);
-        float2 plo[2], phi[2], ps[2], pI[2], cq[2], zF[2], Fp[2], En[2], Iq[2];
-        float tq;
-        {
-            float t0;
-            fetch(0, t0, pI);
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                plo[p] = poly2(cb[p], f2(t0));  // lo edge / hi edge: fixed order over the tile (pre-pass)
-                phi[p] = POINT ? plo[p] : poly2(cf[p], f2(t0));
-                ps[p] = add2(plo[p], phi[p]);
-                cq[p] = zF[p] = Fp[p] = f2(0.f);
-                // first edge: the first above point 0's lo (F = 0 below it); inactive walks never evaluate
-                En[p].x = act[2 * p] ? fmaxf(E0, floorf(plo[p].x) + 1.f) : EM + 1.f;
-                En[p].y = act[2 * p + 1] ? fmaxf(E0, floorf(plo[p].y) + 1.f) : EM + 1.f;
-            }
-            fetch(1, tq, Iq);
-        }
-        const float2 sdir2 = f2(2.f * a.sign * (float)dir);  // c = 2 s dir dI / (sum_{q+1} - sum_q)
-        const int m_ref = a.m_ref;
-        // bits(E + fbias) = 0x4B000000 + e - 1 + RB for edge index e: plane e - 1 mod RB in the low bits
-        const float fbias = 8388608.f + (float)(m_ref - 1 + RB);
-        // planes below the slowest walk's next edge are final; a finished or inactive walk sits at
-        // edge M + 1 (its last point lies above the bins: pre-pass), so it never holds them back
-        auto frontier = [&]() {
-            const float fr = fminf(fminf(En[0].x, En[0].y), fminf(En[1].x, En[1].y));
-            return __reduce_min_sync(0xffffffffu, (int)fr + m_ref) - 1;  // planes < edge - 1
-        };
-        drain(frontier());
-#if DAXM_LOCK_CHECK
-        unsigned viol = 0u;
-#endif
-
-        // iteration jj closes zone jj - 1 of every walk; before its own window a walk's zones lie
-        // below the bins (F offset only), after it above them (no edge left: pre-pass)
-        DAXM_UNROLL(DAXM_LOCK_UNROLL)
-        for (int jj = 1; jj < niter; ++jj) {
-            // point jj (prefetched); refill the ring below the slowest walk; prefetch point jj + 1
-            issue(jj);
-            wait_upto(vmin0 + jj + 1);
-            float2 zlo[2], zw[2], zc[2], zd[2], zg[2], zF0[2], Eb[2];
-            float tn;
-            float2 In[2];
-            fetch(jj + 1, tn, In);
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                // past its window a walk re-reads its last point (lo >= EM, pre-pass): no edges
-                // remain below EM for it, whatever its zone arithmetic produces
-                const float2 lo = poly2(cb[p], f2(tq)), hi = POINT ? lo : poly2(cf[p], f2(tq));
-                const float2 s = add2(lo, hi);
-                const float2 c = mul2(mul2(sdir2, sub2(pI[p], Iq[p])), rcp2(sub2(s, ps[p])));
-                const float2 w = sub2(phi[p], plo[p]);
-                const float2 d = sub2(cq[p], c);
-                const float2 rw = rcp2(max2(w, f2(1e-30f)));
-                zlo[p] = plo[p];
-                zw[p] = w;
-                zc[p] = c;
-                zd[p] = d;
-                zg[p] = mul2(d, mul2(rw, f2(-0.5f)));
-                zF0[p] = zF[p];
-                Eb[p] = min2(lo, f2(EM));
-                // F at the next zone's start: F(lo) = F(plo) + c (lo - plo) + w d / 2
-                zF[p] = fma2(f2(0.5f), mul2(w, d), fma2(c, sub2(lo, plo[p]), zF[p]));
-                plo[p] = lo;
-                phi[p] = hi;
-                ps[p] = s;
-                pI[p] = Iq[p];
-                cq[p] = c;
-                Iq[p] = In[p];
-            }
-            tq = tn;
-            // ---- edges of zone jj - 1: En .. floor(min(lo_jj, EM)), a warp-uniform trip count
-            uint32_t es[4];
-            float2 x[2], cm[2], fl[2];
-            float kmax = 0.f;
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                es[2 * p] = (uint32_t)__float_as_int(En[p].x + fbias) << 9;  // plane * plane bytes (mod RB)
-                es[2 * p + 1] = (uint32_t)__float_as_int(En[p].y + fbias) << 9;
-                fl[p] = add2(make_float2(floorf(Eb[p].x), floorf(Eb[p].y)), f2(1.f));  // first edge after the zone
-                const float2 cnt = sub2(fl[p], En[p]);  // edges of this zone (exact small integers)
-                kmax = fmaxf(kmax, fmaxf(cnt.x, cnt.y));
-                cm[p] = sub2(cnt, f2(1.f));  // trip k stores iff k <= cnt - 1
-                x[p] = sub2(En[p], zlo[p]);   // advanced by +1 per trip (the edge test is on k, exact)
-            }
-            const int K = __reduce_max_sync(0xffffffffu, (int)kmax);
-            float kf = 0.f;
-            DAXM_UNROLL(DAXM_LOCK_KUNROLL)
-            for (int k = 0; k < K; ++k, kf += 1.f) {
-#pragma unroll
+        if constexpr (!OV) {
+            float2 plo[2], phi[2], ps[2], pI[2], cq[2], zF[2], Fp[2], En[2], Iq[2];
+            float tq;
+            {
+                float t0;
+                fetch(0, t0, pI);
+    #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    const float2 xc = min2(x[p], zw[p]);
-                    const float2 F = fma2(xc, fma2(zg[p], xc, zd[p]), fma2(zc[p], x[p], zF0[p]));
-                    const float2 o = sub2(F, Fp[p]);
-                    // predicated store + Fp update (setp inside the asm: no branch, no address remat)
-                    edge_store(out_lane + (es[2 * p] & (uint32_t)((RB - 1) << 9)) + (2 * p) * 128, o.x, F.x, kf,
-                               cm[p].x, Fp[p].x);
-                    edge_store(out_lane + (es[2 * p + 1] & (uint32_t)((RB - 1) << 9)) + (2 * p + 1) * 128, o.y, F.y,
-                               kf, cm[p].y, Fp[p].y);
-                    x[p] = add2(x[p], f2(1.f));
-                    es[2 * p] += 512u;
-                    es[2 * p + 1] += 512u;
+                    plo[p] = poly2(cb[p], f2(t0));  // lo edge / hi edge: fixed order over the tile (pre-pass)
+                    phi[p] = POINT ? plo[p] : poly2(cf[p], f2(t0));
+                    ps[p] = add2(plo[p], phi[p]);
+                    cq[p] = zF[p] = Fp[p] = f2(0.f);
+                    // first edge: the first above point 0's lo (F = 0 below it); inactive walks never evaluate
+                    En[p].x = act[2 * p] ? fmaxf(E0, floorf(plo[p].x) + 1.f) : EM + 1.f;
+                    En[p].y = act[2 * p + 1] ? fmaxf(E0, floorf(plo[p].y) + 1.f) : EM + 1.f;
                 }
+                fetch(1, tq, Iq);
             }
-            // next edge of each walk (edges <= Eb evaluated or, past the window, constant)
-#pragma unroll
-            for (int p = 0; p < 2; ++p) En[p] = max2(En[p], fl[p]);
-#if DAXM_LOCK_CHECK
-            {   // planes written this iteration must lie below done_p + RB (pre-pass guarantee)
-                const float lim = (float)(done_p + RB - m_ref + 1);  // edge bound: e - 1 < done_p + RB
-#pragma unroll
-                for (int p = 0; p < 2; ++p) {
-                    if (cm[p].x >= 0.f && En[p].x - 1.f >= lim) viol = 1u;  // highest edge stored this iteration
-                    if (cm[p].y >= 0.f && En[p].y - 1.f >= lim) viol = 1u;
-                }
-            }
-#endif
+            const float2 sdir2 = f2(2.f * a.sign * (float)dir);  // c = 2 s dir dI / (sum_{q+1} - sum_q)
+            const int m_ref = a.m_ref;
+            // bits(E + fbias) = 0x4B000000 + e - 1 + RB for edge index e: plane e - 1 mod RB in the low bits
+            const float fbias = 8388608.f + (float)(m_ref - 1 + RB);
+            // planes below the slowest walk's next edge are final; a finished or inactive walk sits at
+            // edge M + 1 (its last point lies above the bins: pre-pass), so it never holds them back
+            auto frontier = [&]() {
+                const float fr = fminf(fminf(En[0].x, En[0].y), fminf(En[1].x, En[1].y));
+                return __reduce_min_sync(0xffffffffu, (int)fr + m_ref) - 1;  // planes < edge - 1
+            };
             drain(frontier());
-        }
-#if DAXM_LOCK_CHECK
-        if (viol && a.lock_err) atomicAdd(a.lock_err, 1u);
-#endif
-    }
-    drain(M);
-    // every issued input load has been waited for (wait_upto reached vend), so the CTA may exit
-}
+    #if DAXM_LOCK_CHECK
+            unsigned viol = 0u;
+    #endif
 
-template <typename T, bool POINT, int RB>
-__global__ void __launch_bounds__(LK_THREADS, 2)
-    deposit_lock_ov(const __grid_constant__ CUtensorMap in_map, float* __restrict__ out, const DepositArgs a) {
-    using L = LockSmem<T, RB>;
-    extern __shared__ unsigned char smem_raw[];
-    const uint32_t sbase = (smem_u32(smem_raw) + 127u) & ~127u;
-    unsigned char* smem = smem_raw + (sbase - smem_u32(smem_raw));
-
-    const int tile = a.tr_begin * a.n_tc + (int)blockIdx.x / LOCK_SUBS;
-    const int sub = (int)blockIdx.x % LOCK_SUBS;
-    const TileInfo ti = a.tiles[tile];
-    if ((ti.lock & LOCK_CLASS_MASK) != (RB | LOCK_OVB)) return;
-    if (a.tile_live && !a.tile_live[tile]) return;  // cutoff: zero_dead_tiles writes this tile
-    const int tr = tile / a.n_tc, tc = tile % a.n_tc;
-    const int row0 = (a.tr0 + tr) * TILE_R;  // global row of tile row 0 (>= row_begin: pre-pass)
-    const int col0 = tc * TILE_C;
-    const int nv = ti.k_hi >= ti.k_lo ? ti.k_hi - ti.k_lo + 1 : 0;
-    const int dir = ti.dir;
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int col = lane & 7, rg = lane >> 3;
-    const int wrow = (sub * LOCK_WARPS + warp) * LOCK_ROWS;  // warp's first row in the tile
-    const uint32_t s_out = sbase + L::OFF_OUT + warp * L::OUT_BYTES;
-    const uint32_t s_in = sbase + L::OFF_IN + warp * L::IN_BYTES;
-    const uint32_t s_bar = sbase + L::OFF_BAR + warp * LOCK_NB * 8;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR) + warp * LOCK_NB;
-    float* tau = reinterpret_cast<float*>(smem + L::OFF_TAU);
-    const uint32_t s_tau = sbase + L::OFF_TAU;
-
-    for (int v = threadIdx.x; v < nv; v += blockDim.x) {
-        const int k = dir > 0 ? ti.k_lo + v : ti.k_hi - v;
-        tau[v] = (float)(a.t[k] - ti.t_ref);
-    }
-    if (lane == 0) {
-        for (int s = 0; s < LOCK_NG; ++s) mbar_init(&bars[s], 1);
-        fence_mbar_init();
-    }
-    // zero the output ring: RB planes x 512 B, 16 B per lane per plane
-    const uint32_t s_copy = s_out + (uint32_t)lane * 16u;
-#pragma unroll
-    for (int s = 0; s < RB; ++s) sts_zero4(s_copy + s * LK_PLANE);
-    __syncthreads();
-    // a group without a pixel above the cutoff is written by zero_dead_tiles: its warp is done
-    if (a.grp_live && !a.grp_live[tile * NG16 + wrow / LOCK_ROWS]) return;
-
-    // ---- walks: rows wrow + 4w + rg, column col
-    const int i = col0 + col;
-    float cbs[4][3], cfs[4][3];
-    bool act[4];
-    int vmin0 = INT_MAX, vend = INT_MIN;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-        const int r = wrow + 4 * w + rg;
-        const int j = row0 + r;
-        bool on = true;
-        if (a.use_cutoff && j < a.row_end && i < a.C) {  // intensity cutoff (f1, reading R14)
-            const T* s0 = static_cast<const T*>(a.stack) + (size_t)(j - a.row_begin) * a.C + i;
-            on = (float)s0[0] >= a.cutoff;
-        }
-        // the warp's visit range comes from the geometry windows alone, so an active walk's
-        // arithmetic (hence its output, bit for bit) does not depend on which others are active
-        const LockWalk lw = lock_walk(a, ti, j, i, true);
-        act[w] = on && lw.npts > 0;
-        if (ti.lock & LOCK_FRONT_LO)  // the front edge is the shallower one over the whole tile (pre-pass)
-            lock_coef(a, tile, r, col, POINT, cfs[w], cbs[w]);
-        else
-            lock_coef(a, tile, r, col, POINT, cbs[w], cfs[w]);
-        if (lw.npts > 0) {
-            vmin0 = min(vmin0, lw.v0);
-            vend = max(vend, lw.v0 + lw.npts - 1);
-        }
-    }
-    vmin0 = __reduce_min_sync(0xffffffffu, vmin0);
-    vend = __reduce_max_sync(0xffffffffu, vend);
-    // warp-locked walks: every walk visits vmin0 + jj at iteration jj (0 <= jj < niter)
-    const bool any_act = __any_sync(0xffffffffu, act[0] || act[1] || act[2] || act[3]);
-    const int niter = any_act && vend >= vmin0 ? vend - vmin0 + 1 : 0;
-
-    const int rows_band = a.row_end - a.row_begin;
-    const int row_local = row0 - a.row_begin + wrow;  // input / output row of the warp's first row
-    const float E0 = (float)(-a.m_ref), EM = (float)(a.M - a.m_ref);
-    const int M = a.M;
-
-    // ---- output ring: plane P in slot P mod RB (edge e completes plane e - 1; "plane -1" of
-    // edge 0 is scratch).  Planes [-1, done_p) are copied out and their slots zeroed; walks may
-    // write planes < done_p + RB.  Copy-out: lane l moves row l/2, columns 4(l%2)..+3 of a plane
-    // (LDS.128 -> st.global.cs.v4: every 32-byte output sector is written whole by one instruction).
-    const size_t plane_stride = (size_t)rows_band * a.C;
-    const int crow = row_local + (lane >> 1);
-    const bool c_ok = crow < rows_band && col0 + (lane & 1) * 4 < a.C;
-    float* const gout = out + (size_t)(c_ok ? crow : 0) * a.C + col0 + (lane & 1) * 4;
-    int done_p = -1;
-    float* gp = gout;  // output row chunk of plane done_p (>= 0)
-    auto drain = [&](int upto) {  // warp-uniform: copy out and recycle planes [done_p, min(upto, M))
-        upto = min(upto, M);
-        if (done_p >= upto) return;
-        __syncwarp();
-        if (done_p < 0) {  // scratch slot of edge 0: every walk is past it
-            sts_zero4(s_copy + (uint32_t)(RB - 1) * LK_PLANE);
-            done_p = 0;
-        }
-        auto slot = [&](int p) { return s_copy + (uint32_t)(p & (RB - 1)) * LK_PLANE; };
-#pragma unroll 1
-        for (; DAXM_LOCK_DRAIN2 && done_p + 1 < upto; done_p += 2) {  // two planes per trip: both loads in flight
-            const float4 va = lds128(slot(done_p)), vb = lds128(slot(done_p + 1));
-            sts_zero4(slot(done_p));
-            sts_zero4(slot(done_p + 1));
-            stg128_cs_if(c_ok, gp, va);
-            stg128_cs_if(c_ok, gp + plane_stride, vb);
-            gp += 2 * plane_stride;
-        }
-#pragma unroll 1
-        for (; done_p < upto; ++done_p) {
-            const float4 v = lds128(slot(done_p));
-            sts_zero4(slot(done_p));
-            stg128_cs_if(c_ok, gp, v);
-            gp += plane_stride;
-        }
-        __syncwarp();
-    };
-
-    if (niter > 0) {
-        // ---- input ring: visit v (relative r = v - vmin0) in slot r % NB, parity (r / NB) & 1.
-        // Loads are issued in groups of >= 4 and waited for in groups (warp-uniform bookkeeping).
-        // Visits vmin0 + 4g .. + 3 form group g: one TMA box of LOCK_G consecutive wire steps
-        // (ascending k, so for dir < 0 a group's visits land in reverse slot order: slot =
-        // ((v - vmin0) ^ xr) mod NB) completing mbarrier g mod NG.  Group g reuses the slots of
-        // group g - NG, free once every walk has read past it: at iteration jj the walks have
-        // consumed the visits below vmin0 + jj, so groups up to (jj + NB - G) / G may be in
-        // flight; the prefetch needs visit vmin0 + jj + 1.
-        const int xr = dir > 0 ? 0 : LOCK_G - 1;
-        const int ngroups = (vend - vmin0) / LOCK_G + 1;
-        const int kbase = dir > 0 ? ti.k_lo + vmin0 : ti.k_hi - vmin0 - (LOCK_G - 1);
-        int g_issue = 0, g_wait = 0;  // next group to load / to wait for
-        auto issue = [&](int jj) {    // groups the ring can hold at iteration jj
-            const int lim = min((jj + LOCK_NB - LOCK_G) / LOCK_G, ngroups - 1);
-            if (g_issue > lim) return;
-            if (lane == 0) {
-                for (int g = g_issue; g <= lim; ++g) {
-                    const int b = g & (LOCK_NG - 1);
-                    mbar_arrive_expect_tx(&bars[b], L::IN_GROUP);
-                    tma_load_3d(smem + (s_in - sbase) + b * L::IN_GROUP, &in_map, col0, row_local,
-                                dir > 0 ? kbase + g * LOCK_G : kbase - g * LOCK_G, &bars[b]);
-                }
-            }
-            g_issue = lim + 1;
-        };
-        auto wait_upto = [&](int v) {  // every group up to visit v's (clamped to the last) has landed
-            const int g_need = (min(v, vend) - vmin0) / LOCK_G;
-            if (g_wait > g_need) return;
-            for (; g_wait <= g_need; ++g_wait) {  // compiler-visible retry loop: the warp reconverges after it
-                while (!mbar_try(s_bar + (uint32_t)(g_wait & (LOCK_NG - 1)) * 8u, (uint32_t)(g_wait / LOCK_NG) & 1u)) {
-                }
-            }
-            __syncwarp();
-        };
-        issue(0);
-
-        // per-lane addresses
-        const uint32_t in_lane = s_in + (uint32_t)(rg * TILE_C + col) * (uint32_t)sizeof(T);  // + w * 4 rows
-        const uint32_t out_lane = s_out + (uint32_t)(rg * TILE_C + col) * 4u;                 // + w * 128
-
-        // ---- walk state, packed by walk pairs (0,1), (2,3)
-        float2 cb[2][3], cf[2][3];
-#pragma unroll
-        for (int p = 0; p < 2; ++p)
-#pragma unroll
-            for (int m = 0; m < 3; ++m) {
-                cb[p][m] = make_float2(cbs[2 * p][m], cbs[2 * p + 1][m]);
-                cf[p][m] = make_float2(cfs[2 * p][m], cfs[2 * p + 1][m]);
-            }
-        // wire travel (warp-uniform) and the 4 walks' intensities at visit vmin0 + jj; past the
-        // last visit every walk re-reads it (its points lie above EM: pre-pass)
-        auto fetch = [&](int jj, float& t, float2 I[2]) {
-            const int vv = min(jj, niter - 1);
-            t = lds_f32(s_tau + 4u * (uint32_t)(vmin0 + vv));
-            const uint32_t sl = in_lane + (uint32_t)((vv ^ xr) & (LOCK_NB - 1)) * (uint32_t)L::IN_SLOT;
-            constexpr uint32_t WB = 4 * TILE_C * sizeof(T);  // walk w: rows + 4 w
-            I[0] = make_float2(lds_px<T>(sl), lds_px<T>(sl + WB));
-            I[1] = make_float2(lds_px<T>(sl + 2 * WB), lds_px<T>(sl + 3 * WB));
-        };
-
-        wait_upto(vmin0 + 1);
-        float2 plo[2], phi[2], ps[2], pI[2], cq[2], Fp[2], En[2], Iq[2];
-        // ramp superposition: F(E) = Lr + A (E - plo) + sum over the last
-        // LOCK_P ramps of d_s G_s(E); older ramps are retired into the linear part (Lr, A)
-        float2 Lr[2], A[2], slo[2][LOCK_P], sw[2][LOCK_P], sk[2][LOCK_P], sd[2][LOCK_P];
-        float tq;
-        {
-            float t0;
-            fetch(0, t0, pI);
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                plo[p] = poly2(cb[p], f2(t0));  // lo edge / hi edge: fixed order over the tile (pre-pass)
-                phi[p] = POINT ? plo[p] : poly2(cf[p], f2(t0));
-                ps[p] = add2(plo[p], phi[p]);
-                cq[p] = Fp[p] = Lr[p] = A[p] = f2(0.f);
-#pragma unroll
-                for (int u = 0; u < LOCK_P; ++u) {  // empty slots: zero coefficient, finite shape
-                    slo[p][u] = plo[p];
-                    sw[p][u] = f2(1.f);
-                    sk[p][u] = sd[p][u] = f2(0.f);
-                }
-                // first edge: the first above point 0's lo (F = 0 below it); inactive walks never evaluate
-                En[p].x = act[2 * p] ? fmaxf(E0, floorf(plo[p].x) + 1.f) : EM + 1.f;
-                En[p].y = act[2 * p + 1] ? fmaxf(E0, floorf(plo[p].y) + 1.f) : EM + 1.f;
-            }
-            fetch(1, tq, Iq);
-        }
-        const float2 sdir2 = f2(2.f * a.sign * (float)dir);  // c = 2 s dir dI / (sum_{q+1} - sum_q)
-        const int m_ref = a.m_ref;
-        // bits(E + fbias) = 0x4B000000 + e - 1 + RB for edge index e: plane e - 1 mod RB in the low bits
-        const float fbias = 8388608.f + (float)(m_ref - 1 + RB);
-        // planes below the slowest walk's next edge are final; a finished or inactive walk sits at
-        // edge M + 1 (its last point lies above the bins: pre-pass), so it never holds them back
-        auto frontier = [&]() {
-            const float fr = fminf(fminf(En[0].x, En[0].y), fminf(En[1].x, En[1].y));
-            return __reduce_min_sync(0xffffffffu, (int)fr + m_ref) - 1;  // planes < edge - 1
-        };
-        drain(frontier());
-#if DAXM_LOCK_CHECK
-        unsigned viol = 0u;
-#endif
-
-        // iteration jj closes zone jj - 1 of every walk; before its own window a walk's zones lie
-        // below the bins (F offset only), after it above them (no edge left: pre-pass)
-        // blocks of LOCK_P steps so that ramp jj - 1 goes to the static slot (jj - 1) % LOCK_P;
-        // steps past the last visit close no zone (every walk's last point lies above EM)
-        float2 zlo_next[2];
-#pragma unroll 1
-        for (int jb = 1; jb < niter; jb += LOCK_P)
-#pragma unroll
-        for (int u = 0; u < LOCK_P; ++u) {
-            const int jj = jb + u;
-            // point jj (prefetched); refill the ring below the slowest walk; prefetch point jj + 1
-            issue(jj);
-            wait_upto(vmin0 + jj + 1);
-            float2 Eb[2], off[2][LOCK_P];
-            float tn;
-            float2 In[2];
-            fetch(jj + 1, tn, In);
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                const float2 lo = poly2(cb[p], f2(tq)), hi = POINT ? lo : poly2(cf[p], f2(tq));
-                const float2 s = add2(lo, hi);
-                const float2 c = mul2(mul2(sdir2, sub2(pI[p], Iq[p])), rcp2(sub2(s, ps[p])));  // pair jj - 1
-                const float2 w = sub2(phi[p], plo[p]);          // ramp jj - 1 = point jj - 1's edge span
-                const float2 d = sub2(c, cq[p]);                // its coefficient c_{jj-1} - c_{jj-2}
-                // retire ramp jj - 1 - LOCK_P (finished below plo: pre-pass) into the linear part
-                const float2 h = sub2(sub2(plo[p], slo[p][u]), mul2(f2(0.5f), sw[p][u]));
-                Lr[p] = fma2(sd[p][u], h, Lr[p]);
-                A[p] = add2(A[p], sd[p][u]);
-                slo[p][u] = plo[p];
-                sw[p][u] = w;
-                sd[p][u] = d;
-                sk[p][u] = mul2(d, mul2(rcp2(max2(w, f2(1e-30f))), f2(0.5f)));
-#pragma unroll
-                for (int v = 0; v < LOCK_P; ++v) off[p][v] = sub2(plo[p], slo[p][v]);
-                Eb[p] = min2(lo, f2(EM));
-                ps[p] = s;
-                pI[p] = Iq[p];
-                cq[p] = c;
-                Iq[p] = In[p];
-                phi[p] = hi;
-                // (plo moves to lo after the zone's edges; the linear part follows it then)
-                zlo_next[p] = lo;
-            }
-            tq = tn;
-            // ---- edges of zone jj - 1: En .. floor(min(lo_jj, EM)), a warp-uniform trip count
-            uint32_t es[4];
-            float2 x[2], cm[2], fl[2];
-            float kmax = 0.f;
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                es[2 * p] = (uint32_t)__float_as_int(En[p].x + fbias) << 9;  // plane * plane bytes (mod RB)
-                es[2 * p + 1] = (uint32_t)__float_as_int(En[p].y + fbias) << 9;
-                fl[p] = add2(make_float2(floorf(Eb[p].x), floorf(Eb[p].y)), f2(1.f));  // first edge after the zone
-                const float2 cnt = sub2(fl[p], En[p]);  // edges of this zone (exact small integers)
-                kmax = fmaxf(kmax, fmaxf(cnt.x, cnt.y));
-                cm[p] = sub2(cnt, f2(1.f));  // trip k stores iff k <= cnt - 1
-                x[p] = sub2(En[p], plo[p]);   // advanced by +1 per trip (the edge test is on k, exact)
-            }
-            const int K = __reduce_max_sync(0xffffffffu, (int)kmax);
-            float kf = 0.f;
-            DAXM_UNROLL(DAXM_LOCK_KUNROLL)
-            for (int k = 0; k < K; ++k, kf += 1.f) {
-#pragma unroll
+            // iteration jj closes zone jj - 1 of every walk; before its own window a walk's zones lie
+            // below the bins (F offset only), after it above them (no edge left: pre-pass)
+            DAXM_UNROLL(DAXM_LOCK_UNROLL)
+            for (int jj = 1; jj < niter; ++jj) {
+                // point jj (prefetched); refill the ring below the slowest walk; prefetch point jj + 1
+                issue(jj);
+                wait_upto(vmin0 + jj + 1);
+                float2 zlo[2], zw[2], zc[2], zd[2], zg[2], zF0[2], Eb[2];
+                float tn;
+                float2 In[2];
+                fetch(jj + 1, tn, In);
+    #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    float2 F = fma2(A[p], x[p], Lr[p]);
-#pragma unroll
-                    for (int v = 0; v < LOCK_P; ++v) {  // ramp v: d (xs - xc) + d/(2w) xc^2, xs >= 0
-                        const float2 xs = add2(x[p], off[p][v]);
-                        const float2 xc = min2(xs, sw[p][v]);
-                        F = fma2(sd[p][v], sub2(xs, xc), F);
-                        F = fma2(mul2(sk[p][v], xc), xc, F);
+                    // past its window a walk re-reads its last point (lo >= EM, pre-pass): no edges
+                    // remain below EM for it, whatever its zone arithmetic produces
+                    const float2 lo = poly2(cb[p], f2(tq)), hi = POINT ? lo : poly2(cf[p], f2(tq));
+                    const float2 s = add2(lo, hi);
+                    const float2 c = mul2(mul2(sdir2, sub2(pI[p], Iq[p])), rcp2(sub2(s, ps[p])));
+                    const float2 w = sub2(phi[p], plo[p]);
+                    const float2 d = sub2(cq[p], c);
+                    const float2 rw = rcp2(max2(w, f2(1e-30f)));
+                    zlo[p] = plo[p];
+                    zw[p] = w;
+                    zc[p] = c;
+                    zd[p] = d;
+                    zg[p] = mul2(d, mul2(rw, f2(-0.5f)));
+                    zF0[p] = zF[p];
+                    Eb[p] = min2(lo, f2(EM));
+                    // F at the next zone's start: F(lo) = F(plo) + c (lo - plo) + w d / 2
+                    zF[p] = fma2(f2(0.5f), mul2(w, d), fma2(c, sub2(lo, plo[p]), zF[p]));
+                    plo[p] = lo;
+                    phi[p] = hi;
+                    ps[p] = s;
+                    pI[p] = Iq[p];
+                    cq[p] = c;
+                    Iq[p] = In[p];
+                }
+                tq = tn;
+                // ---- edges of zone jj - 1: En .. floor(min(lo_jj, EM)), a warp-uniform trip count
+                uint32_t es[4];
+                float2 x[2], cm[2], fl[2];
+                float kmax = 0.f;
+    #pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    es[2 * p] = (uint32_t)__float_as_int(En[p].x + fbias) << 9;  // plane * plane bytes (mod RB)
+                    es[2 * p + 1] = (uint32_t)__float_as_int(En[p].y + fbias) << 9;
+                    fl[p] = add2(make_float2(floorf(Eb[p].x), floorf(Eb[p].y)), f2(1.f));  // first edge after the zone
+                    const float2 cnt = sub2(fl[p], En[p]);  // edges of this zone (exact small integers)
+                    kmax = fmaxf(kmax, fmaxf(cnt.x, cnt.y));
+                    cm[p] = sub2(cnt, f2(1.f));  // trip k stores iff k <= cnt - 1
+                    x[p] = sub2(En[p], zlo[p]);   // advanced by +1 per trip (the edge test is on k, exact)
+                }
+                const int K = __reduce_max_sync(0xffffffffu, (int)kmax);
+                float kf = 0.f;
+                DAXM_UNROLL(DAXM_LOCK_KUNROLL)
+                for (int k = 0; k < K; ++k, kf += 1.f) {
+    #pragma unroll
+                    for (int p = 0; p < 2; ++p) {
+                        const float2 xc = min2(x[p], zw[p]);
+                        const float2 F = fma2(xc, fma2(zg[p], xc, zd[p]), fma2(zc[p], x[p], zF0[p]));
+                        const float2 o = sub2(F, Fp[p]);
+                        // predicated store + Fp update (setp inside the asm: no branch, no address remat)
+                        edge_store(out_lane + (es[2 * p] & (uint32_t)((RB - 1) << 9)) + (2 * p) * 128, o.x, F.x, kf,
+                                   cm[p].x, Fp[p].x);
+                        edge_store(out_lane + (es[2 * p + 1] & (uint32_t)((RB - 1) << 9)) + (2 * p + 1) * 128, o.y, F.y,
+                                   kf, cm[p].y, Fp[p].y);
+                        x[p] = add2(x[p], f2(1.f));
+                        es[2 * p] += 512u;
+                        es[2 * p + 1] += 512u;
                     }
-                    const float2 o = sub2(F, Fp[p]);
-                    // predicated store + Fp update (setp inside the asm: no branch, no address remat)
-                    edge_store(out_lane + (es[2 * p] & (uint32_t)((RB - 1) << 9)) + (2 * p) * 128, o.x, F.x, kf,
-                               cm[p].x, Fp[p].x);
-                    edge_store(out_lane + (es[2 * p + 1] & (uint32_t)((RB - 1) << 9)) + (2 * p + 1) * 128, o.y, F.y,
-                               kf, cm[p].y, Fp[p].y);
-                    x[p] = add2(x[p], f2(1.f));
-                    es[2 * p] += 512u;
-                    es[2 * p + 1] += 512u;
                 }
+                // next edge of each walk (edges <= Eb evaluated or, past the window, constant)
+    #pragma unroll
+                for (int p = 0; p < 2; ++p) En[p] = max2(En[p], fl[p]);
+    #if DAXM_LOCK_CHECK
+                {   // planes written this iteration must lie below done_p + RB (pre-pass guarantee)
+                    const float lim = (float)(done_p + RB - m_ref + 1);  // edge bound: e - 1 < done_p + RB
+    #pragma unroll
+                    for (int p = 0; p < 2; ++p) {
+                        if (cm[p].x >= 0.f && En[p].x - 1.f >= lim) viol = 1u;  // highest edge stored this iteration
+                        if (cm[p].y >= 0.f && En[p].y - 1.f >= lim) viol = 1u;
+                    }
+                }
+    #endif
+                drain(frontier());
             }
-            // next edge of each walk (edges <= Eb evaluated or, past the window, constant)
-#pragma unroll
-            for (int p = 0; p < 2; ++p) {
-                En[p] = max2(En[p], fl[p]);
-                Lr[p] = fma2(A[p], sub2(zlo_next[p], plo[p]), Lr[p]);  // linear part's origin -> lo_jj
-                plo[p] = zlo_next[p];
-            }
-#if DAXM_LOCK_CHECK
-            {   // planes written this iteration must lie below done_p + RB (pre-pass guarantee)
-                const float lim = (float)(done_p + RB - m_ref + 1);  // edge bound: e - 1 < done_p + RB
-#pragma unroll
+    #if DAXM_LOCK_CHECK
+            if (viol && a.lock_err) atomicAdd(a.lock_err, 1u);
+    #endif
+        } else {
+            float2 plo[2], phi[2], ps[2], pI[2], cq[2], Fp[2], En[2], Iq[2];
+            // ramp superposition: F(E) = Lr + A (E - plo) + sum over the last
+            // LOCK_P ramps of d_s G_s(E); older ramps are retired into the linear part (Lr, A)
+            float2 Lr[2], A[2], slo[2][LOCK_P], sw[2][LOCK_P], sk[2][LOCK_P], sd[2][LOCK_P];
+            float tq;
+            {
+                float t0;
+                fetch(0, t0, pI);
+    #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    if (cm[p].x >= 0.f && En[p].x - 1.f >= lim) viol = 1u;  // highest edge stored this iteration
-                    if (cm[p].y >= 0.f && En[p].y - 1.f >= lim) viol = 1u;
+                    plo[p] = poly2(cb[p], f2(t0));  // lo edge / hi edge: fixed order over the tile (pre-pass)
+                    phi[p] = POINT ? plo[p] : poly2(cf[p], f2(t0));
+                    ps[p] = add2(plo[p], phi[p]);
+                    cq[p] = Fp[p] = Lr[p] = A[p] = f2(0.f);
+    #pragma unroll
+                    for (int u = 0; u < LOCK_P; ++u) {  // empty slots: zero coefficient, finite shape
+                        slo[p][u] = plo[p];
+                        sw[p][u] = f2(1.f);
+                        sk[p][u] = sd[p][u] = f2(0.f);
+                    }
+                    // first edge: the first above point 0's lo (F = 0 below it); inactive walks never evaluate
+                    En[p].x = act[2 * p] ? fmaxf(E0, floorf(plo[p].x) + 1.f) : EM + 1.f;
+                    En[p].y = act[2 * p + 1] ? fmaxf(E0, floorf(plo[p].y) + 1.f) : EM + 1.f;
                 }
+                fetch(1, tq, Iq);
             }
-#endif
+            const float2 sdir2 = f2(2.f * a.sign * (float)dir);  // c = 2 s dir dI / (sum_{q+1} - sum_q)
+            const int m_ref = a.m_ref;
+            // bits(E + fbias) = 0x4B000000 + e - 1 + RB for edge index e: plane e - 1 mod RB in the low bits
+            const float fbias = 8388608.f + (float)(m_ref - 1 + RB);
+            // planes below the slowest walk's next edge are final; a finished or inactive walk sits at
+            // edge M + 1 (its last point lies above the bins: pre-pass), so it never holds them back
+            auto frontier = [&]() {
+                const float fr = fminf(fminf(En[0].x, En[0].y), fminf(En[1].x, En[1].y));
+                return __reduce_min_sync(0xffffffffu, (int)fr + m_ref) - 1;  // planes < edge - 1
+            };
             drain(frontier());
+    #if DAXM_LOCK_CHECK
+            unsigned viol = 0u;
+    #endif
+
+            // iteration jj closes zone jj - 1 of every walk; before its own window a walk's zones lie
+            // below the bins (F offset only), after it above them (no edge left: pre-pass)
+            // blocks of LOCK_P steps so that ramp jj - 1 goes to the static slot (jj - 1) % LOCK_P;
+            // steps past the last visit close no zone (every walk's last point lies above EM)
+            float2 zlo_next[2];
+    #pragma unroll 1
+            for (int jb = 1; jb < niter; jb += LOCK_P)
+    #pragma unroll
+            for (int u = 0; u < LOCK_P; ++u) {
+                const int jj = jb + u;
+                // point jj (prefetched); refill the ring below the slowest walk; prefetch point jj + 1
+                issue(jj);
+                wait_upto(vmin0 + jj + 1);
+                float2 Eb[2], off[2][LOCK_P];
+                float tn;
+                float2 In[2];
+                fetch(jj + 1, tn, In);
+    #pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const float2 lo = poly2(cb[p], f2(tq)), hi = POINT ? lo : poly2(cf[p], f2(tq));
+                    const float2 s = add2(lo, hi);
+                    const float2 c = mul2(mul2(sdir2, sub2(pI[p], Iq[p])), rcp2(sub2(s, ps[p])));  // pair jj - 1
+                    const float2 w = sub2(phi[p], plo[p]);          // ramp jj - 1 = point jj - 1's edge span
+                    const float2 d = sub2(c, cq[p]);                // its coefficient c_{jj-1} - c_{jj-2}
+                    // retire ramp jj - 1 - LOCK_P (finished below plo: pre-pass) into the linear part
+                    const float2 h = sub2(sub2(plo[p], slo[p][u]), mul2(f2(0.5f), sw[p][u]));
+                    Lr[p] = fma2(sd[p][u], h, Lr[p]);
+                    A[p] = add2(A[p], sd[p][u]);
+                    slo[p][u] = plo[p];
+                    sw[p][u] = w;
+                    sd[p][u] = d;
+                    sk[p][u] = mul2(d, mul2(rcp2(max2(w, f2(1e-30f))), f2(0.5f)));
+    #pragma unroll
+                    for (int v = 0; v < LOCK_P; ++v) off[p][v] = sub2(plo[p], slo[p][v]);
+                    Eb[p] = min2(lo, f2(EM));
+                    ps[p] = s;
+                    pI[p] = Iq[p];
+                    cq[p] = c;
+                    Iq[p] = In[p];
+                    phi[p] = hi;
+                    // (plo moves to lo after the zone's edges; the linear part follows it then)
+                    zlo_next[p] = lo;
+                }
+                tq = tn;
+                // ---- edges of zone jj - 1: En .. floor(min(lo_jj, EM)), a warp-uniform trip count
+                uint32_t es[4];
+                float2 x[2], cm[2], fl[2];
+                float kmax = 0.f;
+    #pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    es[2 * p] = (uint32_t)__float_as_int(En[p].x + fbias) << 9;  // plane * plane bytes (mod RB)
+                    es[2 * p + 1] = (uint32_t)__float_as_int(En[p].y + fbias) << 9;
+                    fl[p] = add2(make_float2(floorf(Eb[p].x), floorf(Eb[p].y)), f2(1.f));  // first edge after the zone
+                    const float2 cnt = sub2(fl[p], En[p]);  // edges of this zone (exact small integers)
+                    kmax = fmaxf(kmax, fmaxf(cnt.x, cnt.y));
+                    cm[p] = sub2(cnt, f2(1.f));  // trip k stores iff k <= cnt - 1
+                    x[p] = sub2(En[p], plo[p]);   // advanced by +1 per trip (the edge test is on k, exact)
+                }
+                const int K = __reduce_max_sync(0xffffffffu, (int)kmax);
+                float kf = 0.f;
+                DAXM_UNROLL(DAXM_LOCK_KUNROLL)
+                for (int k = 0; k < K; ++k, kf += 1.f) {
+    #pragma unroll
+                    for (int p = 0; p < 2; ++p) {
+                        float2 F = fma2(A[p], x[p], Lr[p]);
+    #pragma unroll
+                        for (int v = 0; v < LOCK_P; ++v) {  // ramp v: d (xs - xc) + d/(2w) xc^2, xs >= 0
+                            const float2 xs = add2(x[p], off[p][v]);
+                            const float2 xc = min2(xs, sw[p][v]);
+                            F = fma2(sd[p][v], sub2(xs, xc), F);
+                            F = fma2(mul2(sk[p][v], xc), xc, F);
+                        }
+                        const float2 o = sub2(F, Fp[p]);
+                        // predicated store + Fp update (setp inside the asm: no branch, no address remat)
+                        edge_store(out_lane + (es[2 * p] & (uint32_t)((RB - 1) << 9)) + (2 * p) * 128, o.x, F.x, kf,
+                                   cm[p].x, Fp[p].x);
+                        edge_store(out_lane + (es[2 * p + 1] & (uint32_t)((RB - 1) << 9)) + (2 * p + 1) * 128, o.y, F.y,
+                                   kf, cm[p].y, Fp[p].y);
+                        x[p] = add2(x[p], f2(1.f));
+                        es[2 * p] += 512u;
+                        es[2 * p + 1] += 512u;
+                    }
+                }
+                // next edge of each walk (edges <= Eb evaluated or, past the window, constant)
+    #pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    En[p] = max2(En[p], fl[p]);
+                    Lr[p] = fma2(A[p], sub2(zlo_next[p], plo[p]), Lr[p]);  // linear part's origin -> lo_jj
+                    plo[p] = zlo_next[p];
+                }
+    #if DAXM_LOCK_CHECK
+                {   // planes written this iteration must lie below done_p + RB (pre-pass guarantee)
+                    const float lim = (float)(done_p + RB - m_ref + 1);  // edge bound: e - 1 < done_p + RB
+    #pragma unroll
+                    for (int p = 0; p < 2; ++p) {
+                        if (cm[p].x >= 0.f && En[p].x - 1.f >= lim) viol = 1u;  // highest edge stored this iteration
+                        if (cm[p].y >= 0.f && En[p].y - 1.f >= lim) viol = 1u;
+                    }
+                }
+    #endif
+                drain(frontier());
+            }
+    #if DAXM_LOCK_CHECK
+            if (viol && a.lock_err) atomicAdd(a.lock_err, 1u);
+    #endif
         }
-#if DAXM_LOCK_CHECK
-        if (viol && a.lock_err) atomicAdd(a.lock_err, 1u);
-#endif
     }
     drain(M);
     // every issued input load has been waited for (wait_upto reached vend), so the CTA may exit
 }
-
 // ------------------------------------------------------------------ pre-pass
 // Replays, per tile and lock warp, the kernel's warp-locked walks with its own fp32 arithmetic
 // (lock_poly, fminf, floorf) and classifies the tile:
@@ -823,7 +639,7 @@ __global__ void __launch_bounds__(256) lock_prepass_kernel(DepositArgs a, TileIn
         s_back_lo = s_front_lo = 1;
     }
     __syncthreads();
-    // overlapping tiles -> deposit_lock_ov (ramp superposition); finite pixels only
+    // overlapping tiles -> deposit_lock<..., OV = true> (ramp superposition); finite pixels only
     const bool ov = ti.separated == MODE_OVERLAP && a.lock_ov_enabled && !a.point_mode;
     const bool eligible = (ti.separated == MODE_SEPARATED || ov) && row0 >= a.row_begin && ti.k_hi >= ti.k_lo &&
                           a.table == nullptr && (ti.k_hi - ti.k_lo + 1) <= MAX_FAST_NV;
@@ -923,7 +739,7 @@ __global__ void __launch_bounds__(256) lock_prepass_kernel(DepositArgs a, TileIn
 template <typename T, bool POINT, int RB, bool OV>
 cudaError_t launch_lock_rb(const CUtensorMap* in_map, float* out, const DepositArgs& a, int n_tiles, cudaStream_t st) {
     const size_t sm = LockSmem<T, RB>::bytes(a.max_nv);
-    auto kern = OV ? deposit_lock_ov<T, POINT, RB> : deposit_lock<T, POINT, RB>;
+    auto kern = deposit_lock<T, POINT, RB, OV>;
     static std::atomic<unsigned long long> attr_done{0};  // per device (attributes are per device)
     cudaError_t ea = once_per_device(attr_done, [&]() {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

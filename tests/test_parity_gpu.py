@@ -387,7 +387,7 @@ def test_benchmark_configs_take_the_fast_path(daxm, name):
 
 def test_c5_overlapping_tiles_use_the_ramp_superposition_kernel(daxm):
     """C5's finest bins make the pixel-edge span exceed the per-step sweep on the detector's
-    shallow side: those tiles run the step-locked ramp-superposition kernel (deposit_lock_ov);
+    shallow side: those tiles run the step-locked ramp-superposition kernel (deposit_lock, OV);
     only tiles mixing both regimes fall back to the general kernel."""
     cfg = synth.get_config("C5")
     with daxm.create(synth.geometry(cfg), device=0) as plan:
@@ -416,7 +416,7 @@ def test_overlap_regime_dual_walk_fallback(daxm, dtype, monkeypatch):
 @pytest.mark.parametrize("dtype", ["u16", "f32"])
 def test_overlap_regime_parity(daxm, dtype):
     """Many fine wire steps on a coarse-pitch detector: every pixel's edge span (0.68 um) exceeds
-    the per-step sweep (0.24-0.6 um) -> all tiles overlapping, all in deposit_lock_ov."""
+    the per-step sweep (0.24-0.6 um) -> all tiles overlapping, all in deposit_lock (OV)."""
     g = synth.geometry("C2", n_rows=96, n_cols=64)
     g["wire_xyz"] = synth.wire_positions(1601, t_range=(40.0, 1040.0))
     g["depth_res"] = 0.5
