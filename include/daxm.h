@@ -25,6 +25,10 @@
  *   daxm_reconstruct_host  the same from/to HOST buffers (copies included;
  *                      out of core under a device-memory budget,
  *                      daxm_set_host_budget / daxm_host_ring_info)
+ *   daxm_reconstruct_profile  daxm_reconstruct + the depth profile (fused)
+ *   daxm_set_cutoff / daxm_select_cutoff[_sharded]  intensity cutoff, pixel percentage
+ *   daxm_set_step_weights  per-step intensity normalisation
+ *   daxm_depth_profile  per-bin totals of an output
  *   daxm_plan_info / daxm_plan_stats / daxm_last_error / daxm_status_string
  *   daxm_destroy
  */
