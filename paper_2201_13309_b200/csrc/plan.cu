@@ -33,6 +33,10 @@
 
 using namespace daxm;
 
+#ifndef DAXM_HOST_BANDS
+#define DAXM_HOST_BANDS 16  // row bands of the in-core host pipeline (copy/compute overlap granularity)
+#endif
+
 struct daxm_plan {
     int device = 0;
     // both-edges mode (reading R16): the parent holds one plan per edge and runs both per call
@@ -1913,7 +1917,7 @@ daxm_status daxm_reconstruct_host(daxm_plan* p, const void* h_stack, daxm_dtype 
             e = cudaStreamCreateWithFlags(&p->st_out, cudaStreamNonBlocking);
             if (e != cudaSuccess) goto fail_cuda;
         }
-        const int n_bands = p->n_tr < 8 ? p->n_tr : 8;
+        const int n_bands = p->n_tr < DAXM_HOST_BANDS ? p->n_tr : DAXM_HOST_BANDS;
         while ((int)p->ev.size() < 2 * n_bands) {
             cudaEvent_t ev;
             e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
