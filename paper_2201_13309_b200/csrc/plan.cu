@@ -34,7 +34,7 @@
 using namespace daxm;
 
 #ifndef DAXM_HOST_BANDS
-#define DAXM_HOST_BANDS 16  // row bands of the in-core host pipeline (copy/compute overlap granularity)
+#define DAXM_HOST_BANDS 32  // row bands of the in-core host pipeline (copy/compute overlap granularity)
 #endif
 
 struct daxm_plan {
@@ -1507,16 +1507,15 @@ static daxm_status encode_maps(daxm_plan* p, const void* d_stack, int dt, float*
 
 // Row-segment path: one launch per admission class (ring of 16 / 32 planes) plus the general kernel
 // for the row tiles not admitted, forked onto the plan's class streams and joined back into st.
-// tr_begin / tr_end (deposit-tile rows, host pipeline) select the row tiles of those rows.
-static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_out, cudaStream_t st, int tr_begin,
-                           int tr_end, double* d_profile = nullptr) {
+// g0 / g1 (global rows of a host-pipeline band, g1 < 0: all) select the row tiles of those rows.
+static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_out, cudaStream_t st, int g0,
+                           int g1, double* d_profile = nullptr) {
     daxm_status s = encode_maps(p, d_stack, dt, d_out);
     if (s != DAXM_OK) return s;
     int ra = 0, rb = p->n_rr;
-    if (tr_end >= 0) {
+    if (g1 >= 0) {  // global rows [g0, g1) of a host-pipeline band
         // a row tile straddling a band boundary (odd band start) goes with the later band, whose rows
         // are copied after the earlier band's
-        const int g0 = (p->tr0 + tr_begin) * TILE_R, g1 = (p->tr0 + tr_end) * TILE_R;
         ra = g0 <= p->row_org ? 0 : (g0 - p->row_org) / RW_ROWS;
         rb = g1 >= p->g.row_end ? p->n_rr : std::max(0, (g1 - p->row_org) / RW_ROWS);
     }
@@ -1583,11 +1582,19 @@ static daxm_status run_row(daxm_plan* p, const void* d_stack, int dt, float* d_o
     return DAXM_OK;
 }
 
+// Whether daxm_reconstruct runs the row kernel for this plan (both-edges: both children do).
+static bool uses_row_path(const daxm_plan* p, int dt) {
+    if (p->child[0]) return uses_row_path(p->child[0], dt) && uses_row_path(p->child[1], dt);
+    return fast_possible(p, dt) && p->d_w == nullptr && p->row_ok && getenv("DAXM_NO_ROW") == nullptr;
+}
+
+// Band [g0, g1) of global rows (g1 < 0: the whole plan); the deposit-tile path needs band bounds
+// on multiples of TILE_R (or the plan's ends), the row path on multiples of RW_ROWS.
 static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float* d_out, cudaStream_t st,
-                               int tr_begin = 0, int tr_end = -1) {
+                               int g0 = 0, int g1 = -1) {
     if (p->child[0]) {  // both-edges mode: the leading child stores, the trailing child adds
         for (int e = 0; e < 2; ++e) {
-            daxm_status s = run_deposit(p->child[e], d_stack, dt, d_out, st, tr_begin, tr_end);
+            daxm_status s = run_deposit(p->child[e], d_stack, dt, d_out, st, g0, g1);
             if (s != DAXM_OK) {
                 p->err = p->child[e]->err;
                 return s;
@@ -1598,7 +1605,7 @@ static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float*
     // (per-step weights: the general kernel normalises each intensity, the fast kernels do not)
     bool fast = fast_possible(p, dt) && p->d_w == nullptr;
     if (fast && p->row_ok && getenv("DAXM_NO_ROW") == nullptr)
-        return run_row(p, d_stack, dt, d_out, st, tr_begin, tr_end < 0 ? -1 : tr_end);
+        return run_row(p, d_stack, dt, d_out, st, g0, g1);
     // both-edges children off the row path: the general kernel alone clamps and accumulates
     if (p->is_child) fast = false;
     if (fast) {
@@ -1606,8 +1613,8 @@ static daxm_status run_deposit(daxm_plan* p, const void* d_stack, int dt, float*
         if (s != DAXM_OK) return s;
     }
     DepositArgs a = make_args(p, dt);
-    a.tr_begin = tr_begin;
-    a.tr_end = tr_end < 0 ? p->n_tr : tr_end;
+    a.tr_begin = g1 < 0 ? 0 : std::max(0, g0 / TILE_R - p->tr0);
+    a.tr_end = g1 < 0 ? p->n_tr : std::min(p->n_tr, (g1 + TILE_R - 1) / TILE_R - p->tr0);
     a.stack = d_stack;
     cudaError_t e = cudaSuccess;
     const bool live = a.use_cutoff && !p->is_child && getenv("DAXM_NO_TILE_LIVE") == nullptr;
@@ -1917,7 +1924,13 @@ daxm_status daxm_reconstruct_host(daxm_plan* p, const void* h_stack, daxm_dtype 
             e = cudaStreamCreateWithFlags(&p->st_out, cudaStreamNonBlocking);
             if (e != cudaSuccess) goto fail_cuda;
         }
-        const int n_bands = p->n_tr < DAXM_HOST_BANDS ? p->n_tr : DAXM_HOST_BANDS;
+        // bands of Q-row quanta: on the row path 64 rows counted from the plan's first row (its row
+        // tiles start there, so no tile straddles two bands), else the deposit tiles' global 128
+        const bool rowp = uses_row_path(p, (int)dt);
+        const int Q = rowp ? 64 : TILE_R;
+        const int base = rowp ? p->g.row_begin : 0;
+        const int q0 = (p->g.row_begin - base) / Q, nq = (p->g.row_end - base + Q - 1) / Q - q0;
+        const int n_bands = nq < DAXM_HOST_BANDS ? nq : DAXM_HOST_BANDS;
         while ((int)p->ev.size() < 2 * n_bands) {
             cudaEvent_t ev;
             e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
@@ -1932,8 +1945,9 @@ daxm_status daxm_reconstruct_host(daxm_plan* p, const void* h_stack, daxm_dtype 
         const size_t es = dt == DAXM_U16 ? 2 : 4;
         const size_t row_in = (size_t)p->C * es, row_out = (size_t)p->C * sizeof(float);
         for (int b = 0; b < n_bands; ++b) {
-            const int t0 = b * p->n_tr / n_bands, t1 = (b + 1) * p->n_tr / n_bands;
-            int r0 = (p->tr0 + t0) * TILE_R - p->g.row_begin, r1 = (p->tr0 + t1) * TILE_R - p->g.row_begin;
+            const int g0 = std::max(p->g.row_begin, base + (q0 + b * nq / n_bands) * Q);
+            const int g1 = std::min(p->g.row_end, base + (q0 + (b + 1) * nq / n_bands) * Q);
+            int r0 = g0 - p->g.row_begin, r1 = g1 - p->g.row_begin;
             r0 = r0 < 0 ? 0 : r0;
             r1 = r1 > p->rows ? p->rows : r1;
             if (r1 <= r0) continue;
@@ -1947,7 +1961,7 @@ daxm_status daxm_reconstruct_host(daxm_plan* p, const void* h_stack, daxm_dtype 
             e = cudaStreamWaitEvent(st, p->ev[2 * b], 0);
             if (e != cudaSuccess) goto fail_cuda;
             {
-                daxm_status s = run_deposit(p, p->d_stack_buf, (int)dt, p->d_out_buf, st, t0, t1);
+                daxm_status s = run_deposit(p, p->d_stack_buf, (int)dt, p->d_out_buf, st, g0, g1);
                 if (s != DAXM_OK) return s;
             }
             e = cudaEventRecord(p->ev[2 * b + 1], st);

@@ -434,7 +434,7 @@ def test_host_path_pipelined_bands(daxm):
     import torch
     g = synth.geometry("C3")
     host = synth.stack_numpy(synth.make_maps("C3"), "u16", noise=True)
-    for rows in [(0, 1024), (70, 901)]:
+    for rows in [(0, 1024), (70, 901), (71, 899)]:  # (an odd start: row tiles start at row 71)
         band = np.ascontiguousarray(host[:, rows[0]:rows[1]])
         with daxm.create(g, device=0, rows=rows) as plan:
             dev = plan.reconstruct(torch.from_numpy(band).cuda())
