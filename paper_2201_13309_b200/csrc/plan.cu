@@ -1711,8 +1711,12 @@ static daxm_status host_ring(daxm_plan* p, const void* h_stack, daxm_dtype dt, f
     const size_t row_in = (size_t)p->C * es, row_out = (size_t)p->C * sizeof(float);
     const size_t per_row = row_in * p->S + row_out * p->M;  // one detector row of one slot
     const uint64_t rows_fit = p->host_budget / (2 * per_row);
-    const int B = (int)std::min<uint64_t>(rows_fit / TILE_R, (uint64_t)(p->g.n_rows / TILE_R + 1)) * TILE_R;
-    if (B < TILE_R)
+    // the largest band whose two slots fit, but at most 1/16 of the rows (a deeper pipeline: the first
+    // band's copy in and the last one's copy out are not overlapped)
+    const uint64_t b_pipe = std::max<uint64_t>(1, (uint64_t)p->rows / (16 * TILE_R));
+    const int B = (int)std::min<uint64_t>(std::min<uint64_t>(rows_fit / TILE_R, b_pipe),
+                                          (uint64_t)(p->g.n_rows / TILE_R + 1)) * TILE_R;
+    if (rows_fit < (uint64_t)TILE_R)
         return fail(p, DAXM_ERR_OUT_OF_MEMORY,
                     "host budget %llu bytes holds no two %d-row ring slots (%zu bytes per row and slot)",
                     (unsigned long long)p->host_budget, TILE_R, per_row);
