@@ -1,35 +1,33 @@
-// deposit_row.cu -- the production gather deposit for pixels in
-// the separated-span regime, and the pre-pass replay that admits a row tile to it.
+// deposit_row.cu -- the production gather deposit and the pre-pass
+// replay that admits a row tile to it.
 //
 // What is computed: per pixel, with the step pairs visited in the order their
 // trapezoids move deeper and c_q = dI_q / A_q, the intensity deposited below bin edge E is,
 // inside zone q = [lo_q, lo_{q+1}),
 //     F(E) = F(lo_q) + c_q x + xc (d_q + g_q xc),  x = E - lo_q, xc = min(x, w_q),
 //     d_q = c_{q-1} - c_q,  g_q = -d_q / (2 w_q),  w_q = hi_q - lo_q,
-// and bin m = [E_m, E_{m+1}) receives F(E_{m+1}) - F(E_m): the trapezoid overlaps of P:L320-331
-// (device_depth_resolve_pixel / device_get_trapezoid_height) summed over the pairs
-// (P:L332-334), one owner per (bin, pixel), no atomics.  dI_q = s (I_q - I_{q+1})
-// (readings R1, R2) is formed from the streamed planes.
+// (separated spans; the general-span variant keeps pairs v, v-1, v-2 open) and bin m = [E_m, E_{m+1})
+// receives F(E_{m+1}) - F(E_m): the trapezoid overlaps of P:L320-331 (device_depth_resolve_pixel /
+// device_get_trapezoid_height) summed over the pairs, one owner per (bin,
+// pixel), no atomics.  dI_q = s (I_q - I_{q+1}) (readings R1, R2) is formed
+// from the streamed planes.
 //
-// Schedule.  One warp = one row tile: RW_ROWS detector rows x RW_COLS columns.  Lane l owns
-// columns col0 + l + 32 p (p = 0, 1) of both rows: two walk pairs (rows 0 / 1 of one column,
-// packed fp32x2).  A pair advances one wire step (point) per iteration: it closes the zone its new
-// point ends and evaluates that zone's bin edges in a warp-uniform, fully unrolled predicated loop
-// (at most RW_KT edges).  Different columns sit at different depths for the same step
-// (0.68 bins per column at C4), so each pair starts at its own window and keeps its own visit
-// index; a pair whose walks are more than RW_LEAD bins ahead of the slowest walk of the warp waits
-// (its state is untouched), which keeps all 128 walks of the warp within a few bins of each other.
-// Pausing never changes a walk's arithmetic, only when it happens, and the schedule depends on
-// geometry alone (inactive walks keep advancing, they just store nothing), so an active walk's
-// output is bit-identical whatever the cutoff.
+// Schedule.  One warp = one row tile of 2 detector rows x 64 columns; lane l owns two adjacent
+// columns of one column half (both rows): two walk pairs packed fp32x2.  All lanes advance one visit
+// (wire step) per iteration in lock step, each from its own middle-aligned start, so the 128 walks
+// of a warp stay within a few bins of each other; a point closes the zone of each walk and that
+// zone's bin edges receive F through 3, 4 (+ a rare 5th) or 5 (+ a rare 6th) unrolled predicated
+// stores (edge-trip class of the tile).  The schedule depends on geometry alone (inactive walks keep
+// advancing, they just store nothing), so an active walk's output is bit-identical whatever the cutoff.
 //
-//   input : TMA loads of [RW_G steps][2 rows][64 cols] (128-byte rows) into an RW_NB-slot ring, one
-//           mbarrier per group; lane 0 refills the slots every pair has read past.
-//   output: a ring of RB staged planes [2][64] fp32 (+ RW_KT - 1 overflow planes, so that the
-//           unrolled edge stores use immediate offsets); once the slowest walk has passed a batch
-//           of RW_PB planes, lane 0 writes the batch with one TMA store of a [RW_PB][2][64] box
-//           (256-byte rows: the pattern that reaches the copy ceiling, profiles/r02b_membench.md);
-//           its slots are zeroed at the next drain, after the store has read them.
+//   input : per column half, TMA loads of [4 steps][2 rows][32 cols] boxes into a 24-slot ring (32
+//           for tiles whose lanes spread wider), one mbarrier per group; lane 0 refills the slots
+//           every lane has read past, once per four iterations.
+//   output: F staging -- a ring of RB planes [2][64] fp32 (+ trips - 1 overflow planes, so that the
+//           unrolled edge stores use immediate offsets) holds F at each bin edge; once the slowest
+//           walk has passed edge P + 1 every lane subtracts its 16 bytes of edges P and P + 1 and
+//           writes plane P with one st.global.cs.v4 (the warp writes two 256-byte rows: the pattern
+//           that reaches the copy ceiling, profiles/r02b_membench.md).
 // The pre-pass (row_admit_kernel) replays every warp's schedule with the kernel's own fp32
 // arithmetic and admits a tile only if the output ring, the unrolled edge loop and the input ring
 // provably suffice; the rest goes to the general kernel.
