@@ -165,12 +165,13 @@ constexpr int lock_need_max(int rb) { return rb; }
 static_assert(LOCK_NB % LOCK_G == 0 && (LOCK_NB / LOCK_G & (LOCK_NB / LOCK_G - 1)) == 0, "lock input ring shape");
 
 // ---- Row-segment deposit kernel (deposit_row.cu), the production path.
-// One warp = one "row tile" of RW_ROWS detector rows x RW_COLS columns, aligned to global rows
-// and columns; lane l owns columns col0 + l + 32 h (h < RW_COLS / 32) of all RW_ROWS rows: four
-// pixel walks, packed in two pairs (two rows of one column).  Output planes leave as TMA stores of
-// [RW_PB planes][RW_ROWS][RW_COLS] boxes (256-byte rows), the stack arrives as TMA loads of
-// [RW_G steps][RW_ROWS][RW_COLS] boxes (128-byte rows for u16): the store geometry that reaches
-// the copy ceiling (profiles/r02b_membench.md), where the round-1 16 x 8 warp block could not.
+// One warp = one "row tile" of RW_ROWS detector rows x RW_COLS columns, aligned to the band's first
+// row and to global columns; lane l owns two adjacent columns of one column half, both rows: four
+// pixel walks, packed in two pairs (two rows of one column).  Output planes leave as two 256-byte
+// rows per warp (st.global.cs.v4 per lane; tiles without a change: TMA zero stores of
+// [RW_PB planes][RW_ROWS][RW_COLS] boxes), the stack arrives as TMA loads of [RW_G steps][RW_ROWS]
+// [32 cols] boxes per column half: the store geometry that reaches the copy ceiling
+// (profiles/r02b_membench.md), where the round-1 16 x 8 warp block could not.
 #ifndef DAXM_RW_ROWS
 #define DAXM_RW_ROWS 2
 #endif
@@ -188,7 +189,7 @@ constexpr int RW_G = 4;             // wire steps per TMA load box
 #ifndef DAXM_RW_PB
 #define DAXM_RW_PB 4
 #endif
-constexpr int RW_PB = DAXM_RW_PB;   // output planes per TMA store box
+constexpr int RW_PB = DAXM_RW_PB;   // planes per TMA zero-store box (tiles without a change)
 constexpr int RW_EXT = 16;          // steps a row tile's range extends below its windows (lock-step starts)
 constexpr int RW_KT = DAXM_RW_KT;   // max bin edges one walk evaluates per iteration (unrolled trips)
 constexpr int RW_RB_SMALL = 16, RW_RB_LARGE = 32;  // output ring planes (+ RW_KT - 1 overflow planes)
